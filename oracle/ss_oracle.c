@@ -1,0 +1,324 @@
+/*
+ * ss_oracle.c — plain, slow, obviously correct CPU oracle for ScaleSearch
+ * NVFP4 quantization (arxiv 2605.12464, Algorithm 1).
+ *
+ * TEST INFRASTRUCTURE ONLY (see ss_oracle.h).  It shares no code with the
+ * CUDA path and is never linked into the product.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC
+ * (x86-64 SSE: every float operation below is a single IEEE-754 binary32
+ * operation rounded to nearest-even; FMAs appear only where fmaf() is
+ * written, as the arithmetic contract in DESIGN.md §3 (R7, R8, R12) says).
+ *
+ * Style: scalar loops, rounding by enumerating the format's values and
+ * taking the nearest (ties to the even code), no bit tricks, no tables
+ * shared with anything else.  Each step cites the paper passage it follows.
+ */
+#include "ss_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---------------------------------------------------------------------- */
+/* E2M1: R_E2M1 = {0, +-0.5, +-1, +-1.5, +-2, +-3, +-4, +-6}.  */
+/* Magnitude code k = (exponent bits << 1) | mantissa bit, sign in bit 3.  */
+/* ---------------------------------------------------------------------- */
+static const double E2M1_MAGNITUDE[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+
+double so_e2m1_value(int nibble) {
+  double v = E2M1_MAGNITUDE[nibble & 7];
+  return (nibble & 8) ? -v : v;
+}
+
+/* round_E2M1 ("ordinary nearest-neighbor rounding"): the
+ * magnitude nearest |t|, ties to the even code (R10); |t| above the largest
+ * value saturates to 6 (satfinite, R10); the sign bit is copied from t, so a
+ * negative t that rounds to 0 gives nibble 0x8 (R11). */
+int so_e2m1_encode(float t) {
+  int sign = signbit(t) ? 8 : 0;
+  double a = fabs((double)t);
+  if (a > 6.0) return sign | 7; /* nearest value of the set is 6 */
+  /* For a <= 6 every difference below is exact in double precision. */
+  int best = 0;
+  double best_d = fabs(a - E2M1_MAGNITUDE[0]);
+  for (int k = 1; k < 8; k++) {
+    double d = fabs(a - E2M1_MAGNITUDE[k]);
+    if (d < best_d || (d == best_d && (k % 2) == 0)) {
+      best = k;
+      best_d = d;
+    }
+  }
+  return sign | best;
+}
+
+/* ---------------------------------------------------------------------- */
+/* UE4M3 scale (R1): OCP E4M3 with bias 7, e = code>>3, m = code&7,  */
+/* value = m * 2^-9 if e == 0 else (1 + m/8) * 2^(e-7); code 127 is NaN.    */
+/* ---------------------------------------------------------------------- */
+float so_e4m3_value(int code) {
+  if (code < 0 || code > 126) return NAN;
+  int e = code >> 3, m = code & 7;
+  double v = (e == 0) ? ldexp((double)m, -9) : ldexp(1.0 + m / 8.0, e - 7);
+  return (float)v; /* exact: at most 4 significant bits */
+}
+
+/* round_UE4M3 (Alg. 1 line 2): the finite code nearest v >= 0, ties
+ * to the even code; v above the largest finite value 448 gives 448
+ * (satfinite).  Codes 0..126 only (R2). */
+int so_e4m3_encode(float v) {
+  double a = (double)v;
+  if (!(a >= 0.0)) return 0; /* negative or NaN never reach here */
+  if (a >= 448.0) return 126;
+  /* For a < 448 every difference below is exact in double precision. */
+  int best = 0;
+  double best_d = fabs(a - (double)so_e4m3_value(0));
+  for (int c = 1; c <= 126; c++) {
+    double d = fabs(a - (double)so_e4m3_value(c));
+    if (d < best_d || (d == best_d && (c % 2) == 0)) {
+      best = c;
+      best_d = d;
+    }
+  }
+  return best;
+}
+
+void so_e2m1_encode_array(const float* t, int64_t n, uint8_t* nib) {
+  for (int64_t i = 0; i < n; i++) nib[i] = (uint8_t)so_e2m1_encode(t[i]);
+}
+
+void so_e4m3_encode_array(const float* v, int64_t n, uint8_t* code) {
+  for (int64_t i = 0; i < n; i++) code[i] = (uint8_t)so_e4m3_encode(v[i]);
+}
+
+/* ---------------------------------------------------------------------- */
+/* One candidate scale: quantize, dequantize, loss (Alg. 1 lines 7-9).     */
+/* ---------------------------------------------------------------------- */
+static float candidate_loss(const float y[16], float s, float rho, uint8_t nib[16]) {
+  float d[16];
+  for (int i = 0; i < 16; i++) {
+    /* q_i = round_E2M1(x_i / s) (Alg. 1 line 7), with x_i / s computed as
+     * x_i * RN(1/s) the way the vLLM kernel does (figVLLMnvf4; R7). */
+    float t = y[i] * rho;
+    nib[i] = (uint8_t)so_e2m1_encode(t);
+    float q = (float)so_e2m1_value(nib[i]);
+    /* xhat_i = q_i * s (line 8; exact: <= 6 significant bits) and the
+     * residual x_i - xhat_i, rounded once. */
+    d[i] = fmaf(-q, s, y[i]);
+  }
+  /* loss = sum_i (x_i - xhat_i)^2 (line 9) in the fixed order of R12:
+   * two FMA chains, even indices and odd indices, then one add. */
+  float a = d[0] * d[0];
+  for (int i = 2; i < 16; i += 2) a = fmaf(d[i], d[i], a);
+  float b = d[1] * d[1];
+  for (int i = 3; i < 16; i += 2) b = fmaf(d[i], d[i], b);
+  return a + b;
+}
+
+/* Algorithm 1, "NVFP4 Scale Search", with the readings R2-R5. */
+int so_search_block(const float y[16], int fmin, int fmax, so_block_result* out) {
+  if (fmin > 0 || fmax < 0) return 1;
+  /* line 1: x_max = max_i |x_i| */
+  float xmax = 0.0f;
+  for (int i = 0; i < 16; i++)
+    if (fabsf(y[i]) > xmax) xmax = fabsf(y[i]);
+  /* line 2: s = round_UE4M3(x_max * (1.0/6.0)); 1/6 rounded once (R8) */
+  const float one_sixth = 1.0f / 6.0f;
+  float v = xmax * one_sixth;
+  int c0 = so_e4m3_encode(v);
+  /* line 3: s_int8 = reinterpret(s, int8) == c0.  line 4: l* = +inf. */
+  int have = 0, cstar = -1, n_eval = 0;
+  float best = INFINITY, base = NAN;
+  uint8_t nib[16], best_nib[16] = {0};
+  for (int f = fmin; f <= fmax; f++) { /* line 5 */
+    int c = c0 + f;
+    float s, rho;
+    if (f == 0 && c0 == 0) {
+      /* zero-scale candidate (R3): every value quantizes to 0. */
+      s = 0.0f;
+      rho = 0.0f;
+    } else if (c < 1 || c > 126) {
+      continue; /* line 6: scale out of range (127 is NaN, R2) */
+    } else {
+      s = so_e4m3_value(c); /* line 7: s^(f) = reinterpret(s_int8 + f) */
+      rho = 1.0f / s;
+    }
+    float loss = candidate_loss(y, s, rho, nib);
+    n_eval++;
+    if (f == 0) base = loss;
+    /* line 10: strict "<" while scanning f upward, so equal losses keep the
+     * smaller scale (R4); the first valid candidate is always taken (R3). */
+    if (!have || loss < best) {
+      have = 1;
+      best = loss;
+      cstar = c;
+      memcpy(best_nib, nib, 16);
+    }
+  }
+  out->c0 = c0;
+  out->cstar = cstar;
+  out->fstar = cstar - c0; /* R5 */
+  out->n_evaluated = n_eval;
+  out->err_best = best;
+  out->err_base = base;
+  memcpy(out->nib, best_nib, 16);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------- */
+/* Tensor level.                                                            */
+/* ---------------------------------------------------------------------- */
+static float bf16_to_float(uint16_t h) {
+  /* bf16 is the top half of a binary32: the conversion is exact. */
+  uint32_t u = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+static uint32_t float_bits(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return u;
+}
+
+static float bits_float(uint32_t u) {
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+/* A = max |x| over the tensor ("dividing by the global scale from ...
+ * tensor scaling"); non-finite input is an error (R14). */
+int so_tensor_amax(const uint16_t* x, int64_t n, uint32_t* amax_bits) {
+  float a = 0.0f;
+  for (int64_t i = 0; i < n; i++) {
+    float v = bf16_to_float(x[i]);
+    if (!isfinite(v)) return 4;
+    if (fabsf(v) > a) a = fabsf(v);
+  }
+  *amax_bits = float_bits(a);
+  return 0;
+}
+
+/* G maps the tensor amax onto 6 * 448 = 2688, the largest NVFP4 magnitude
+ * (figVLLMnvf4 P:126-129 SFScaleVal multiplies; R9). */
+int so_global_scale(int gmode, uint32_t amax_bits, float* G) {
+  if (gmode == 0) {
+    *G = 1.0f;
+    return 0;
+  }
+  float A = bits_float(amax_bits);
+  if (!isfinite(A) || A < 0.0f) return 4;
+  if (A == 0.0f) {
+    *G = 1.0f;
+    return 0;
+  }
+  float g = 2688.0f / A;
+  if (!isfinite(g)) return 5;
+  *G = g;
+  return 0;
+}
+
+int so_quantize(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int fmax,
+                int gmode, const uint32_t* amax_bits_in, uint8_t* codes,
+                uint8_t* scales, int8_t* offsets, float* err, double* sums,
+                int64_t* n_eval, float* G_out, int threads) {
+  if (rows < 0 || cols < 0 || cols % 16 != 0 || fmin > 0 || fmax < 0) return 1;
+  if (gmode < 0 || gmode > 2 || (gmode == 2 && !amax_bits_in)) return 1;
+  if (fmin < -126) fmin = -126;
+  if (fmax > 126) fmax = 126;
+  uint32_t amax_bits = 0;
+  if (gmode == 1) {
+    int st = so_tensor_amax(x, rows * cols, &amax_bits);
+    if (st) return st;
+  } else if (gmode == 2) {
+    amax_bits = *amax_bits_in;
+  }
+  float G;
+  int st = so_global_scale(gmode, amax_bits, &G);
+  if (st) return st;
+  if (G_out) *G_out = G;
+
+  const int64_t nbr = cols / 16, nb = rows * nbr;
+  float* e = (float*)malloc(sizeof(float) * 2 * (nb > 0 ? nb : 1));
+  int32_t* ne = (int32_t*)malloc(sizeof(int32_t) * (nb > 0 ? nb : 1));
+  if (!e || !ne) {
+    free(e);
+    free(ne);
+    return 1;
+  }
+#ifdef _OPENMP
+  if (threads <= 0) threads = omp_get_num_procs();
+#pragma omp parallel for schedule(dynamic, 16) num_threads(threads)
+#endif
+  for (int64_t r = 0; r < rows; r++) {
+    for (int64_t bj = 0; bj < nbr; bj++) {
+      const int64_t blk = r * nbr + bj;
+      float y[16];
+      for (int i = 0; i < 16; i++) /* y = x * G (mode NONE: y = x exactly) */
+        y[i] = (gmode == 0) ? bf16_to_float(x[r * cols + bj * 16 + i])
+                            : bf16_to_float(x[r * cols + bj * 16 + i]) * G;
+      so_block_result res;
+      so_search_block(y, fmin, fmax, &res);
+      for (int j = 0; j < 8; j++)
+        codes[r * (cols / 2) + bj * 8 + j] =
+            (uint8_t)(res.nib[2 * j] | (res.nib[2 * j + 1] << 4));
+      scales[blk] = (uint8_t)res.cstar;
+      if (offsets) offsets[blk] = (int8_t)res.fstar;
+      e[2 * blk] = res.err_best;
+      e[2 * blk + 1] = res.err_base;
+      ne[blk] = res.n_evaluated;
+    }
+  }
+  double sb = 0.0, s0 = 0.0;
+  int64_t total = 0;
+  for (int64_t b = 0; b < nb; b++) { /* FP64 sums in block order */
+    sb += (double)e[2 * b];
+    s0 += (double)e[2 * b + 1];
+    total += ne[b];
+  }
+  if (err) memcpy(err, e, sizeof(float) * 2 * nb);
+  if (sums) {
+    sums[0] = sb;
+    sums[1] = s0;
+  }
+  if (n_eval) *n_eval = total;
+  free(e);
+  free(ne);
+  return 0;
+}
+
+/* Round a binary32 to the nearest bfloat16, ties to even: pick the nearer of
+ * the two bf16 values that bracket v. */
+static uint16_t float_to_bf16_rne(float v) {
+  uint32_t u = float_bits(v);
+  uint32_t lo = u & 0xFFFF0000u;           /* toward zero */
+  uint32_t hi = lo + 0x00010000u;           /* next bf16 away from zero */
+  double dv = (double)v;
+  double dl = fabs(dv - (double)bits_float(lo));
+  double dh = fabs((double)bits_float(hi) - dv);
+  if ((u & 0xFFFFu) == 0) return (uint16_t)(lo >> 16);
+  if (dl < dh) return (uint16_t)(lo >> 16);
+  if (dh < dl) return (uint16_t)(hi >> 16);
+  return ((lo >> 16) & 1) ? (uint16_t)(hi >> 16) : (uint16_t)(lo >> 16);
+}
+
+int so_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows,
+                  int64_t cols, float G, uint16_t* out) {
+  if (rows < 0 || cols < 0 || cols % 16 != 0 || !(G > 0.0f)) return 1;
+  const int64_t nbr = cols / 16;
+  for (int64_t r = 0; r < rows; r++)
+    for (int64_t k = 0; k < cols; k++) {
+      uint8_t byte = codes[r * (cols / 2) + k / 2];
+      int nib = (k % 2 == 0) ? (byte & 15) : (byte >> 4);
+      float s = so_e4m3_value(scales[r * nbr + k / 16]);
+      float q = (float)so_e2m1_value(nib);
+      float xs = q * s; /* exact */
+      out[r * cols + k] = float_to_bf16_rne(xs / G);
+    }
+  return 0;
+}
