@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""bench.py — ScaleSearch NVFP4 quantization throughput on B200 (driver contract).
+
+One step = the whole hot path over one batch: for every tensor of the
+workload, the amax pass (a2), the global scale (a3) and the candidate search
++ emit (a4-a7) with radius 8, writing codes, scales and the per-block
+{err_best, err_base}.  Default workload = BASELINE.json configs[1]: the 252
+linear weights of Qwen3-8B (6.95 G bf16 elements, 13.9 GB), rows sharded over
+the ranks when N > 1 with ONE max all-reduce of the 252 shard amaxes (NCCL).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+``--impl reference`` times the CPU oracle (this tier's reference arm) on a
+bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scalesearch_nvfp4_quantize_gbs_bf16_in"
+UNIT = "GB/s"
+FP32_LANES_PER_SM = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="c2_qwen3_8b_weights")
+    ap.add_argument("--radius", type=int, default=8)
+    ap.add_argument("--fmin", type=int, default=None)
+    ap.add_argument("--fmax", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no clocks, e2e or cpu baseline")
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    a = ap.parse_args()
+    if a.fmin is None and a.fmax is None:
+        a.fmin, a.fmax = -min(a.radius, 126), min(a.radius, 126)
+    if a.profile:
+        a.no_e2e = a.no_cpu_baseline = a.no_clocks = True
+    return a
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "sm_max_mhz": float(m["sm_max_mhz"]),
+             "source": "MEASURED_PEAKS.json"}
+    except Exception:
+        pass
+    return p
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "sm_mhz_min": min(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle on the host cores
+# ---------------------------------------------------------------------------
+def oracle_sample(specs, frac_rows: float):
+    """Bounded sample of the workload: the first ``frac_rows`` of the rows of
+    the first layer's tensors (every projection shape of the model)."""
+    import ssgen
+    first = specs[: min(len(specs), 7)]
+    out = []
+    for s in first:
+        r = max(1, int(s.rows * frac_rows))
+        out.append((s, ssgen.generate(s.kind, s.rows, s.cols, seed=ssgen.workloads.BASE_SEED,
+                                      tid=s.tid, row_start=0, row_end=r)))
+    return out
+
+
+def time_oracle(sample, fmin, fmax, threads=0):
+    import oracle
+    t0 = time.perf_counter()
+    n = 0
+    for s, x in sample:
+        amax = oracle.tensor_amax(x)          # amax of the sampled rows (a2)
+        oracle.quantize(x, x.shape[0], s.cols, fmin, fmax, "given", amax_bits=amax, threads=threads)
+        n += x.numel()
+    return n, time.perf_counter() - t0
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    import ssgen
+    import oracle
+    oracle.build()
+    specs = ssgen.workload(a.workload)
+    sample = oracle_sample(specs, 1.0 / 16)
+    cores = os.cpu_count() or 1
+    for _ in range(a.warmup):
+        time_oracle(sample, a.fmin, a.fmax)
+    times = []
+    n = 0
+    for _ in range(a.steps):
+        n, dt = time_oracle(sample, a.fmin, a.fmax)
+        times.append(dt)
+    t = sum(times) / len(times)
+    gbs = n * 2 / t / 1e9
+    desc = ("first 1/16 of the rows of layer 0's 7 projections (%d bf16 elements per step); "
+            "amax + search over the sampled rows, window [%d, %d]" % (n, a.fmin, a.fmax))
+    line = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(a, specs, world),
+            "cpu_baseline": {"value": gbs, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": gbs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(line, a)
+
+
+def config_dict(a, specs, world):
+    n = sum(s.numel for s in specs)
+    return {"workload": a.workload, "tensors": len(specs), "elements": n,
+            "bf16_bytes": 2 * n, "window": [a.fmin, a.fmax],
+            "global_scale": "per-tensor amax (max all-reduce over row shards when N>1)",
+            "outputs": "codes+scales+err{best,base}+err sums",
+            "l2": "inputs %.1f GB >> 126 MB L2 across a step (no flush needed); each tensor's "
+                  "amax->quantize reuse of L2 is part of the design" % (2 * n / 1e9),
+            "parallelism": "row-shard x%d" % world}
+
+
+def emit(line, a):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(s + "\n")
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+class QuantEvents:
+    """CUDA events around every quantize launch in the timed region (the
+    launching stream is torch's current stream, which the binding uses)."""
+
+    def __init__(self, torch, n):
+        self.torch = torch
+        self.ev = []
+        self.active = False
+
+    def before(self, k):
+        if self.active:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.ev.append([e, None])
+
+    def after(self, k):
+        if self.active:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.ev[-1][1] = e
+
+    def total_ms(self):
+        return sum(a.elapsed_time(b) for a, b in self.ev)
+
+
+def c_eff_of(torch, outs, shards, fmin, fmax, max_tensors=8):
+    """Mean number of VALID candidates per block (the algorithmic work; SURVEY
+    §8(d)), counted from c0 = c* - f* of an untimed pass with offsets."""
+    import paper_2605_12464_b200 as ss
+    tot, cnt = 0.0, 0
+    for x in shards[:max_tensors]:
+        if x.shape[0] == 0:
+            continue
+        o = ss.quantize(x, fmin=fmin, fmax=fmax, gmode="tensor", want_err=False)
+        c0 = o.scales.reshape(-1).to(torch.int32) - o.offsets.to(torch.int32)
+        f = torch.arange(fmin, fmax + 1, device=x.device, dtype=torch.int32)
+        c = c0[:, None] + f[None, :]
+        valid = ((c >= 1) & (c <= 126)) | ((f[None, :] == 0) & (c0[:, None] == 0))
+        tot += valid.sum().item()
+        cnt += c0.numel()
+        del o
+    return tot / max(cnt, 1)
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import ssgen
+    import paper_2605_12464_b200 as ss
+    from paper_2605_12464_b200.dist import CudaOps, RowShardQuantizer, ShardPlan
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ss.lib()
+    specs = ssgen.workload(a.workload)
+    plan = ShardPlan([(s.rows, s.cols) for s in specs], rank, world)
+    shards = []
+    for k, s in enumerate(specs):
+        lo, hi = plan.rows(k)
+        shards.append(ssgen.generate(s.kind, s.rows, s.cols, seed=ssgen.workloads.BASE_SEED,
+                                     tid=s.tid, row_start=lo, row_end=hi, device=dev))
+    ops = CudaOps(a.fmin, a.fmax, want_err=True, want_sums=True)
+    outs = [ops.alloc_out(x) for x in shards]
+    q = RowShardQuantizer(plan, ops, group=None, device=dev)
+    hooks = QuantEvents(torch, len(shards))
+    torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        q.step(shards, outs)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank) if not a.no_clocks else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    hooks.active = True
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start.record()
+    launches = 0
+    for _ in range(a.steps):
+        launches += q.step(shards, outs, hooks)
+    stop.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    hooks.active = False
+    clk = clocks.stop() if clocks else None
+    ms = start.elapsed_time(stop) / a.steps
+    quant_ms = hooks.total_ms() / a.steps
+    t = torch.tensor([ms, quant_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, quant_ms = t.tolist()
+
+    n_total = sum(s.numel for s in specs)          # all ranks together process every element
+    value = 2.0 * n_total / (ms * 1e-3) / 1e9
+    n_local = plan.local_numel()
+
+    # MSE cut over the whole workload (fp64 sums from the kernels)
+    sums = torch.stack([o.sums for o in outs if o.sums is not None]).sum(0)
+    if world > 1:
+        dist.all_reduce(sums)
+    s_best, s_base = sums.tolist()
+    cut = 100.0 * (1.0 - s_best / s_base) if s_base > 0 else 0.0
+
+    ceff = c_eff_of(torch, outs, shards, a.fmin, a.fmax)
+    pk = peaks()
+    ops_per_elem = 4.0 * ceff + 2.0
+    achieved = n_local * ops_per_elem / (quant_ms * 1e-3) / 1e12        # T lane-op/s
+    peak = 148 * FP32_LANES_PER_SM * pk["sm_max_mhz"] * 1e6 / 1e12
+    bytes_q = n_local * (2.0 + 0.5 + 0.0625 + 0.5)                     # in + codes + scales + err
+    hbm_achieved = bytes_q / (quant_ms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "quant_traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                tj = json.load(f)
+            traffic = tj["dram_bytes_per_elem"] * n_local / max(1, len(shards))
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "ss::quant_kernel<%d>" % (a.fmax - a.fmin + 1),
+            "ops_per_elem": ops_per_elem, "c_eff": ceff,
+            "peak_source": "148 SMs x 128 FP32 lanes x %.0f MHz (%s)" % (pk["sm_max_mhz"], pk["source"]),
+            "quant_ms_per_step": quant_ms, "quant_share_of_step": quant_ms / ms,
+            "quant_launches_per_step": len(shards),
+            "hbm_gbs_achieved": hbm_achieved, "hbm_peak_gbs": pk["hbm_gbs"],
+            "hbm_frac": hbm_achieved / pk["hbm_gbs"]}
+    if clk and clk.get("sm_mhz"):
+        roof["frac_at_run_clock"] = achieved / (148 * FP32_LANES_PER_SM * clk["sm_mhz"] * 1e6 / 1e12)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (ssgen, seed %d: Qwen3-8B-shaped random weights N(0, 0.02^2) with "
+                    "0.1%% input channels x50)" % ssgen.workloads.BASE_SEED,
+            "config": config_dict(a, specs, world),
+            "mse_cut_pct": cut, "mse_base": s_base / n_total, "mse_best": s_best / n_total,
+            "gpu_launches": launches, "roofline": roof}
+    if clk:
+        line["clocks"] = clk
+
+    # e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    if not a.no_e2e:
+        line["e2e"] = run_e2e(a, torch, ss, shards, specs, plan, world, dev)
+
+    del outs
+    if not a.no_cpu_baseline and rank == 0 and world == 1:
+        import oracle
+        oracle.build()
+        sample = oracle_sample(specs, 1.0 / 8)
+        n, dt = time_oracle(sample, a.fmin, a.fmax)
+        line["cpu_baseline"] = {
+            "value": 2.0 * n / dt / 1e9, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": "first 1/8 of the rows of layer 0's 7 projections: %d bf16 elements, "
+                      "amax + search, window [%d, %d], %.1f s" % (n, a.fmin, a.fmax, dt)}
+    if rank == 0:
+        emit(line, a)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(a, torch, ss, shards, specs, plan, world, dev):
+    import torch.distributed as dist
+    hx = [x.cpu().pin_memory() for x in shards]
+    hc = [torch.empty(x.shape[0], x.shape[1] // 2, dtype=torch.uint8).pin_memory() for x in shards]
+    hs = [torch.empty(x.shape[0], x.shape[1] // 16, dtype=torch.uint8).pin_memory() for x in shards]
+    he = [torch.empty(x.numel() // 16, 2, dtype=torch.float32).pin_memory() for x in shards]
+    bi = sum(x.numel() * 2 for x in hx)
+    bo = sum(c.numel() + s.numel() + e.numel() * 4 for c, s, e in zip(hc, hs, he))
+
+    def one_step():
+        if world == 1:
+            # the C-ABI host entry point: H2D, amax, quantize, D2H per tensor
+            for x, c, s, e in zip(hx, hc, hs, he):
+                ss.quantize_host(x, x.shape[0], x.shape[1], a.fmin, a.fmax, "tensor", c, s, e)
+        else:
+            # sharded: same calls composed through the public API + one all-reduce
+            dx = [torch.empty_like(x, device=dev) for x in hx]
+            amax = torch.zeros(len(hx), dtype=torch.int32, device=dev)
+            for k, x in enumerate(hx):
+                dx[k].copy_(x, non_blocking=True)
+                if x.shape[0]:
+                    ss.tensor_amax(dx[k], out=amax[k:k + 1])
+            dist.all_reduce(amax, op=dist.ReduceOp.MAX)
+            for k, x in enumerate(dx):
+                if x.shape[0] == 0:
+                    continue
+                o = ss.quantize(x, fmin=a.fmin, fmax=a.fmax, gmode="device_amax",
+                                amax=amax[k:k + 1], want_offsets=False, want_sums=False)
+                hc[k].copy_(o.codes, non_blocking=True)
+                hs[k].copy_(o.scales, non_blocking=True)
+                he[k].copy_(o.err, non_blocking=True)
+            torch.cuda.synchronize()
+
+    one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(a.e2e_steps):
+        one_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / a.e2e_steps
+    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = t.item()
+    n_total = sum(s.numel for s in specs)
+    return {"value": 2.0 * n_total / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "ms_per_step": dt * 1e3,
+            "path": "ss_quantize_nvfp4_host per tensor" if world == 1 else
+                    "public API: H2D + ss_tensor_amax + NCCL max + ss_quantize_nvfp4_ex + D2H"}
+
+
+def main():
+    a = parse()
+    rank, world, local_rank = env_rank()
+    if a.gpus != world and world == 1 and a.gpus > 1:
+        print(json.dumps({"error": "use torchrun --nproc-per-node %d for --gpus %d" % (a.gpus, a.gpus)}))
+        sys.exit(2)
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    run_ours(a, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

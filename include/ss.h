@@ -1,0 +1,170 @@
+/*
+ * ss.h — C ABI of libss.so: ScaleSearch NVFP4 quantization on B200 (sm_100a).
+ *
+ * Method: arxiv 2605.12464, "Search Your Block Floating Point Scales!".
+ * Citations "P:n" are lines of the paper's LaTeX source; "R<k>"
+ * are the readings of the paper listed in DESIGN.md §3.
+ *
+ * Formats.  A bf16 tensor X[rows][cols] (row-major, cols % 16 == 0)
+ * is cut into 16-element blocks along each row.  Each block is stored
+ * as 16 E2M1 nibbles (values {0,±0.5,±1,±1.5,±2,±3,±4,±6}) and one
+ * UE4M3 scale byte (OCP E4M3 code 0..126, bias 7; R1, R2).  A per-tensor FP32
+ * global scale G = RN(2688 / max|X|) maps the tensor amax onto 6*448 first
+ * (figVLLMnvf4; R9), so block b quantizes y = RN(x * G).
+ *
+ * ScaleSearch (Algorithm 1): per block, c0 = round_UE4M3(max|y| *
+ * RN(1/6)) (R8); for each offset f in [f_min, f_max] (R6) with valid code
+ * c = c0 + f (1 <= c <= 126; plus the zero scale when c0 == 0, f == 0; R2, R3)
+ * the block is quantized with t_i = RN(y_i * RN(1/s_c)) (R7), q_i =
+ * E2M1_RNE_satfinite(t_i) (R10), d_i = RN(y_i - q_i*s_c) and loss
+ * L = RN(a + b) with a, b the FP32 FMA chains of d_i^2 over even / odd i (R12).
+ * The winner is the lexicographic minimum of (L, c): ties keep the smaller
+ * scale (Alg. 1 strict <; R4).  Outputs are bit-identical to the CPU
+ * oracle (oracle/ss_oracle.c) under this contract.
+ *
+ * Layouts (R15): codes [rows][cols/2] u8, element 2j in the low nibble of byte
+ * j, sign in bit 3 of each nibble (negative values that round to 0 keep the
+ * sign, R11); scales [rows][cols/16] u8 E4M3 codes, linear row-major.
+ *
+ * Conventions for every entry point:
+ *  - All array arguments are DEVICE pointers owned by the caller unless the
+ *    name starts with h_ (host).  The library never keeps a pointer after the
+ *    call returns; its only allocations are a small per-(device, stream)
+ *    workspace (amax slot, status flags, per-CTA partial sums), created on
+ *    first use and reused.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call only enqueues work on `stream` and returns; none synchronizes
+ *    except ss_get_device_status and ss_quantize_nvfp4_host.
+ *  - Argument errors are detected synchronously and returned without
+ *    launching anything.  A failed launch returns SS_ERR_CUDA.
+ *  - Non-finite input (NaN/Inf) cannot be reported synchronously: the amax
+ *    pass sets a sticky device flag (read with ss_get_device_status), uses
+ *    G = 1, and the outputs are defined but meaningless.
+ *  - Reentrant; calls on distinct streams may run concurrently.
+ *  - There is no CPU fallback: without an sm_100 device every call returns
+ *    SS_ERR_UNSUPPORTED_DEVICE.
+ */
+#ifndef SS_H
+#define SS_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SS_API __attribute__((visibility("default")))
+#else
+#define SS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SS_OK = 0,
+  SS_ERR_INVALID_ARG = 1,        /* null pointer, bad size, cols % 16, f_min > 0 or f_max < 0 */
+  SS_ERR_ALIGNMENT = 2,          /* in_bf16 / out_bf16 not 16-B aligned, codes not 8-B aligned */
+  SS_ERR_CUDA = 3,               /* a CUDA runtime call or launch failed                      */
+  SS_ERR_NONFINITE = 4,          /* (device flag) NaN/Inf seen by an amax pass                */
+  SS_ERR_RANGE = 5,              /* (device flag) 0 < amax < 2688/FLT_MAX: G overflows        */
+  SS_ERR_UNSUPPORTED_DEVICE = 6  /* current device is not compute capability 10.x            */
+} ss_status;
+
+/* Global-scale modes (R9). */
+enum {
+  SS_GLOBAL_NONE = 0,        /* G = 1: y = x (the paper's §4.1 synthetic setting)      */
+  SS_GLOBAL_TENSOR = 1,      /* G from the amax of THIS tensor (one extra HBM read pass)      */
+  SS_GLOBAL_DEVICE_AMAX = 2  /* G from *d_amax_bits supplied by the caller, e.g. the NCCL max  */
+                             /* over all row shards of a tensor                */
+};
+
+/* Human-readable name of a status code (static string). */
+SS_API const char* ss_status_string(int status);
+
+/* ABI version (major * 100 + minor). */
+SS_API int ss_version(void);
+
+/*
+ * Global amax (step a2; "dividing by the global scale from ... tensor
+ * scaling").  Reduces max|x| over n bf16 values at in_bf16 into
+ * *d_amax_bits as the FP32 bit pattern of the maximum (bf16 -> f32 is exact,
+ * so this is exact and independent of order).  The reduction is an unsigned
+ * integer max on |x| bit patterns, so NaN > Inf > any finite value: a result
+ * >= 0x7F800000 means the input was not finite.
+ *   accumulate = 0: *d_amax_bits is overwritten with the max of this call.
+ *   accumulate = 1: *d_amax_bits = max(*d_amax_bits, max of this call)
+ *                   (several chunks or row shards into one slot).
+ * in_bf16 must be 16-B aligned; n >= 0 (n == 0 leaves / sets 0).
+ */
+SS_API ss_status ss_tensor_amax(const void* in_bf16, int64_t n, uint32_t* d_amax_bits,
+                         int accumulate, void* stream);
+
+/*
+ * ScaleSearch quantization with a symmetric window f in [-radius, radius]
+ * (north star; radius > 126 is clamped to 126 = exhaustive search).
+ *   in_bf16     [rows][cols] bf16, 16-B aligned, cols % 16 == 0, rows >= 0
+ *   global_scale_mode  SS_GLOBAL_NONE or SS_GLOBAL_TENSOR (this call runs the
+ *               amax pass itself; a row shard of a larger tensor must use
+ *               ss_quantize_nvfp4_ex with SS_GLOBAL_DEVICE_AMAX instead)
+ *   out_codes   [rows][cols/2] u8, 8-B aligned
+ *   out_scales  [rows][cols/16] u8
+ *   out_err     nullable; [rows*cols/16][2] f32 {err_best, err_base}, the
+ *               y-domain squared error of the winner and of the max-abs
+ *               scale (f = 0), 8-B aligned
+ */
+SS_API ss_status ss_quantize_nvfp4(const void* in_bf16, int64_t rows, int64_t cols, int radius,
+                            int global_scale_mode, uint8_t* out_codes, uint8_t* out_scales,
+                            float* out_err, void* stream);
+
+/* Full argument set.  Unused nullable outputs cost nothing. */
+typedef struct {
+  const void* in_bf16;          /* [rows][cols] bf16, 16-B aligned                         */
+  int64_t rows, cols;           /* rows >= 0, cols % 16 == 0                                */
+  int f_min, f_max;             /* inclusive window, f_min <= 0 <= f_max (R6); clamped to   */
+                                /* [-126, 126]; e.g. the paper's production [-2, 6] */
+  int global_scale_mode;        /* SS_GLOBAL_*                                              */
+  const uint32_t* d_amax_bits;  /* SS_GLOBAL_DEVICE_AMAX: device u32 FP32 bits of the amax  */
+  uint8_t* out_codes;           /* [rows][cols/2] u8, 8-B aligned                           */
+  uint8_t* out_scales;          /* [rows][cols/16] u8                                       */
+  float* out_err;               /* nullable: [nb][2] f32 {err_best, err_base}, 8-B aligned  */
+  int8_t* out_offset;           /* nullable: [nb] f* = c* - c0 (R5)                          */
+  double* d_err_sums;           /* nullable: device f64[2] = {sum err_best, sum err_base},  */
+                                /* overwritten; fixed-order reduction (deterministic)       */
+  float* d_global_scale;        /* nullable: device f32 receives G (for dequantization)     */
+  void* stream;
+} ss_quant_args;
+
+SS_API ss_status ss_quantize_nvfp4_ex(const ss_quant_args* args);
+
+/*
+ * Dequantization (step a8): xhat = RNE_bf16(RN((q * s) / G)).
+ *   codes [rows][cols/2] u8 (8-B aligned), scales [rows][cols/16] u8,
+ *   d_global_scale nullable (NULL => G = 1), out_bf16 [rows][cols] (16-B aligned).
+ */
+SS_API ss_status ss_dequantize_nvfp4(const uint8_t* codes, const uint8_t* scales, int64_t rows,
+                              int64_t cols, const float* d_global_scale, void* out_bf16,
+                              void* stream);
+
+/*
+ * End-to-end from HOST memory (the e2e leg of bench.py): copies h_in to the
+ * device in chunks, runs the amax pass per chunk as it lands (SS_GLOBAL_TENSOR)
+ * and the quantization per chunk, and copies codes / scales (and errors when
+ * h_err != NULL) back to host memory, overlapping copies with kernels on two
+ * internal streams.  Host buffers should be pinned (cudaHostAlloc /
+ * torch pin_memory) for full PCIe bandwidth; pageable memory works but is
+ * staged by the driver.  Synchronous: returns after the outputs are in host
+ * memory.  Device buffers are library-owned, cached per device and grown on
+ * demand (size of one tensor plus its outputs).
+ */
+SS_API ss_status ss_quantize_nvfp4_host(const void* h_in_bf16, int64_t rows, int64_t cols, int f_min,
+                                 int f_max, int global_scale_mode, uint8_t* h_codes,
+                                 uint8_t* h_scales, float* h_err);
+
+/* Synchronizes `stream`, returns and clears the sticky device flags of this
+ * (device, stream) workspace: bit 0 = non-finite input seen (SS_ERR_NONFINITE),
+ * bit 1 = global scale out of range (SS_ERR_RANGE). */
+SS_API ss_status ss_get_device_status(int* flags, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_H */

@@ -1,0 +1,28 @@
+"""ScaleSearch NVFP4 quantization on B200 (arxiv 2605.12464), B200-native.
+
+The compute path is libss.so (include/ss.h): hand-written sm_100a kernels for
+the amax, search-quantize and dequantize steps.  This package is the thin
+Python binding (argument marshalling only) plus the row-shard driver that
+runs one process per GPU over torch.distributed/NCCL.
+"""
+from ._binding import (  # noqa: F401
+    FLAG_NONFINITE,
+    FLAG_RANGE,
+    GMODES,
+    LIB_PATH,
+    QuantOut,
+    SSError,
+    dequantize,
+    device_status,
+    lib,
+    quantize,
+    quantize_host,
+    quantize_simple,
+    status_string,
+    tensor_amax,
+)
+
+__all__ = [
+    "lib", "tensor_amax", "quantize", "quantize_simple", "dequantize", "quantize_host",
+    "device_status", "status_string", "SSError", "QuantOut", "GMODES",
+]

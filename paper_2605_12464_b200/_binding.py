@@ -1,0 +1,189 @@
+"""ctypes binding of libss.so (include/ss.h).  Argument marshalling only.
+
+Every step of the quantization runs in the sm_100a kernels behind the C ABI;
+there is no Python or CPU compute path.  If the library cannot be loaded, or
+the current device is not sm_100, calls raise ``SSError`` -- nothing falls back.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import NamedTuple, Optional
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libss.so")
+
+SS_OK, SS_ERR_INVALID_ARG, SS_ERR_ALIGNMENT, SS_ERR_CUDA = 0, 1, 2, 3
+SS_ERR_NONFINITE, SS_ERR_RANGE, SS_ERR_UNSUPPORTED_DEVICE = 4, 5, 6
+GMODES = {"none": 0, "tensor": 1, "device_amax": 2}
+FLAG_NONFINITE, FLAG_RANGE = 1, 2
+
+_lock = threading.Lock()
+_lib = None
+
+
+class SSError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        msg = "libss: %s" % (status_string(status) if _lib is not None else "status %d" % status)
+        super().__init__(msg + (" (%s)" % what if what else ""))
+
+
+class QuantArgs(ctypes.Structure):
+    _fields_ = [
+        ("in_bf16", ctypes.c_void_p),
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("f_min", ctypes.c_int),
+        ("f_max", ctypes.c_int),
+        ("global_scale_mode", ctypes.c_int),
+        ("d_amax_bits", ctypes.c_void_p),
+        ("out_codes", ctypes.c_void_p),
+        ("out_scales", ctypes.c_void_p),
+        ("out_err", ctypes.c_void_p),
+        ("out_offset", ctypes.c_void_p),
+        ("d_err_sums", ctypes.c_void_p),
+        ("d_global_scale", ctypes.c_void_p),
+        ("stream", ctypes.c_void_p),
+    ]
+
+
+def lib():
+    """Load libss.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError("libss.so not built: run `python -m paper_2605_12464_b200.build` "
+                                  "or __graft_entry__.build(); there is no CPU fallback")
+            L = ctypes.CDLL(LIB_PATH)
+            P, i64, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+            L.ss_status_string.restype = ctypes.c_char_p
+            L.ss_status_string.argtypes = [I]
+            L.ss_version.restype = I
+            L.ss_version.argtypes = []
+            L.ss_tensor_amax.restype = I
+            L.ss_tensor_amax.argtypes = [P, i64, P, I, P]
+            L.ss_quantize_nvfp4.restype = I
+            L.ss_quantize_nvfp4.argtypes = [P, i64, i64, I, I, P, P, P, P]
+            L.ss_quantize_nvfp4_ex.restype = I
+            L.ss_quantize_nvfp4_ex.argtypes = [ctypes.POINTER(QuantArgs)]
+            L.ss_dequantize_nvfp4.restype = I
+            L.ss_dequantize_nvfp4.argtypes = [P, P, i64, i64, P, P, P]
+            L.ss_quantize_nvfp4_host.restype = I
+            L.ss_quantize_nvfp4_host.argtypes = [P, i64, i64, I, I, I, P, P, P]
+            L.ss_get_device_status.restype = I
+            L.ss_get_device_status.argtypes = [ctypes.POINTER(ctypes.c_int), P]
+            _lib = L
+    return _lib
+
+
+def status_string(status: int) -> str:
+    return lib().ss_status_string(int(status)).decode()
+
+
+def _check(st: int, what: str = ""):
+    if st != SS_OK:
+        raise SSError(st, what)
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _window(radius, fmin, fmax):
+    if fmin is None and fmax is None:
+        r = 8 if radius is None else int(radius)
+        if r < 0:
+            raise ValueError("radius must be >= 0")
+        return -min(r, 126), min(r, 126)
+    if radius is not None:
+        raise ValueError("give either radius or (fmin, fmax)")
+    return int(fmin), int(fmax)
+
+
+class QuantOut(NamedTuple):
+    codes: "torch.Tensor"            # [rows][cols/2] uint8
+    scales: "torch.Tensor"           # [rows][cols/16] uint8 (E4M3 codes)
+    err: "Optional[torch.Tensor]"    # [nb][2] float32 {best, base}
+    offsets: "Optional[torch.Tensor]"  # [nb] int8
+    sums: "Optional[torch.Tensor]"   # [2] float64
+    G: "Optional[torch.Tensor]"      # [1] float32
+
+
+def tensor_amax(x, out=None, accumulate: bool = False, stream=None):
+    """Device u32 tensor holding the FP32 bits of max|x| (ss_tensor_amax)."""
+    import torch
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous()
+    if out is None:
+        out = torch.zeros(1, dtype=torch.int32, device=x.device)
+    _check(lib().ss_tensor_amax(_ptr(x), x.numel(), _ptr(out), int(accumulate), _stream_ptr(stream)),
+           "ss_tensor_amax")
+    return out
+
+
+def quantize(x, radius=None, fmin=None, fmax=None, gmode: str = "tensor", amax=None,
+             want_err: bool = True, want_offsets: bool = True, want_sums: bool = True,
+             want_g: bool = True, out: Optional[QuantOut] = None, stream=None) -> QuantOut:
+    """ScaleSearch NVFP4 quantization of a [rows][cols] bf16 CUDA tensor (ss_quantize_nvfp4_ex)."""
+    import torch
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+    rows, cols = x.shape
+    lo, hi = _window(radius, fmin, fmax)
+    gm = GMODES[gmode]
+    if gm == 2 and amax is None:
+        raise ValueError("gmode='device_amax' needs amax (device int32/uint32 tensor)")
+    nb = rows * cols // 16
+    dev = x.device
+    if out is None:
+        out = QuantOut(
+            torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev),
+            torch.empty(rows, cols // 16, dtype=torch.uint8, device=dev),
+            torch.empty(nb, 2, dtype=torch.float32, device=dev) if want_err else None,
+            torch.empty(nb, dtype=torch.int8, device=dev) if want_offsets else None,
+            torch.empty(2, dtype=torch.float64, device=dev) if want_sums else None,
+            torch.empty(1, dtype=torch.float32, device=dev) if want_g else None,
+        )
+    a = QuantArgs(_ptr(x), rows, cols, lo, hi, gm, _ptr(amax), _ptr(out.codes), _ptr(out.scales),
+                  _ptr(out.err), _ptr(out.offsets), _ptr(out.sums), _ptr(out.G), _stream_ptr(stream))
+    _check(lib().ss_quantize_nvfp4_ex(ctypes.byref(a)), "ss_quantize_nvfp4_ex")
+    return out
+
+
+def quantize_simple(x, radius: int, gmode: str, codes, scales, err=None, stream=None):
+    """The three-output entry point of the north star (ss_quantize_nvfp4)."""
+    rows, cols = x.shape
+    _check(lib().ss_quantize_nvfp4(_ptr(x), rows, cols, int(radius), GMODES[gmode], _ptr(codes),
+                                   _ptr(scales), _ptr(err), _stream_ptr(stream)), "ss_quantize_nvfp4")
+
+
+def dequantize(codes, scales, rows: int, cols: int, G=None, out=None, stream=None):
+    """bf16 [rows][cols] reconstruction (ss_dequantize_nvfp4); G is a device f32[1] or None."""
+    import torch
+    if out is None:
+        out = torch.empty(rows, cols, dtype=torch.bfloat16, device=codes.device)
+    _check(lib().ss_dequantize_nvfp4(_ptr(codes), _ptr(scales), rows, cols, _ptr(G), _ptr(out),
+                                     _stream_ptr(stream)), "ss_dequantize_nvfp4")
+    return out
+
+
+def quantize_host(h_x, rows: int, cols: int, fmin: int, fmax: int, gmode: str,
+                  h_codes, h_scales, h_err=None):
+    """End to end from host memory (ss_quantize_nvfp4_host); synchronous."""
+    _check(lib().ss_quantize_nvfp4_host(_ptr(h_x), rows, cols, int(fmin), int(fmax), GMODES[gmode],
+                                        _ptr(h_codes), _ptr(h_scales), _ptr(h_err)),
+           "ss_quantize_nvfp4_host")
+
+
+def device_status(stream=None) -> int:
+    f = ctypes.c_int(0)
+    _check(lib().ss_get_device_status(ctypes.byref(f), _stream_ptr(stream)), "ss_get_device_status")
+    return f.value

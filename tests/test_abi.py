@@ -1,0 +1,82 @@
+"""The C-ABI library builds, loads and exports every symbol include/ss.h declares;
+argument errors are synchronous; without an sm_100 device nothing falls back."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ss.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2605_12464_b200 import build, _binding
+    build.build()
+    return _binding.lib()
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ss_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert {"ss_tensor_amax", "ss_quantize_nvfp4", "ss_dequantize_nvfp4"} <= set(names)
+    for n in names:
+        assert hasattr(L, n), n
+    nm = os.popen("nm -D --defined-only %s" % os.path.join(ROOT, "paper_2605_12464_b200", "libss.so")).read()
+    exported = set(re.findall(r"\bT (ss_\w+)", nm))
+    assert set(names) == exported, (set(names) ^ exported)
+
+
+def test_status_strings(L):
+    assert L.ss_version() == 100
+    for s in range(7):
+        assert L.ss_status_string(s)
+    assert L.ss_status_string(6).decode().startswith("unsupported device")
+
+
+def test_argument_errors_are_synchronous(L):
+    from paper_2605_12464_b200 import _binding as B
+    P = ctypes.c_void_p
+    buf = ctypes.create_string_buffer(1024 + 64)
+    base = (ctypes.addressof(buf) + 63) // 64 * 64
+    # cols % 16 != 0
+    assert L.ss_quantize_nvfp4(P(base), 4, 24, 8, 1, P(base), P(base), None, None) == B.SS_ERR_INVALID_ARG
+    # negative radius / rows
+    assert L.ss_quantize_nvfp4(P(base), 4, 32, -1, 1, P(base), P(base), None, None) == B.SS_ERR_INVALID_ARG
+    assert L.ss_quantize_nvfp4(P(base), -1, 32, 8, 1, P(base), P(base), None, None) == B.SS_ERR_INVALID_ARG
+    # null outputs
+    assert L.ss_quantize_nvfp4(P(base), 4, 32, 8, 1, None, P(base), None, None) == B.SS_ERR_INVALID_ARG
+    # misaligned input
+    assert L.ss_quantize_nvfp4(P(base + 2), 4, 32, 8, 1, P(base), P(base), None, None) == B.SS_ERR_ALIGNMENT
+    # f_min > 0 in the extended form; DEVICE_AMAX without a pointer
+    a = B.QuantArgs(base, 4, 32, 1, 8, 0, None, base, base, None, None, None, None, None)
+    assert L.ss_quantize_nvfp4_ex(ctypes.byref(a)) == B.SS_ERR_INVALID_ARG
+    a = B.QuantArgs(base, 4, 32, -2, 6, 2, None, base, base, None, None, None, None, None)
+    assert L.ss_quantize_nvfp4_ex(ctypes.byref(a)) == B.SS_ERR_INVALID_ARG
+    assert L.ss_tensor_amax(P(base), -5, P(base), 0, None) == B.SS_ERR_INVALID_ARG
+    assert L.ss_dequantize_nvfp4(P(base), P(base), 4, 20, None, P(base), None) == B.SS_ERR_INVALID_ARG
+
+
+@pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) is None and
+                    os.path.exists("/dev/nvidia0"), reason="a GPU is present")
+def test_no_fallback_without_device(L):
+    # valid arguments on a host without an sm_100 device: an error, never a CPU result
+    from paper_2605_12464_b200 import _binding as B
+    P = ctypes.c_void_p
+    buf = ctypes.create_string_buffer(4096)
+    base = (ctypes.addressof(buf) + 63) // 64 * 64
+    st = L.ss_quantize_nvfp4(P(base), 2, 32, 8, 1, P(base + 1024), P(base + 2048), None, None)
+    assert st == B.SS_ERR_UNSUPPORTED_DEVICE
+    assert L.ss_tensor_amax(P(base), 64, P(base + 1024), 0, None) == B.SS_ERR_UNSUPPORTED_DEVICE
+
+
+def test_binding_raises_not_falls_back():
+    from paper_2605_12464_b200 import _binding as B
+    e = B.SSError(B.SS_ERR_UNSUPPORTED_DEVICE, "x")
+    assert isinstance(e, RuntimeError)

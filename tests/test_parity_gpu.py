@@ -1,0 +1,240 @@
+"""GPU parity: libss.so (through the C ABI) against the CPU oracle, element by element.
+
+Bar: codes, scales, offsets and per-block errors bit-exact; the
+FP64 error sums within 1e-9 relative (north star asks 1e-6); every shape spans
+several 256-block CTA tiles plus a ragged tail.  Full-size configs are
+checked on sampled rows the oracle recomputes one by one, in the launch
+configuration bench.py times.
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import ssgen
+
+pytestmark = pytest.mark.gpu
+
+WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-2, 6), (-3, 3), (-4, 4), (-8, 8), (-16, 16), (-126, 126),
+           (-5, 0), (0, 5), (-12, 12)]
+
+
+@pytest.fixture(scope="module")
+def ss():
+    import paper_2605_12464_b200 as ss
+    from paper_2605_12464_b200 import build
+    build.build()
+    assert torch.cuda.is_available()
+    return ss
+
+
+def _cmp(gpu, ref, rows, cols, sums_tol=1e-9, check_err=True):
+    codes = gpu.codes.cpu().numpy()
+    scales = gpu.scales.cpu().numpy()
+    bad = np.argwhere(codes != ref.codes)
+    assert bad.size == 0, ("codes differ", bad[:5], codes[tuple(bad[0])], ref.codes[tuple(bad[0])])
+    assert np.array_equal(scales, ref.scales)
+    if gpu.offsets is not None:
+        assert np.array_equal(gpu.offsets.cpu().numpy(), ref.offsets)
+    if check_err and gpu.err is not None:
+        e = gpu.err.cpu().numpy()
+        assert np.array_equal(e.view(np.uint32), ref.err.view(np.uint32))
+    if gpu.sums is not None:
+        s = gpu.sums.cpu().numpy()
+        for k in range(2):
+            assert abs(s[k] - ref.sums[k]) <= sums_tol * abs(ref.sums[k]) + 1e-300
+    if gpu.G is not None:
+        assert gpu.G.cpu().numpy()[0] == np.float32(ref.G)
+
+
+def _run(ss, oracle_lib, x, fmin, fmax, gmode):
+    rows, cols = x.shape
+    g = ss.quantize(x.cuda(), fmin=fmin, fmax=fmax, gmode=gmode)
+    torch.cuda.synchronize()
+    ref = oracle_lib.quantize(x, rows, cols, fmin, fmax, gmode)
+    return g, ref
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "student_t", "weight_outlier", "kv_k"])
+@pytest.mark.parametrize("shape", [(37, 16), (129, 256), (300, 96), (64, 4096)])
+@pytest.mark.parametrize("gmode", ["none", "tensor"])
+def test_parity_small(ss, oracle_lib, kind, shape, gmode):
+    x = ssgen.generate(kind, *shape, seed=123, tid=zlib.crc32(repr((kind, shape)).encode()) & 0xFFFF)
+    for fmin, fmax in [(-8, 8), (0, 0), (-2, 6)]:
+        g, ref = _run(ss, oracle_lib, x, fmin, fmax, gmode)
+        _cmp(g, ref, *shape)
+
+
+@pytest.mark.parametrize("win", WINDOWS)
+def test_parity_windows(ss, oracle_lib, win):
+    x = ssgen.generate("gaussian", 333, 272, seed=5, tid=77)
+    for gmode in ("none", "tensor"):
+        g, ref = _run(ss, oracle_lib, x, win[0], win[1], gmode)
+        _cmp(g, ref, 333, 272)
+
+
+def test_parity_every_candidate_count(ss, oracle_lib):
+    # every compiled variant NC = 1..17, 25, 33 and the generic loop
+    x = ssgen.generate("student_t", 130, 160, seed=8, tid=3)
+    for nc in list(range(1, 20)) + [25, 33, 40, 127, 200, 253]:
+        fmin = -(nc // 2)
+        fmax = nc - 1 + fmin
+        g, ref = _run(ss, oracle_lib, x, max(fmin, -126), min(fmax, 126), "tensor")
+        _cmp(g, ref, 130, 160)
+
+
+def test_parity_adversarial(ss, oracle_lib):
+    x = ssgen.adversarial_rows()
+    rows, cols = x.shape
+    for gmode in ("none", "tensor"):
+        for win in [(0, 0), (-1, 1), (-8, 8), (-2, 6), (-126, 126)]:
+            g, ref = _run(ss, oracle_lib, x, win[0], win[1], gmode)
+            _cmp(g, ref, rows, cols)
+
+
+def test_parity_c1_full(ss, oracle_lib):
+    # configs[0]: 4096 x 4096 Gaussian, radius 8, both global-scale modes, full tensor
+    spec = ssgen.workload("c1_gauss4096")[0]
+    x = ssgen.generate(spec.kind, spec.rows, spec.cols, seed=ssgen.workloads.BASE_SEED, tid=spec.tid)
+    for gmode in ("tensor", "none"):
+        g, ref = _run(ss, oracle_lib, x, -8, 8, gmode)
+        _cmp(g, ref, spec.rows, spec.cols)
+        cut_g = 1 - g.sums[0].item() / g.sums[1].item()
+        cut_o = 1 - ref.sums[0] / ref.sums[1]
+        assert abs(cut_g - cut_o) <= 1e-6 * abs(cut_o)
+
+
+def test_empty_and_tiny(ss, oracle_lib):
+    x = torch.zeros(0, 64, dtype=torch.bfloat16, device="cuda")
+    out = ss.quantize(x, radius=8)
+    torch.cuda.synchronize()
+    assert out.codes.numel() == 0 and out.sums.cpu().tolist() == [0.0, 0.0]
+    x = ssgen.generate("gaussian", 1, 16, seed=1, tid=1)
+    g, ref = _run(ss, oracle_lib, x, -8, 8, "tensor")
+    _cmp(g, ref, 1, 16)
+
+
+def test_simple_entry_point(ss, oracle_lib):
+    x = ssgen.generate("weight_outlier", 96, 512, seed=2, tid=2)
+    xc = x.cuda()
+    codes = torch.empty(96, 256, dtype=torch.uint8, device="cuda")
+    scales = torch.empty(96, 32, dtype=torch.uint8, device="cuda")
+    err = torch.empty(96 * 32, 2, dtype=torch.float32, device="cuda")
+    ss.quantize_simple(xc, 8, "tensor", codes, scales, err)
+    torch.cuda.synchronize()
+    ref = oracle_lib.quantize(x, 96, 512, -8, 8, "tensor")
+    assert np.array_equal(codes.cpu().numpy(), ref.codes)
+    assert np.array_equal(scales.cpu().numpy(), ref.scales)
+    assert np.array_equal(err.cpu().numpy().view(np.uint32), ref.err.view(np.uint32))
+
+
+def test_amax(ss, oracle_lib):
+    for n in (1, 7, 8, 9, 4095, 1 << 20, (1 << 20) + 5):
+        x = ssgen.generate("student_t", 1, n, seed=n, tid=9).reshape(-1)
+        a = ss.tensor_amax(x.cuda())
+        torch.cuda.synchronize()
+        assert (a.cpu().numpy().view(np.uint32)[0]) == oracle_lib.tensor_amax(x)
+    # accumulate over two halves == whole
+    x = ssgen.generate("gaussian", 64, 1024, seed=3, tid=3).cuda()
+    a = ss.tensor_amax(x[:20].contiguous())
+    ss.tensor_amax(x[20:].contiguous(), out=a, accumulate=True)
+    torch.cuda.synchronize()
+    assert a.cpu().numpy().view(np.uint32)[0] == oracle_lib.tensor_amax(x.cpu())
+
+
+def test_device_amax_mode_matches_tensor(ss, oracle_lib):
+    x = ssgen.generate("kv_k", 512, 128, seed=4, tid=4).cuda()
+    a = ss.tensor_amax(x)
+    g1 = ss.quantize(x, radius=8, gmode="tensor")
+    g2 = ss.quantize(x, radius=8, gmode="device_amax", amax=a)
+    torch.cuda.synchronize()
+    assert torch.equal(g1.codes, g2.codes) and torch.equal(g1.scales, g2.scales)
+    assert torch.equal(g1.G, g2.G)
+
+
+def test_nonfinite_and_range_flags(ss):
+    ss.device_status()  # clear
+    x = torch.ones(8, 32, dtype=torch.bfloat16, device="cuda")
+    x[3, 5] = float("nan")
+    ss.quantize(x, radius=8, gmode="tensor")
+    assert ss.device_status() & ss.FLAG_NONFINITE
+    assert ss.device_status() == 0  # cleared
+    y = torch.zeros(8, 32, dtype=torch.int16, device="cuda")
+    y[0, 0] = 1  # smallest bf16 subnormal: 2688 / 2^-133 overflows binary32
+    ss.quantize(y.view(torch.bfloat16), radius=8, gmode="tensor")
+    assert ss.device_status() & ss.FLAG_RANGE
+
+
+def test_dequantize_parity(ss, oracle_lib):
+    x = ssgen.generate("student_t", 257, 96, seed=6, tid=6)
+    g = ss.quantize(x.cuda(), radius=8, gmode="tensor")
+    d = ss.dequantize(g.codes, g.scales, 257, 96, g.G)
+    torch.cuda.synchronize()
+    ref = oracle_lib.quantize(x, 257, 96, -8, 8, "tensor")
+    rd = oracle_lib.dequantize(ref.codes, ref.scales, 257, 96, ref.G)
+    assert np.array_equal(d.cpu().view(torch.int16).numpy().view(np.uint16), rd)
+
+
+def test_host_entry_point(ss, oracle_lib):
+    rows, cols = 1000, 4096
+    x = ssgen.generate("weight_outlier", rows, cols, seed=7, tid=7)
+    hx = x.pin_memory()
+    for gmode in ("tensor", "none"):
+        hc = torch.empty(rows, cols // 2, dtype=torch.uint8).pin_memory()
+        hs = torch.empty(rows, cols // 16, dtype=torch.uint8).pin_memory()
+        he = torch.empty(rows * cols // 16, 2, dtype=torch.float32).pin_memory()
+        ss.quantize_host(hx, rows, cols, -8, 8, gmode, hc, hs, he)
+        ref = oracle_lib.quantize(x, rows, cols, -8, 8, gmode)
+        assert np.array_equal(hc.numpy(), ref.codes)
+        assert np.array_equal(hs.numpy(), ref.scales)
+        assert np.array_equal(he.numpy().view(np.uint32), ref.err.view(np.uint32))
+
+
+def _sampled_rows_check(ss, oracle_lib, spec, fmin=-8, fmax=8, nrows=64, seed=0):
+    """Full-size tensor on the GPU, oracle on sampled rows with the oracle's own amax."""
+    x = ssgen.generate(spec.kind, spec.rows, spec.cols, seed=ssgen.workloads.BASE_SEED,
+                       tid=spec.tid, device="cuda")
+    g = ss.quantize(x, fmin=fmin, fmax=fmax, gmode="tensor")
+    torch.cuda.synchronize()
+    xh = x.cpu()
+    amax = oracle_lib.tensor_amax(xh)
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([[0, spec.rows - 1], rng.integers(0, spec.rows, nrows)]))
+    sub = xh[torch.from_numpy(rows)].contiguous()
+    ref = oracle_lib.quantize(sub, len(rows), spec.cols, fmin, fmax, "given", amax_bits=amax)
+    r_t = torch.from_numpy(rows).cuda()
+    assert np.array_equal(g.codes[r_t].cpu().numpy(), ref.codes)
+    assert np.array_equal(g.scales[r_t].cpu().numpy(), ref.scales)
+    nbr = spec.cols // 16
+    blk = (rows[:, None] * nbr + np.arange(nbr)[None, :]).ravel()
+    e = g.err.cpu().numpy()[blk]
+    assert np.array_equal(e.view(np.uint32), ref.err.view(np.uint32))
+    assert g.G.item() == np.float32(ref.G)
+    s = g.sums.cpu().numpy()
+    assert s[0] <= s[1]                                   # dominance holds at any size
+    return g
+
+
+def test_full_size_c3_sampled(ss, oracle_lib):
+    spec = ssgen.workload("c3_act_student_t")[0]
+    for win in [(0, 0), (-8, 8), (-16, 16)]:
+        _sampled_rows_check(ss, oracle_lib, spec, *win, nrows=32)
+
+
+def test_full_size_c2_sampled(ss, oracle_lib):
+    specs = ssgen.workload("c2_qwen3_8b_weights")
+    for spec in (specs[1], specs[4], specs[6], specs[-1]):   # k, gate, down, last down
+        _sampled_rows_check(ss, oracle_lib, spec, nrows=24)
+
+
+def test_full_size_c4_sampled(ss, oracle_lib):
+    specs = ssgen.workload("c4_llama70b_kv")
+    for spec in (specs[0], specs[1], specs[-1]):
+        _sampled_rows_check(ss, oracle_lib, spec, nrows=48)
+
+
+def test_full_size_c5_sampled(ss, oracle_lib):
+    spec = ssgen.workload("c5_gauss_1gib")[0]
+    for win in [(0, 0), (-8, 8), (-126, 126)]:
+        _sampled_rows_check(ss, oracle_lib, spec, *win, nrows=8)
