@@ -99,6 +99,17 @@ SS_API ss_status ss_tensor_amax(const void* in_bf16, int64_t n, uint32_t* d_amax
                          int accumulate, void* stream);
 
 /*
+ * Batched global amax: d_amax_bits[i] = max|x| of tensor i (same semantics as
+ * ss_tensor_amax), for `count` tensors in ONE launch (per launch at most 128
+ * tensors; more are split into several launches).  in_bf16[i] / n[i] are HOST
+ * arrays of device pointers / element counts; d_amax_bits is a device array
+ * of `count` u32.  This is the per-shard half of the multi-GPU exchange step:
+ * the slots can go straight into one NCCL max all-reduce.
+ */
+SS_API ss_status ss_tensor_amax_batched(const void* const* in_bf16, const int64_t* n, int count,
+                                 uint32_t* d_amax_bits, int accumulate, void* stream);
+
+/*
  * ScaleSearch quantization with a symmetric window f in [-radius, radius]
  * (north star; radius > 126 is clamped to 126 = exhaustive search).
  *   in_bf16     [rows][cols] bf16, 16-B aligned, cols % 16 == 0, rows >= 0
@@ -128,12 +139,36 @@ typedef struct {
   float* out_err;               /* nullable: [nb][2] f32 {err_best, err_base}, 8-B aligned  */
   int8_t* out_offset;           /* nullable: [nb] f* = c* - c0 (R5)                          */
   double* d_err_sums;           /* nullable: device f64[2] = {sum err_best, sum err_base},  */
-                                /* overwritten; fixed-order reduction (deterministic)       */
+                                /* overwritten; fixed-order two-level reduction of per-32-  */
+                                /* block partials: deterministic for any grid               */
   float* d_global_scale;        /* nullable: device f32 receives G (for dequantization)     */
   void* stream;
 } ss_quant_args;
 
 SS_API ss_status ss_quantize_nvfp4_ex(const ss_quant_args* args);
+
+/* One tensor of a batched call; fields as in ss_quant_args. */
+typedef struct {
+  const void* in_bf16;          /* [rows][cols] bf16, 16-B aligned                         */
+  int64_t rows, cols;           /* rows >= 0, cols % 16 == 0                                */
+  const uint32_t* d_amax_bits;  /* SS_GLOBAL_DEVICE_AMAX: device u32 amax bits of THIS tensor */
+  uint8_t* out_codes;           /* [rows][cols/2] u8, 8-B aligned                           */
+  uint8_t* out_scales;          /* [rows][cols/16] u8                                       */
+  float* out_err;               /* nullable: [nb][2] f32 {err_best, err_base}, 8-B aligned  */
+  int8_t* out_offset;           /* nullable: [nb] f* = c* - c0                               */
+  double* d_err_sums;           /* nullable: device f64[2] of THIS tensor, overwritten      */
+  float* d_global_scale;        /* nullable: device f32 receives this tensor's G            */
+} ss_tensor_io;
+
+/*
+ * Batched ScaleSearch quantization: every tensor of `tensors[0..count)` (a
+ * HOST array) with one window and one global-scale mode, in as few launches
+ * as possible (one persistent grid per 128 tensors, so a step over many
+ * small tensors has no per-tensor tail).  SS_GLOBAL_TENSOR runs one batched
+ * amax launch first.  Results are bit-identical to per-tensor calls.
+ */
+SS_API ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min,
+                                    int f_max, int global_scale_mode, void* stream);
 
 /*
  * Dequantization (step a8): xhat = RNE_bf16(RN((q * s) / G)).

@@ -12,17 +12,20 @@ from ._binding import (  # noqa: F401
     LIB_PATH,
     QuantOut,
     SSError,
+    alloc_out,
     dequantize,
     device_status,
     lib,
     quantize,
+    quantize_batched,
     quantize_host,
     quantize_simple,
     status_string,
     tensor_amax,
+    tensor_amax_batched,
 )
 
 __all__ = [
-    "lib", "tensor_amax", "quantize", "quantize_simple", "dequantize", "quantize_host",
+    "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host",
     "device_status", "status_string", "SSError", "QuantOut", "GMODES",
 ]

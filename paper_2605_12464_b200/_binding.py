@@ -12,7 +12,10 @@ import threading
 from typing import NamedTuple, Optional
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libss.so")
+# SS_LIB_VARIANT selects an alternative in-tree build of the same library
+# (tools/kbench.py compiles kernel-tuning variants as libss_<variant>.so).
+LIB_PATH = os.path.join(PKG, "libss%s.so" % (("_" + os.environ["SS_LIB_VARIANT"])
+                                              if os.environ.get("SS_LIB_VARIANT") else ""))
 
 SS_OK, SS_ERR_INVALID_ARG, SS_ERR_ALIGNMENT, SS_ERR_CUDA = 0, 1, 2, 3
 SS_ERR_NONFINITE, SS_ERR_RANGE, SS_ERR_UNSUPPORTED_DEVICE = 4, 5, 6
@@ -28,6 +31,21 @@ class SSError(RuntimeError):
         self.status = status
         msg = "libss: %s" % (status_string(status) if _lib is not None else "status %d" % status)
         super().__init__(msg + (" (%s)" % what if what else ""))
+
+
+class TensorIO(ctypes.Structure):
+    _fields_ = [
+        ("in_bf16", ctypes.c_void_p),
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("d_amax_bits", ctypes.c_void_p),
+        ("out_codes", ctypes.c_void_p),
+        ("out_scales", ctypes.c_void_p),
+        ("out_err", ctypes.c_void_p),
+        ("out_offset", ctypes.c_void_p),
+        ("d_err_sums", ctypes.c_void_p),
+        ("d_global_scale", ctypes.c_void_p),
+    ]
 
 
 class QuantArgs(ctypes.Structure):
@@ -67,6 +85,10 @@ def lib():
             L.ss_tensor_amax.argtypes = [P, i64, P, I, P]
             L.ss_quantize_nvfp4.restype = I
             L.ss_quantize_nvfp4.argtypes = [P, i64, i64, I, I, P, P, P, P]
+            L.ss_tensor_amax_batched.restype = I
+            L.ss_tensor_amax_batched.argtypes = [P, P, I, P, I, P]
+            L.ss_quantize_nvfp4_batched.restype = I
+            L.ss_quantize_nvfp4_batched.argtypes = [ctypes.POINTER(TensorIO), I, I, I, I, P]
             L.ss_quantize_nvfp4_ex.restype = I
             L.ss_quantize_nvfp4_ex.argtypes = [ctypes.POINTER(QuantArgs)]
             L.ss_dequantize_nvfp4.restype = I
@@ -141,21 +163,66 @@ def quantize(x, radius=None, fmin=None, fmax=None, gmode: str = "tensor", amax=N
     gm = GMODES[gmode]
     if gm == 2 and amax is None:
         raise ValueError("gmode='device_amax' needs amax (device int32/uint32 tensor)")
-    nb = rows * cols // 16
-    dev = x.device
     if out is None:
-        out = QuantOut(
-            torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev),
-            torch.empty(rows, cols // 16, dtype=torch.uint8, device=dev),
-            torch.empty(nb, 2, dtype=torch.float32, device=dev) if want_err else None,
-            torch.empty(nb, dtype=torch.int8, device=dev) if want_offsets else None,
-            torch.empty(2, dtype=torch.float64, device=dev) if want_sums else None,
-            torch.empty(1, dtype=torch.float32, device=dev) if want_g else None,
-        )
+        out = alloc_out(x, want_err, want_offsets, want_sums, want_g)
     a = QuantArgs(_ptr(x), rows, cols, lo, hi, gm, _ptr(amax), _ptr(out.codes), _ptr(out.scales),
                   _ptr(out.err), _ptr(out.offsets), _ptr(out.sums), _ptr(out.G), _stream_ptr(stream))
     _check(lib().ss_quantize_nvfp4_ex(ctypes.byref(a)), "ss_quantize_nvfp4_ex")
     return out
+
+
+def tensor_amax_batched(xs, out=None, accumulate: bool = False, stream=None):
+    """Device int32 [len(xs)] of FP32 amax bits, one launch (ss_tensor_amax_batched)."""
+    import torch
+    n = len(xs)
+    for x in xs:
+        assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous()
+    if out is None:
+        out = torch.zeros(n, dtype=torch.int32, device=xs[0].device if n else "cuda")
+    ptrs = (ctypes.c_void_p * max(n, 1))(*[x.data_ptr() for x in xs])
+    ns = (ctypes.c_int64 * max(n, 1))(*[x.numel() for x in xs])
+    _check(lib().ss_tensor_amax_batched(ptrs, ns, n, _ptr(out), int(accumulate), _stream_ptr(stream)),
+           "ss_tensor_amax_batched")
+    return out
+
+
+def alloc_out(x, want_err=True, want_offsets=True, want_sums=True, want_g=True) -> QuantOut:
+    import torch
+    rows, cols = x.shape
+    nb = rows * cols // 16
+    dev = x.device
+    return QuantOut(
+        torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev),
+        torch.empty(rows, cols // 16, dtype=torch.uint8, device=dev),
+        torch.empty(nb, 2, dtype=torch.float32, device=dev) if want_err else None,
+        torch.empty(nb, dtype=torch.int8, device=dev) if want_offsets else None,
+        torch.empty(2, dtype=torch.float64, device=dev) if want_sums else None,
+        torch.empty(1, dtype=torch.float32, device=dev) if want_g else None,
+    )
+
+
+def quantize_batched(xs, outs, radius=None, fmin=None, fmax=None, gmode: str = "tensor",
+                     amax=None, stream=None):
+    """All tensors of ``xs`` into ``outs`` (QuantOut each) in one call
+    (ss_quantize_nvfp4_batched).  ``amax``: device int32 [len(xs)] for
+    gmode='device_amax' (e.g. after the NCCL max all-reduce)."""
+    import torch
+    lo, hi = _window(radius, fmin, fmax)
+    gm = GMODES[gmode]
+    n = len(xs)
+    if gm == 2:
+        if amax is None or amax.numel() < n:
+            raise ValueError("gmode='device_amax' needs amax with one slot per tensor")
+    arr = (TensorIO * max(n, 1))()
+    for i, (x, o) in enumerate(zip(xs, outs)):
+        assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+        rows, cols = x.shape
+        arr[i] = TensorIO(_ptr(x), rows, cols, amax.data_ptr() + 4 * i if gm == 2 else None,
+                          _ptr(o.codes), _ptr(o.scales), _ptr(o.err), _ptr(o.offsets), _ptr(o.sums),
+                          _ptr(o.G))
+    _check(lib().ss_quantize_nvfp4_batched(arr, n, lo, hi, gm, _stream_ptr(stream)),
+           "ss_quantize_nvfp4_batched")
+    return outs
 
 
 def quantize_simple(x, radius: int, gmode: str, codes, scales, err=None, stream=None):

@@ -32,28 +32,37 @@ def _deps():
     return files
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def lib_path(variant: str | None = None) -> str:
+    return LIB if not variant else os.path.join(PKG, "libss_%s.so" % variant)
+
+
+def up_to_date(path: str = LIB) -> bool:
+    if not os.path.exists(path):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(path)
     return all(os.path.getmtime(f) <= t for f in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if up_to_date() and not force:
-        return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp, *sources()]
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines=()) -> str:
+    """Compile libss.so; ``variant`` + ``defines`` build a tuning variant
+    libss_<variant>.so of the same sources (tools/kbench.py)."""
+    out = lib_path(variant)
+    if up_to_date(out) and not force:
+        return out
+    tmp = out + ".tmp%d" % os.getpid()
+    cmd = ["nvcc", *NVCC_FLAGS, *["-D" + d for d in defines], "-I", INCLUDE, "-I", CSRC,
+           "-o", tmp, *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libss.so")
-    with open(os.path.join(PKG, "build_ptxas.log"), "w") as f:
+    with open(os.path.join(PKG, "build_ptxas%s.log" % ("_" + variant if variant else "")), "w") as f:
         f.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

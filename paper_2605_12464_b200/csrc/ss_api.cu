@@ -1,9 +1,9 @@
 // ss_api.cu — host side of libss.so: the C ABI declared in include/ss.h.
 //
-// Argument validation, per-(device, stream) workspace, kernel-variant
-// dispatch by candidate count, the end-to-end host-buffer pipeline, and
-// status reporting.  No CPU compute path exists: every entry point either
-// launches sm_100a kernels or returns an error.
+// Argument validation, per-(device, stream) workspace, batching of tensors
+// into launches, kernel-variant dispatch by search window, the end-to-end
+// host-buffer pipeline, and status reporting.  No CPU compute path exists:
+// every entry point either launches sm_100a kernels or returns an error.
 #include "ss.h"
 #include "ss_kernels.cuh"
 
@@ -14,18 +14,27 @@
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
 
 namespace {
 
-using ss::Cand;
-using ss::QuantParams;
+using ss::AmaxBatch;
+using ss::ATensor;
+using ss::QTensor;
+using ss::QuantBatch;
 
+// ---- per-(device, stream) workspace -----------------------------------------
 struct Workspace {
-  uint32_t* amax = nullptr;     // SS_GLOBAL_TENSOR slot
-  uint32_t* flags = nullptr;    // sticky status flags
-  uint32_t* ticket = nullptr;   // last-CTA reduction counter (self re-arming)
-  double2* partials = nullptr;  // per-CTA error partial sums
-  int partial_cap = 0;
+  uint32_t* flags = nullptr;     // sticky status flags (1 word)
+  uint32_t* tick2 = nullptr;     // [kMaxTensors] per-tensor tickets (zero, self re-arming)
+  uint32_t* amax = nullptr;      // SS_GLOBAL_TENSOR slots
+  int64_t amax_cap = 0;
+  double2* part1 = nullptr;      // per-task partial sums
+  int64_t part1_cap = 0;
+  double2* part2 = nullptr;      // per-group partial sums
+  int64_t part2_cap = 0;
+  uint32_t* tick1 = nullptr;     // per-group tickets (zero, self re-arming)
+  int64_t group_cap = 0;
 };
 
 std::mutex g_mu;
@@ -60,24 +69,36 @@ ss_status device_check(int* dev_out, DeviceInfo* info_out) {
   return SS_OK;
 }
 
-ss_status get_ws(int dev, void* stream, int need_partials, Workspace** out) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  Workspace& w = g_ws[std::make_pair(dev, stream)];
-  if (!w.amax) {
-    void* p = nullptr;
-    if (cudaMalloc(&p, 64) != cudaSuccess) return SS_ERR_CUDA;
-    if (cudaMemset(p, 0, 64) != cudaSuccess) return SS_ERR_CUDA;
-    w.amax = reinterpret_cast<uint32_t*>(p);
-    w.flags = w.amax + 1;
-    w.ticket = w.amax + 2;
+// Grow a device array; a buffer that may still be in use by queued kernels is
+// released only after the stream drains.  `zero` clears the new buffer (on the
+// stream, before any later kernel).
+template <typename T>
+ss_status grow_dev(T** p, int64_t* cap, int64_t need, bool zero, cudaStream_t st) {
+  if (need <= *cap) return SS_OK;
+  const int64_t n = std::max<int64_t>(need, std::max<int64_t>(2 * *cap, 1024));
+  if (*p) {
+    if (cudaStreamSynchronize(st) != cudaSuccess) return SS_ERR_CUDA;
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
   }
-  if (need_partials > w.partial_cap) {
-    if (w.partials) cudaFree(w.partials);
+  void* q = nullptr;
+  if (cudaMalloc(&q, sizeof(T) * n) != cudaSuccess) return SS_ERR_CUDA;
+  if (zero && cudaMemsetAsync(q, 0, sizeof(T) * n, st) != cudaSuccess) return SS_ERR_CUDA;
+  *p = reinterpret_cast<T*>(q);
+  *cap = n;
+  return SS_OK;
+}
+
+ss_status get_ws(int dev, void* stream, Workspace** out) {
+  Workspace& w = g_ws[std::make_pair(dev, stream)];
+  if (!w.flags) {
     void* p = nullptr;
-    int cap = std::max(need_partials, 4096);
-    if (cudaMalloc(&p, sizeof(double2) * cap) != cudaSuccess) return SS_ERR_CUDA;
-    w.partials = reinterpret_cast<double2*>(p);
-    w.partial_cap = cap;
+    const size_t bytes = sizeof(uint32_t) * (1 + ss::kMaxTensors);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return SS_ERR_CUDA;
+    if (cudaMemset(p, 0, bytes) != cudaSuccess) return SS_ERR_CUDA;
+    w.flags = reinterpret_cast<uint32_t*>(p);
+    w.tick2 = w.flags + 1;
   }
   *out = &w;
   return SS_OK;
@@ -90,35 +111,68 @@ ss_status launch_status() {
   return e == cudaSuccess ? SS_OK : SS_ERR_CUDA;
 }
 
-ss_status amax_launch(const void* in, int64_t n, uint32_t* d_amax, bool accumulate,
-                      cudaStream_t st, int sms) {
-  if (!accumulate && cudaMemsetAsync(d_amax, 0, 4, st) != cudaSuccess) return SS_ERR_CUDA;
-  if (n == 0) return SS_OK;
-  const int64_t n16 = n / 8;
-  const int n_tail = (int)(n % 8);
-  const uint16_t* tail = reinterpret_cast<const uint16_t*>(in) + n16 * 8;
-  int64_t want = (n16 + 255) / 256;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-  ss::amax_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(in), n16, tail, n_tail,
-                                        d_amax);
-  return launch_status();
+// ---- amax --------------------------------------------------------------------
+int amax_grid(int sms) {
+  static int occ = 0;
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ss::amax_kernel, ss::kThreads, 0) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      occ = 4;
+    }
+    occ = std::max(occ, 1);
+  }
+  return sms * occ;
 }
 
-// ---- quantize kernel variants ----------------------------------------------
-typedef void (*QuantKernel)(QuantParams);
-
-template <int NC>
-QuantKernel kernel_for() { return ss::quant_kernel<NC>; }
-
-QuantKernel pick_kernel(int nc) {
-  switch (nc) {
-#define SS_CASE(N) case N: return kernel_for<N>();
-    SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
-    SS_CASE(9) SS_CASE(10) SS_CASE(11) SS_CASE(12) SS_CASE(13) SS_CASE(14) SS_CASE(15)
-    SS_CASE(16) SS_CASE(17) SS_CASE(25) SS_CASE(33)
-#undef SS_CASE
-    default: return kernel_for<0>();
+// Launch the batched amax over `count` tensors into the device slots out[0..count).
+ss_status amax_launch(const void* const* in, const int64_t* n, uint32_t* out, int count,
+                      bool accumulate, cudaStream_t st, int sms) {
+  if (!accumulate && count > 0 && cudaMemsetAsync(out, 0, 4 * (size_t)count, st) != cudaSuccess)
+    return SS_ERR_CUDA;
+  int i = 0;
+  while (i < count) {
+    AmaxBatch b;
+    std::memset(&b, 0, sizeof(b));
+    int64_t chunks = 0;
+    for (; i < count && b.n < ss::kMaxTensors; i++) {
+      if (n[i] == 0) continue;
+      ATensor& t = b.t[b.n++];
+      t.in = reinterpret_cast<const uint4*>(in[i]);
+      t.nvec = n[i] / 8;
+      t.ntail = (int)(n[i] % 8);
+      t.chunk0 = chunks;
+      t.out = out + i;
+      const int64_t full = t.nvec / ss::kAmaxChunk;
+      chunks += full + ((t.nvec % ss::kAmaxChunk) || t.ntail ? 1 : 0);
+    }
+    if (b.n == 0) break;
+    b.nchunks = chunks;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, amax_grid(sms)));
+    ss::amax_kernel<<<grid, ss::kThreads, 0, st>>>(b);
+    if (ss_status s = launch_status()) return s;
   }
+  return SS_OK;
+}
+
+// ---- quantize kernel variants --------------------------------------------------
+typedef void (*QuantKernel)(QuantBatch);
+
+template <int NEG, int POS>
+QuantKernel qk() { return ss::quant_kernel<NEG, POS>; }
+
+QuantKernel pick_kernel(int fmin, int fmax) {
+  if (fmin == -fmax) {
+    switch (fmax) {
+#define SS_SYM(R) case R: return qk<R, R>();
+      SS_SYM(0) SS_SYM(1) SS_SYM(2) SS_SYM(3) SS_SYM(4) SS_SYM(5) SS_SYM(6) SS_SYM(7) SS_SYM(8)
+      SS_SYM(9) SS_SYM(10) SS_SYM(11) SS_SYM(12) SS_SYM(13) SS_SYM(14) SS_SYM(15) SS_SYM(16)
+#undef SS_SYM
+      default: break;
+    }
+  }
+  if (fmin == -2 && fmax == 6) return qk<2, 6>();  // the paper's production window
+  return qk<-1, -1>();
 }
 
 int occupancy(QuantKernel k) {
@@ -137,60 +191,148 @@ int occupancy(QuantKernel k) {
   return occ;
 }
 
-ss_status quantize_impl(const ss_quant_args* a) {
-  if (!a) return SS_ERR_INVALID_ARG;
-  if (a->rows < 0 || a->cols < 0 || (a->cols % 16) != 0) return SS_ERR_INVALID_ARG;
-  if (a->f_min > 0 || a->f_max < 0) return SS_ERR_INVALID_ARG;
-  if (a->global_scale_mode < 0 || a->global_scale_mode > 2) return SS_ERR_INVALID_ARG;
-  if (a->global_scale_mode == SS_GLOBAL_DEVICE_AMAX && !a->d_amax_bits) return SS_ERR_INVALID_ARG;
-  const int64_t n = a->rows * a->cols, nb = n / 16;
-  if (nb > 0 && (!a->in_bf16 || !a->out_codes || !a->out_scales)) return SS_ERR_INVALID_ARG;
-  if (!aligned(a->in_bf16, 16) || !aligned(a->out_codes, 8) || !aligned(a->out_err, 8))
+inline int64_t tasks_of(int64_t nb) { return (nb + ss::kTaskBlocks - 1) / ss::kTaskBlocks; }
+inline int64_t groups_of(int64_t nb) {
+  return (tasks_of(nb) + ss::kGroupTasks - 1) / ss::kGroupTasks;
+}
+
+ss_status validate_io(const ss_tensor_io& t, int gmode) {
+  if (t.rows < 0 || t.cols < 0 || (t.cols % 16) != 0) return SS_ERR_INVALID_ARG;
+  const int64_t nb = t.rows * t.cols / 16;
+  if (nb > 0 && (!t.in_bf16 || !t.out_codes || !t.out_scales)) return SS_ERR_INVALID_ARG;
+  if (gmode == SS_GLOBAL_DEVICE_AMAX && !t.d_amax_bits) return SS_ERR_INVALID_ARG;
+  if (!aligned(t.in_bf16, 16) || !aligned(t.out_codes, 8) || !aligned(t.out_err, 8) ||
+      !aligned(t.d_err_sums, 8) || !aligned(t.d_amax_bits, 4) || !aligned(t.d_global_scale, 4))
     return SS_ERR_ALIGNMENT;
+  return SS_OK;
+}
+
+// The one quantization path behind every entry point.
+ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
+                        void* stream) {
+  if (count < 0 || (count > 0 && !io)) return SS_ERR_INVALID_ARG;
+  if (f_min > 0 || f_max < 0) return SS_ERR_INVALID_ARG;
+  if (gmode < SS_GLOBAL_NONE || gmode > SS_GLOBAL_DEVICE_AMAX) return SS_ERR_INVALID_ARG;
+  for (int i = 0; i < count; i++)
+    if (ss_status s = validate_io(io[i], gmode)) return s;
   int dev;
   DeviceInfo info;
-  ss_status st = device_check(&dev, &info);
-  if (st) return st;
-  const int fmin = std::max(a->f_min, -126), fmax = std::min(a->f_max, 126);
-  const int nc = fmax - fmin + 1;
-  QuantKernel k = pick_kernel(nc);
-  const int occ = occupancy(k);
-  int64_t want = (nb + ss::kThreads - 1) / ss::kThreads;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)info.sms * occ));
+  if (ss_status s = device_check(&dev, &info)) return s;
+  if (count == 0) return SS_OK;
+  const int fmin = std::max(f_min, -126), fmax = std::min(f_max, 126);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
 
+  std::lock_guard<std::mutex> lk(g_mu);
   Workspace* ws = nullptr;
-  st = get_ws(dev, a->stream, a->d_err_sums ? grid : 0, &ws);
-  if (st) return st;
-  cudaStream_t cs = reinterpret_cast<cudaStream_t>(a->stream);
+  if (ss_status s = get_ws(dev, stream, &ws)) return s;
 
-  const uint32_t* amax = a->d_amax_bits;
-  if (a->global_scale_mode == SS_GLOBAL_TENSOR) {
-    st = amax_launch(a->in_bf16, n, ws->amax, false, cs, info.sms);
-    if (st) return st;
-    amax = ws->amax;
+  // sizes of the largest launch (workspace grown once, before any launch)
+  int64_t max_tasks = 0, max_groups = 0;
+  bool any_sums = false;
+  {
+    int64_t tk = 0, gr = 0;
+    int in_batch = 0;
+    for (int i = 0; i < count; i++) {
+      const int64_t nb = io[i].rows * io[i].cols / 16;
+      if (nb == 0) continue;
+      if (in_batch == ss::kMaxTensors) {
+        max_tasks = std::max(max_tasks, tk);
+        max_groups = std::max(max_groups, gr);
+        tk = gr = 0;
+        in_batch = 0;
+      }
+      tk += tasks_of(nb);
+      gr += groups_of(nb);
+      in_batch++;
+      any_sums |= io[i].d_err_sums != nullptr;
+    }
+    max_tasks = std::max(max_tasks, tk);
+    max_groups = std::max(max_groups, gr);
   }
-  if (nb == 0) {
-    if (a->d_err_sums && cudaMemsetAsync(a->d_err_sums, 0, 16, cs) != cudaSuccess) return SS_ERR_CUDA;
-    return SS_OK;
+  if (any_sums) {
+    if (ss_status s = grow_dev(&ws->part1, &ws->part1_cap, max_tasks, false, cs)) return s;
+    if (ss_status s = grow_dev(&ws->part2, &ws->part2_cap, max_groups, false, cs)) return s;
+    if (ss_status s = grow_dev(&ws->tick1, &ws->group_cap, max_groups, true, cs)) return s;
   }
-  QuantParams p;
-  p.in = reinterpret_cast<const uint4*>(a->in_bf16);
-  p.nb = nb;
-  p.fmin = fmin;
-  p.fmax = fmax;
-  p.gmode = a->global_scale_mode == SS_GLOBAL_NONE ? 0 : 1;
-  p.amax_bits = amax ? amax : ws->amax;
-  p.codes = reinterpret_cast<uint2*>(a->out_codes);
-  p.scales = a->out_scales;
-  p.offsets = a->out_offset;
-  p.err = reinterpret_cast<float2*>(a->out_err);
-  p.partials = a->d_err_sums ? ws->partials : nullptr;
-  p.sums = a->d_err_sums;
-  p.ticket = ws->ticket;
-  p.g_out = a->d_global_scale;
-  p.flags = ws->flags;
-  k<<<grid, ss::kThreads, 0, cs>>>(p);
-  return launch_status();
+
+  // SS_GLOBAL_TENSOR: the amax pass of every tensor first (a2)
+  std::vector<const uint32_t*> amax(count, nullptr);
+  if (gmode == SS_GLOBAL_TENSOR) {
+    if (ss_status s = grow_dev(&ws->amax, &ws->amax_cap, count, false, cs)) return s;
+    std::vector<const void*> ins(count);
+    std::vector<int64_t> ns(count);
+    for (int i = 0; i < count; i++) {
+      ins[i] = io[i].in_bf16;
+      ns[i] = io[i].rows * io[i].cols;
+      amax[i] = ws->amax + i;
+    }
+    if (ss_status s = amax_launch(ins.data(), ns.data(), ws->amax, count, false, cs, info.sms))
+      return s;
+  } else if (gmode == SS_GLOBAL_DEVICE_AMAX) {
+    for (int i = 0; i < count; i++) amax[i] = io[i].d_amax_bits;
+  }
+
+  QuantKernel k = pick_kernel(fmin, fmax);
+  const int64_t slots = (int64_t)info.sms * occupancy(k);
+  int i = 0;
+  while (i < count) {
+    QuantBatch b;
+    std::memset(&b, 0, sizeof(b));
+    b.fmin = fmin;
+    b.fmax = fmax;
+    b.gmode = gmode == SS_GLOBAL_NONE ? 0 : 1;
+    b.part1 = ws->part1;
+    b.part2 = ws->part2;
+    b.tick1 = ws->tick1;
+    b.tick2 = ws->tick2;
+    b.flags = ws->flags;
+    int64_t tk = 0, gr = 0;
+    for (; i < count && b.n < ss::kMaxTensors; i++) {
+      const ss_tensor_io& t = io[i];
+      const int64_t nb = t.rows * t.cols / 16;
+      if (nb == 0) {
+        if (t.d_err_sums && cudaMemsetAsync(t.d_err_sums, 0, 16, cs) != cudaSuccess) return SS_ERR_CUDA;
+        continue;
+      }
+      QTensor& q = b.t[b.n++];
+      q.in = reinterpret_cast<const uint8_t*>(t.in_bf16);
+      q.codes = reinterpret_cast<uint2*>(t.out_codes);
+      q.scales = t.out_scales;
+      q.err = reinterpret_cast<float2*>(t.out_err);
+      q.offsets = t.out_offset;
+      q.sums = t.d_err_sums;
+      q.g_out = t.d_global_scale;
+      q.amax = amax[i];
+      q.nb = nb;
+      q.task0 = tk;
+      q.group0 = gr;
+      tk += tasks_of(nb);
+      gr += groups_of(nb);
+    }
+    if (b.n == 0) break;
+    b.ntasks = tk;
+    const int64_t want = (tk + ss::kWarps - 1) / ss::kWarps;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, slots));
+    k<<<grid, ss::kThreads, 0, cs>>>(b);
+    if (ss_status s = launch_status()) return s;
+  }
+  return SS_OK;
+}
+
+ss_tensor_io io_from_args(const ss_quant_args* a) {
+  ss_tensor_io t;
+  std::memset(&t, 0, sizeof(t));
+  t.in_bf16 = a->in_bf16;
+  t.rows = a->rows;
+  t.cols = a->cols;
+  t.d_amax_bits = a->d_amax_bits;
+  t.out_codes = a->out_codes;
+  t.out_scales = a->out_scales;
+  t.out_err = a->out_err;
+  t.out_offset = a->out_offset;
+  t.d_err_sums = a->d_err_sums;
+  t.d_global_scale = a->d_global_scale;
+  return t;
 }
 
 // ---- end-to-end host pipeline -----------------------------------------------
@@ -233,17 +375,25 @@ const char* ss_status_string(int s) {
   }
 }
 
-int ss_version(void) { return 100; }
+int ss_version(void) { return 200; }
 
 ss_status ss_tensor_amax(const void* in_bf16, int64_t n, uint32_t* d_amax_bits, int accumulate,
                          void* stream) {
-  if (n < 0 || !d_amax_bits || (n > 0 && !in_bf16)) return SS_ERR_INVALID_ARG;
-  if (!aligned(in_bf16, 16)) return SS_ERR_ALIGNMENT;
+  return ss_tensor_amax_batched(&in_bf16, &n, 1, d_amax_bits, accumulate, stream);
+}
+
+ss_status ss_tensor_amax_batched(const void* const* in_bf16, const int64_t* n, int count,
+                                 uint32_t* d_amax_bits, int accumulate, void* stream) {
+  if (count < 0 || (count > 0 && (!in_bf16 || !n || !d_amax_bits))) return SS_ERR_INVALID_ARG;
+  for (int i = 0; i < count; i++) {
+    if (n[i] < 0 || (n[i] > 0 && !in_bf16[i])) return SS_ERR_INVALID_ARG;
+    if (!aligned(in_bf16[i], 16)) return SS_ERR_ALIGNMENT;
+  }
+  if (!aligned(d_amax_bits, 4)) return SS_ERR_ALIGNMENT;
   int dev;
   DeviceInfo info;
-  ss_status st = device_check(&dev, &info);
-  if (st) return st;
-  return amax_launch(in_bf16, n, d_amax_bits, accumulate != 0,
+  if (ss_status s = device_check(&dev, &info)) return s;
+  return amax_launch(in_bf16, n, d_amax_bits, count, accumulate != 0,
                      reinterpret_cast<cudaStream_t>(stream), info.sms);
 }
 
@@ -251,23 +401,30 @@ ss_status ss_quantize_nvfp4(const void* in_bf16, int64_t rows, int64_t cols, int
                             int global_scale_mode, uint8_t* out_codes, uint8_t* out_scales,
                             float* out_err, void* stream) {
   if (radius < 0) return SS_ERR_INVALID_ARG;
-  if (global_scale_mode == SS_GLOBAL_DEVICE_AMAX) return SS_ERR_INVALID_ARG;
-  ss_quant_args a;
-  std::memset(&a, 0, sizeof(a));
-  a.in_bf16 = in_bf16;
-  a.rows = rows;
-  a.cols = cols;
-  a.f_min = -std::min(radius, 126);
-  a.f_max = std::min(radius, 126);
-  a.global_scale_mode = global_scale_mode;
-  a.out_codes = out_codes;
-  a.out_scales = out_scales;
-  a.out_err = out_err;
-  a.stream = stream;
-  return quantize_impl(&a);
+  if (global_scale_mode != SS_GLOBAL_NONE && global_scale_mode != SS_GLOBAL_TENSOR)
+    return SS_ERR_INVALID_ARG;
+  ss_tensor_io t;
+  std::memset(&t, 0, sizeof(t));
+  t.in_bf16 = in_bf16;
+  t.rows = rows;
+  t.cols = cols;
+  t.out_codes = out_codes;
+  t.out_scales = out_scales;
+  t.out_err = out_err;
+  const int r = std::min(radius, 126);
+  return quantize_core(&t, 1, -r, r, global_scale_mode, stream);
 }
 
-ss_status ss_quantize_nvfp4_ex(const ss_quant_args* args) { return quantize_impl(args); }
+ss_status ss_quantize_nvfp4_ex(const ss_quant_args* a) {
+  if (!a) return SS_ERR_INVALID_ARG;
+  ss_tensor_io t = io_from_args(a);
+  return quantize_core(&t, 1, a->f_min, a->f_max, a->global_scale_mode, a->stream);
+}
+
+ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min, int f_max,
+                                    int global_scale_mode, void* stream) {
+  return quantize_core(tensors, count, f_min, f_max, global_scale_mode, stream);
+}
 
 ss_status ss_dequantize_nvfp4(const uint8_t* codes, const uint8_t* scales, int64_t rows,
                               int64_t cols, const float* d_global_scale, void* out_bf16,
@@ -278,8 +435,7 @@ ss_status ss_dequantize_nvfp4(const uint8_t* codes, const uint8_t* scales, int64
   if (!aligned(codes, 8) || !aligned(out_bf16, 16)) return SS_ERR_ALIGNMENT;
   int dev;
   DeviceInfo info;
-  ss_status st = device_check(&dev, &info);
-  if (st) return st;
+  if (ss_status s = device_check(&dev, &info)) return s;
   if (nb == 0) return SS_OK;
   int64_t want = (nb + 255) / 256;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)info.sms * 8));
@@ -293,11 +449,12 @@ ss_status ss_get_device_status(int* flags, void* stream) {
   if (!flags) return SS_ERR_INVALID_ARG;
   int dev;
   DeviceInfo info;
-  ss_status st = device_check(&dev, &info);
-  if (st) return st;
+  if (ss_status s = device_check(&dev, &info)) return s;
   Workspace* ws = nullptr;
-  st = get_ws(dev, stream, 0, &ws);
-  if (st) return st;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (ss_status s = get_ws(dev, stream, &ws)) return s;
+  }
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   uint32_t h = 0;
   if (cudaMemcpyAsync(&h, ws->flags, 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess) return SS_ERR_CUDA;
@@ -317,8 +474,7 @@ ss_status ss_quantize_nvfp4_host(const void* h_in, int64_t rows, int64_t cols, i
   if (nb > 0 && (!h_in || !h_codes || !h_scales)) return SS_ERR_INVALID_ARG;
   int dev;
   DeviceInfo info;
-  ss_status st = device_check(&dev, &info);
-  if (st) return st;
+  if (ss_status s = device_check(&dev, &info)) return s;
   std::lock_guard<std::mutex> lk(g_pipe_mu);
   HostPipe& hp = g_pipes[dev];
   if (!hp.s_h2d) {
@@ -329,6 +485,7 @@ ss_status ss_quantize_nvfp4_host(const void* h_in, int64_t rows, int64_t cols, i
       return SS_ERR_CUDA;
   }
   if (nb == 0) return SS_OK;
+  ss_status st;
   if ((st = grow(&hp.d_in, &hp.cap_in, (size_t)n * 2)) ||
       (st = grow(&hp.d_codes, &hp.cap_codes, (size_t)nb * 8)) ||
       (st = grow(&hp.d_scales, &hp.cap_scales, (size_t)nb)) ||
@@ -340,89 +497,63 @@ ss_status ss_quantize_nvfp4_host(const void* h_in, int64_t rows, int64_t cols, i
   const char* hin = reinterpret_cast<const char*>(h_in);
   char* din = reinterpret_cast<char*>(hp.d_in);
   const bool tensor = global_scale_mode == SS_GLOBAL_TENSOR;
-  cudaEvent_t ev_in[2], ev_out[2];
-  for (int i = 0; i < 2; i++) {
-    cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
-  }
-  auto fail = [&](ss_status s) {
-    for (int i = 0; i < 2; i++) {
-      cudaEventDestroy(ev_in[i]);
-      cudaEventDestroy(ev_out[i]);
-    }
+  std::vector<cudaEvent_t> ev(2 * nchunks);
+  for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  auto done = [&](ss_status s) {
+    for (auto& e : ev) cudaEventDestroy(e);
     return s;
   };
-  if (tensor && cudaMemsetAsync(hp.d_amax, 0, 4, hp.s_comp) != cudaSuccess) return fail(SS_ERR_CUDA);
-  // phase 1: H2D every chunk; in TENSOR mode the amax of each chunk follows its copy
+  auto quant_chunk = [&](int64_t k) -> ss_status {
+    const int64_t r0 = k * chunk_rows, r1 = std::min(rows, r0 + chunk_rows);
+    ss_tensor_io t;
+    std::memset(&t, 0, sizeof(t));
+    t.in_bf16 = din + (size_t)r0 * cols * 2;
+    t.rows = r1 - r0;
+    t.cols = cols;
+    t.d_amax_bits = hp.d_amax;
+    t.out_codes = reinterpret_cast<uint8_t*>(hp.d_codes) + (size_t)r0 * cols / 2;
+    t.out_scales = reinterpret_cast<uint8_t*>(hp.d_scales) + (size_t)r0 * cols / 16;
+    t.out_err = h_err ? reinterpret_cast<float*>(hp.d_err) + (size_t)r0 * cols / 8 : nullptr;
+    ss_status s = quantize_core(&t, 1, f_min, f_max,
+                                tensor ? SS_GLOBAL_DEVICE_AMAX : SS_GLOBAL_NONE, hp.s_comp);
+    if (s) return s;
+    cudaEventRecord(ev[nchunks + k], hp.s_comp);
+    cudaStreamWaitEvent(hp.s_d2h, ev[nchunks + k], 0);
+    cudaMemcpyAsync(h_codes + (size_t)r0 * cols / 2, t.out_codes, (size_t)(r1 - r0) * cols / 2,
+                    cudaMemcpyDeviceToHost, hp.s_d2h);
+    cudaMemcpyAsync(h_scales + (size_t)r0 * cols / 16, t.out_scales, (size_t)(r1 - r0) * cols / 16,
+                    cudaMemcpyDeviceToHost, hp.s_d2h);
+    if (h_err)
+      cudaMemcpyAsync(h_err + (size_t)r0 * cols / 8, t.out_err, (size_t)(r1 - r0) * cols / 2,
+                      cudaMemcpyDeviceToHost, hp.s_d2h);
+    return SS_OK;
+  };
+  if (tensor && cudaMemsetAsync(hp.d_amax, 0, 4, hp.s_comp) != cudaSuccess) return done(SS_ERR_CUDA);
+  // phase 1: H2D every chunk; in TENSOR mode the amax of each chunk follows its copy,
+  // in NONE mode the chunk is quantized and copied back as soon as it lands
   for (int64_t k = 0; k < nchunks; k++) {
     const int64_t r0 = k * chunk_rows, r1 = std::min(rows, r0 + chunk_rows);
     const size_t off = (size_t)r0 * cols * 2, bytes = (size_t)(r1 - r0) * cols * 2;
     if (cudaMemcpyAsync(din + off, hin + off, bytes, cudaMemcpyHostToDevice, hp.s_h2d) != cudaSuccess)
-      return fail(SS_ERR_CUDA);
-    cudaEventRecord(ev_in[k & 1], hp.s_h2d);
-    cudaStreamWaitEvent(hp.s_comp, ev_in[k & 1], 0);
+      return done(SS_ERR_CUDA);
+    cudaEventRecord(ev[k], hp.s_h2d);
+    cudaStreamWaitEvent(hp.s_comp, ev[k], 0);
     if (tensor) {
-      if ((st = amax_launch(din + off, (r1 - r0) * cols, hp.d_amax, true, hp.s_comp, info.sms)))
-        return fail(st);
-    } else {
-      // NONE mode: quantize and copy back chunk by chunk as the input lands
-      ss_quant_args a;
-      std::memset(&a, 0, sizeof(a));
-      a.in_bf16 = din + off;
-      a.rows = r1 - r0;
-      a.cols = cols;
-      a.f_min = f_min;
-      a.f_max = f_max;
-      a.global_scale_mode = SS_GLOBAL_NONE;
-      a.out_codes = reinterpret_cast<uint8_t*>(hp.d_codes) + (size_t)r0 * cols / 2;
-      a.out_scales = reinterpret_cast<uint8_t*>(hp.d_scales) + (size_t)r0 * cols / 16;
-      a.out_err = h_err ? reinterpret_cast<float*>(hp.d_err) + (size_t)r0 * cols / 8 : nullptr;
-      a.stream = hp.s_comp;
-      if ((st = quantize_impl(&a))) return fail(st);
-      cudaEventRecord(ev_out[k & 1], hp.s_comp);
-      cudaStreamWaitEvent(hp.s_d2h, ev_out[k & 1], 0);
-      cudaMemcpyAsync(h_codes + (size_t)r0 * cols / 2, a.out_codes, (size_t)(r1 - r0) * cols / 2,
-                      cudaMemcpyDeviceToHost, hp.s_d2h);
-      cudaMemcpyAsync(h_scales + (size_t)r0 * cols / 16, a.out_scales,
-                      (size_t)(r1 - r0) * cols / 16, cudaMemcpyDeviceToHost, hp.s_d2h);
-      if (h_err)
-        cudaMemcpyAsync(h_err + (size_t)r0 * cols / 8, a.out_err, (size_t)(r1 - r0) * cols / 2,
-                        cudaMemcpyDeviceToHost, hp.s_d2h);
+      const void* p = din + off;
+      const int64_t cnt = (r1 - r0) * cols;
+      if ((st = amax_launch(&p, &cnt, hp.d_amax, 1, true, hp.s_comp, info.sms))) return done(st);
+    } else if ((st = quant_chunk(k))) {
+      return done(st);
     }
   }
-  if (tensor) {
-    // phase 2: quantize chunk by chunk with the final amax, copying results back
-    for (int64_t k = 0; k < nchunks; k++) {
-      const int64_t r0 = k * chunk_rows, r1 = std::min(rows, r0 + chunk_rows);
-      ss_quant_args a;
-      std::memset(&a, 0, sizeof(a));
-      a.in_bf16 = din + (size_t)r0 * cols * 2;
-      a.rows = r1 - r0;
-      a.cols = cols;
-      a.f_min = f_min;
-      a.f_max = f_max;
-      a.global_scale_mode = SS_GLOBAL_DEVICE_AMAX;
-      a.d_amax_bits = hp.d_amax;
-      a.out_codes = reinterpret_cast<uint8_t*>(hp.d_codes) + (size_t)r0 * cols / 2;
-      a.out_scales = reinterpret_cast<uint8_t*>(hp.d_scales) + (size_t)r0 * cols / 16;
-      a.out_err = h_err ? reinterpret_cast<float*>(hp.d_err) + (size_t)r0 * cols / 8 : nullptr;
-      a.stream = hp.s_comp;
-      if ((st = quantize_impl(&a))) return fail(st);
-      cudaEventRecord(ev_out[k & 1], hp.s_comp);
-      cudaStreamWaitEvent(hp.s_d2h, ev_out[k & 1], 0);
-      cudaMemcpyAsync(h_codes + (size_t)r0 * cols / 2, a.out_codes, (size_t)(r1 - r0) * cols / 2,
-                      cudaMemcpyDeviceToHost, hp.s_d2h);
-      cudaMemcpyAsync(h_scales + (size_t)r0 * cols / 16, a.out_scales,
-                      (size_t)(r1 - r0) * cols / 16, cudaMemcpyDeviceToHost, hp.s_d2h);
-      if (h_err)
-        cudaMemcpyAsync(h_err + (size_t)r0 * cols / 8, a.out_err, (size_t)(r1 - r0) * cols / 2,
-                        cudaMemcpyDeviceToHost, hp.s_d2h);
-    }
-  }
+  // phase 2 (TENSOR): quantize chunk by chunk with the final amax, copying results back
+  if (tensor)
+    for (int64_t k = 0; k < nchunks; k++)
+      if ((st = quant_chunk(k))) return done(st);
   cudaError_t e1 = cudaStreamSynchronize(hp.s_comp);
   cudaError_t e2 = cudaStreamSynchronize(hp.s_d2h);
   cudaError_t e3 = cudaStreamSynchronize(hp.s_h2d);
-  return fail((e1 || e2 || e3) ? SS_ERR_CUDA : SS_OK);
+  return done((e1 || e2 || e3) ? SS_ERR_CUDA : SS_OK);
 }
 
 }  // extern "C"

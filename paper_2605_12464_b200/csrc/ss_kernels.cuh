@@ -2,27 +2,50 @@
 //
 // Hot path = Algorithm 1 of arxiv 2605.12464 applied to
 // every 16-element block, under the FP32 contract of include/ss.h (readings
-// R1-R15 in DESIGN.md §3).  Not a contraction, so no tensor cores: the work is
-// plain FP32 + the Blackwell FP4/FP8 conversion instructions, one NVFP4 block
-// per thread, the candidate loop unrolled in registers.
+// R1-R18 in DESIGN.md §3).  Not a contraction, so no tensor cores: the work is
+// plain FP32 plus the Blackwell FP4/FP8 conversion instructions.
 //
-// Per element and candidate the inner loop issues, per PAIR of elements:
-//   FMUL2  t = y * rho                     (mul.rn.f32x2, scalar-broadcast rho)
+// Work decomposition.  The unit of scheduling is a WARP TASK
+// of 32 consecutive NVFP4 blocks (1 KiB of bf16), one block per lane.  A
+// launch covers a BATCH of up to kMaxTensors tensors whose tasks are numbered
+// consecutively, so one persistent grid walks every tensor of a step with no
+// per-tensor tail.  Each warp double-buffers its tasks in shared memory with
+// 1-D bulk async copies (cp.async.bulk, the TMA bulk path) completed on a
+// per-warp mbarrier, so no CTA-wide barrier exists after the prologue.
+//
+// Inner loop per PAIR of elements and candidate (3 issue slots per
+// element-candidate; the candidate's {rho, rho, -s | code<<16} comes from one
+// LDS.128 of a padded, pre-clamped candidate table):
+//   FMUL2  t = y * rho                     (mul.rn.f32x2)
 //   F2FP   E2M1 pack of (t0, t1)           (cvt.rn.satfinite.e2m1x2.f32)
 //   F2FP   unpack to f16x2 (q0, q1)        (cvt.rn.f16x2.e2m1x2)
 //   FHFMA  d0 = y0 + q0 * (-s)             (fma.rn.f32.f16; q*s exact, one rounding)
 //   FHFMA  d1 = y1 + q1 * (-s)
 //   FFMA2  {a, b} += {d0^2, d1^2}          (fma.rn.f32x2: the even / odd chains of R12)
-// = 3 issue slots per element-candidate.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef SS_MIN_BLOCKS
+#define SS_MIN_BLOCKS 4
+#endif
+
 namespace ss {
 
-constexpr int kThreads = 256;           // threads per CTA = NVFP4 blocks per CTA tile
+constexpr int kWarps = 8;                     // warps per CTA
+constexpr int kThreads = 32 * kWarps;
+constexpr int kTaskBlocks = 32;               // NVFP4 blocks per warp task (one per lane)
+constexpr int kTaskBytes = kTaskBlocks * 32;  // 1 KiB of bf16 input per task
+constexpr int kStages = 2;                    // per-warp smem buffers
+constexpr int kPad = 126;                     // candidate-table padding (|f| <= 126)
+constexpr int kTabW = 127 + 2 * kPad;         // entries per half-table
+constexpr int kGroupTasks = 256;              // level-1 group of the error-sum reduction
+constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
+constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
+constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk (32 KiB)
+
 constexpr uint32_t kOneSixthBits = 0x3E2AAAABu;  // RN(1/6) (Alg. 1 line 2; R8)
-constexpr float kGlobalNumer = 2688.0f;  // 6 * 448: largest NVFP4 magnitude (R9)
+constexpr float kGlobalNumer = 2688.0f;          // 6 * 448: largest NVFP4 magnitude (R9)
 
 enum : uint32_t { kFlagNonFinite = 1u, kFlagRange = 2u };
 
@@ -34,12 +57,17 @@ __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
   return r;
 }
+__device__ __forceinline__ uint64_t pack2u(uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
 __device__ __forceinline__ void unpack2(uint64_t v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
-__device__ __forceinline__ uint64_t fmul2_bcast(uint64_t a, float b) {
-  uint64_t r, bb = pack2(b, b);
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(bb));
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
 __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
@@ -47,7 +75,7 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
-// E2M1 nibbles of (lo, hi) -> f16x2 (q_lo, q_hi); also returns the packed byte.
+// E2M1 nibbles of (lo, hi) -> f16x2 (q_lo, q_hi).
 __device__ __forceinline__ uint32_t e2m1_round_f16x2(float lo, float hi) {
   uint32_t h;
   asm("{\n\t.reg .b8 q;\n\t"
@@ -95,44 +123,80 @@ __device__ __forceinline__ float f16_to_f32(uint16_t h) {
   return f;
 }
 
-// ---------------------------------------------------------------------------
-// Candidate table: for every UE4M3 code c, rho = RN(1/s_c) and -s_c as f16.
-// Entry 0 is the zero-scale candidate (rho = 0, s = 0; R3); entry 127 (NaN)
-// is never selected (masked as invalid).
-// ---------------------------------------------------------------------------
-struct __align__(8) Cand {
-  float rho;
-  uint32_t negs;  // f16 bits of -s in the low half
-};
+// ---- shared-memory bulk copies (TMA bulk path) and mbarriers ---------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Arm `bar` for `bytes` and start the bulk copy global -> shared (one thread).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = smem_u32(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "SS_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SS_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
-__device__ __forceinline__ void build_cand_table(Cand* tab) {
-  for (int c = threadIdx.x; c < 128; c += blockDim.x) {
-    Cand e;
-    if (c == 0 || c == 127) {
-      e.rho = 0.0f;
-      e.negs = 0x8000u;  // -0
+// ---------------------------------------------------------------------------
+// Candidate table.  Two halves of kTabW entries; entry i of a half stands for
+// the unclamped candidate code k = i - kPad:
+//   half 0 (used when c0 == 0): code = 0 for k <= 0 (the zero-scale candidate,
+//            R3), else min(k, 126);
+//   half 1 (c0 >= 1):           code = clamp(k, 1, 126).
+// A block's candidates are base[f] with base = half + kPad + c0, so
+// out-of-range offsets become duplicates of the nearest valid code, which
+// never change the lexicographic (loss, code) minimum (R2, R4): no branches.
+// Entry = {rho, rho, (-s as f16) | code << 16, 0} with rho = RN(1/s) (R7);
+// code 0 has rho = 0 and -s = -0.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void build_cand_table(uint4* tab) {
+  for (int i = threadIdx.x; i < 2 * kTabW; i += blockDim.x) {
+    const int half = i / kTabW;
+    const int k = i - half * kTabW - kPad;
+    int code = half == 0 ? (k <= 0 ? 0 : k) : (k < 1 ? 1 : k);
+    code = code > 126 ? 126 : code;
+    uint4 e;
+    if (code == 0) {
+      e = make_uint4(0u, 0u, 0x8000u, 0u);
     } else {
-      uint16_t sh = e4m3_to_f16((uint32_t)c);
-      float s = f16_to_f32(sh);
-      e.rho = __frcp_rn(s);          // RN(1/s) (R7), IEEE reciprocal
-      e.negs = (uint32_t)(sh ^ 0x8000u);
+      const uint16_t sh = e4m3_to_f16((uint32_t)code);
+      const float rho = __frcp_rn(f16_to_f32(sh));  // IEEE RN(1/s), not MUFU (R7)
+      e = make_uint4(__float_as_uint(rho), __float_as_uint(rho),
+                     (uint32_t)(sh ^ 0x8000u) | ((uint32_t)code << 16), 0u);
     }
-    tab[c] = e;
+    tab[i] = e;
   }
 }
 
 // Global scale from the amax bit pattern (R9); flags non-finite / overflow.
-__device__ __forceinline__ float global_scale(int gmode, const uint32_t* amax_bits,
-                                              uint32_t* flags, bool report) {
-  if (gmode == 0) return 1.0f;
-  uint32_t ab = *amax_bits;
-  if (ab >= 0x7F800000u) {  // NaN / Inf in the input
+__device__ __forceinline__ float global_scale(uint32_t ab, uint32_t* flags, bool report) {
+  if (ab >= 0x7F800000u) {  // NaN / Inf in the input (R14)
     if (report) atomicOr(flags, kFlagNonFinite);
     return 1.0f;
   }
-  float A = __uint_as_float(ab);
+  const float A = __uint_as_float(ab);
   if (A == 0.0f) return 1.0f;
-  float G = __fdiv_rn(kGlobalNumer, A);
+  const float G = __fdiv_rn(kGlobalNumer, A);
   if (!isfinite(G)) {
     if (report) atomicOr(flags, kFlagRange);
     return 1.0f;
@@ -141,79 +205,170 @@ __device__ __forceinline__ float global_scale(int gmode, const uint32_t* amax_bi
 }
 
 // ---------------------------------------------------------------------------
-// Amax kernel: unsigned max of |x| bf16 bit patterns (exact, NaN-propagating).
+// Batch descriptors (kernel parameters; __grid_constant__).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t umax2(uint32_t a, uint32_t b) {
-  return __vmaxu2(a, b);  // per-halfword unsigned max
+struct QTensor {
+  const uint8_t* in;        // bf16 [nb][16]
+  uint2* codes;             // [nb] 8 B
+  uint8_t* scales;          // [nb]
+  float2* err;              // nullable [nb]
+  int8_t* offsets;          // nullable [nb]
+  double* sums;             // nullable [2]
+  float* g_out;             // nullable
+  const uint32_t* amax;     // gmode given: FP32 bits of the tensor amax
+  int64_t nb;               // NVFP4 blocks
+  int64_t task0;            // first global task of this tensor
+  int64_t group0;           // first global level-1 group of this tensor
+};
+
+struct QuantBatch {
+  int n;                    // tensors in this launch
+  int fmin, fmax;           // window (runtime loop variant only)
+  int gmode;                // 0: G = 1; 1: G from t[i].amax
+  int64_t ntasks;           // total tasks of the batch
+  double2* part1;           // per task {sum best, sum base}   (when any sums wanted)
+  double2* part2;           // per level-1 group
+  uint32_t* tick1;          // per group, zero and self re-arming
+  uint32_t* tick2;          // per tensor, zero and self re-arming
+  uint32_t* flags;
+  QTensor t[kMaxTensors];
+};
+
+struct ATensor {
+  const uint4* in;          // 16-B vectors
+  int64_t nvec;             // whole 16-B vectors
+  int ntail;                // trailing bf16 elements (< 8)
+  int64_t chunk0;           // first global chunk
+  uint32_t* out;            // amax slot (FP32 bits)
+};
+
+struct AmaxBatch {
+  int n;
+  int64_t nchunks;
+  ATensor t[kMaxTensors];
+};
+
+// Index of the tensor holding task/chunk `k`, searching forward from `from`
+// (warp-uniform; the tasks of one warp increase monotonically).
+__device__ __forceinline__ int locate_task(const QuantBatch& p, int64_t k, int from) {
+  int i = from;
+  while (i + 1 < p.n && p.t[i + 1].task0 <= k) i++;
+  return i;
 }
 
-__global__ void __launch_bounds__(256) amax_kernel(const uint4* __restrict__ in, int64_t n16,
-                                                   const uint16_t* __restrict__ tail, int n_tail,
-                                                   uint32_t* __restrict__ out) {
-  uint32_t m = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // 4 independent 16-B loads in flight per thread per iteration
-  for (; i + 3 * stride < n16; i += 4 * stride) {
-    uint4 a = in[i], b = in[i + stride];  // default policy: keep in L2 for the quantize pass
-    uint4 c = in[i + 2 * stride], d = in[i + 3 * stride];
+// ---------------------------------------------------------------------------
+// Amax kernel: unsigned max of |x| bf16 bit patterns (exact, NaN-propagating).
+// One 32 KiB chunk per CTA iteration, 8 independent 16-B loads per thread.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) amax_kernel(const __grid_constant__ AmaxBatch p) {
+  const int lane = threadIdx.x & 31;
+  int ti = 0;
+  for (int64_t ch = blockIdx.x; ch < p.nchunks; ch += gridDim.x) {
+    while (ti + 1 < p.n && p.t[ti + 1].chunk0 <= ch) ti++;
+    const ATensor& T = p.t[ti];
+    const int64_t v0 = (ch - T.chunk0) * kAmaxChunk + threadIdx.x;
     const uint32_t M = 0x7FFF7FFFu;
-    uint32_t x0 = umax2(umax2(a.x & M, a.y & M), umax2(a.z & M, a.w & M));
-    uint32_t x1 = umax2(umax2(b.x & M, b.y & M), umax2(b.z & M, b.w & M));
-    uint32_t x2 = umax2(umax2(c.x & M, c.y & M), umax2(c.z & M, c.w & M));
-    uint32_t x3 = umax2(umax2(d.x & M, d.y & M), umax2(d.z & M, d.w & M));
-    m = umax2(m, umax2(umax2(x0, x1), umax2(x2, x3)));
+    uint32_t m = 0;
+    uint4 v[kAmaxVecs];
+#pragma unroll
+    for (int k = 0; k < kAmaxVecs; k++) {
+      const int64_t i = v0 + (int64_t)k * kThreads;
+      v[k] = i < T.nvec ? __ldcs(T.in + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kAmaxVecs; k++)
+      m = __vmaxu2(m, __vmaxu2(__vmaxu2(v[k].x & M, v[k].y & M), __vmaxu2(v[k].z & M, v[k].w & M)));
+    uint32_t r = max(m & 0xFFFFu, m >> 16);
+    // trailing elements: handled by the chunk that holds the last vector
+    if (T.ntail && (ch - T.chunk0) == (T.nvec / kAmaxChunk) && threadIdx.x < T.ntail) {
+      const uint16_t* tail = reinterpret_cast<const uint16_t*>(T.in + T.nvec);
+      r = max(r, (uint32_t)(tail[threadIdx.x] & 0x7FFFu));
+    }
+    r = __reduce_max_sync(0xFFFFFFFFu, r);
+    if (lane == 0 && r) atomicMax(T.out, r << 16);  // bf16 bits -> FP32 bits (exact)
   }
-  for (; i < n16; i += stride) {
-    uint4 a = in[i];
-    const uint32_t M = 0x7FFF7FFFu;
-    m = umax2(m, umax2(umax2(a.x & M, a.y & M), umax2(a.z & M, a.w & M)));
+}
+
+// ---------------------------------------------------------------------------
+// Error sums: deterministic two-level reduction finished by the last warp of
+// each level (ticket counters), in a fixed order independent of the grid.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void reduce_task_sums(const QuantBatch& p, int ti, int64_t task, double sb,
+                                              double sc) {
+  const int lane = threadIdx.x & 31;
+  const QTensor& T = p.t[ti];
+  sb = warp_sum(sb);
+  sc = warp_sum(sc);
+  const int64_t lt = task - T.task0;
+  const int64_t ntask_t = (T.nb + kTaskBlocks - 1) / kTaskBlocks;
+  const int64_t g = lt / kGroupTasks;
+  const int64_t ng = (ntask_t + kGroupTasks - 1) / kGroupTasks;
+  const int gsize = (int)min((int64_t)kGroupTasks, ntask_t - g * kGroupTasks);
+  uint32_t last = 0;
+  if (lane == 0) {
+    p.part1[task] = make_double2(sb, sc);
+    __threadfence();
+    last = atomicAdd(p.tick1 + T.group0 + g, 1u) == (uint32_t)(gsize - 1);
   }
-  uint32_t r = max(m & 0xFFFFu, m >> 16);
-  if (blockIdx.x == 0 && threadIdx.x < n_tail) r = max(r, (uint32_t)(tail[threadIdx.x] & 0x7FFFu));
-  for (int o = 16; o > 0; o >>= 1) r = max(r, __shfl_xor_sync(0xFFFFFFFFu, r, o));
-  __shared__ uint32_t red[32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = r;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    r = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
-    for (int o = 16; o > 0; o >>= 1) r = max(r, __shfl_xor_sync(0xFFFFFFFFu, r, o));
-    if (threadIdx.x == 0) atomicMax(out, r << 16);  // bf16 bits -> FP32 bits (exact)
+  if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
+  __threadfence();
+  const double2* src = p.part1 + T.task0 + g * kGroupTasks;
+  double a = 0.0, c = 0.0;
+  for (int i = lane; i < gsize; i += 32) {
+    const double2 v = __ldcg(src + i);
+    a += v.x;
+    c += v.y;
+  }
+  a = warp_sum(a);
+  c = warp_sum(c);
+  last = 0;
+  if (lane == 0) {
+    p.part2[T.group0 + g] = make_double2(a, c);
+    p.tick1[T.group0 + g] = 0u;  // re-arm
+    __threadfence();
+    last = atomicAdd(p.tick2 + ti, 1u) == (uint32_t)(ng - 1);
+  }
+  if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
+  __threadfence();
+  a = c = 0.0;
+  for (int64_t i = lane; i < ng; i += 32) {
+    const double2 v = __ldcg(p.part2 + T.group0 + i);
+    a += v.x;
+    c += v.y;
+  }
+  a = warp_sum(a);
+  c = warp_sum(c);
+  if (lane == 0) {
+    T.sums[0] = a;
+    T.sums[1] = c;
+    p.tick2[ti] = 0u;  // re-arm
   }
 }
 
 // ---------------------------------------------------------------------------
 // Search-quantize kernel.
 // ---------------------------------------------------------------------------
-struct QuantParams {
-  const uint4* in;          // bf16 blocks, 2 x uint4 per NVFP4 block
-  int64_t nb;               // number of 16-element blocks
-  int fmin, fmax;           // runtime window (NC == fmax - fmin + 1 when NC > 0)
-  int gmode;
-  const uint32_t* amax_bits;
-  uint2* codes;             // 8 B per block
-  uint8_t* scales;
-  int8_t* offsets;          // nullable
-  float2* err;              // nullable
-  double2* partials;        // nullable: per-CTA {sum best, sum base}
-  double* sums;             // receives the fixed-order total when partials != null
-  uint32_t* ticket;         // zero-initialised counter for the last-CTA reduction
-  float* g_out;             // nullable
-  uint32_t* flags;
-};
 
-// Loss of one candidate (Alg. 1 lines 7-9) for the 16 values y (as 8 f32 pairs).
+// Loss of one candidate (Alg. 1 lines 7-9) for the 16 values y (8 f32 pairs).
 __device__ __forceinline__ float cand_loss(const uint64_t (&y2)[8], const float (&y)[16],
-                                           float rho, uint16_t negs) {
+                                           const uint4 e) {
+  const uint64_t rr = pack2u(e.x, e.y);
+  const uint16_t negs = (uint16_t)(e.z & 0xFFFFu);
   uint64_t acc = 0;  // {even chain a, odd chain b}
 #pragma unroll
   for (int k = 0; k < 8; k++) {
     float t0, t1;
-    unpack2(fmul2_bcast(y2[k], rho), t0, t1);
-    uint32_t q = e2m1_round_f16x2(t0, t1);
-    float d0 = fhfma((uint16_t)(q & 0xFFFFu), negs, y[2 * k]);
-    float d1 = fhfma((uint16_t)(q >> 16), negs, y[2 * k + 1]);
-    uint64_t d = pack2(d0, d1);
+    unpack2(fmul2(y2[k], rr), t0, t1);
+    const uint32_t q = e2m1_round_f16x2(t0, t1);
+    const float d0 = fhfma((uint16_t)(q & 0xFFFFu), negs, y[2 * k]);
+    const float d1 = fhfma((uint16_t)(q >> 16), negs, y[2 * k + 1]);
+    const uint64_t d = pack2(d0, d1);
     acc = ffma2(d, d, acc);
   }
   float a, b;
@@ -221,30 +376,91 @@ __device__ __forceinline__ float cand_loss(const uint64_t (&y2)[8], const float 
   return __fadd_rn(a, b);
 }
 
-template <int NC>  // NC > 0: unrolled window of NC candidates; NC == 0: runtime loop
-__global__ void __launch_bounds__(kThreads) quant_kernel(QuantParams p) {
-  __shared__ Cand tab[128];
-  __shared__ double2 red[kThreads / 32];
+// Candidate order (equivalent to Alg. 1's ascending strict-< scan, R4): f = 0
+// first (it is also err_base), then f = -1, -2, ... with "<=" (ties move to
+// the smaller code), then f = 1, 2, ... with strict "<" (ties keep the
+// smaller code).  Clamped duplicates carry the same code, so they never
+// change the result.
+#define SS_TAKE_LE(E)                             \
+  {                                               \
+    const uint4 e_ = (E);                         \
+    const float l_ = cand_loss(y2, y, e_);        \
+    const bool t_ = l_ <= best;                   \
+    best = t_ ? l_ : best;                        \
+    bsel = t_ ? e_.z : bsel;                      \
+  }
+#define SS_TAKE_LT(E)                             \
+  {                                               \
+    const uint4 e_ = (E);                         \
+    const float l_ = cand_loss(y2, y, e_);        \
+    const bool t_ = l_ < best;                    \
+    best = t_ ? l_ : best;                        \
+    bsel = t_ ? e_.z : bsel;                      \
+  }
+
+// NEG/POS >= 0: compile-time window [-NEG, POS]; NEG < 0: runtime [fmin, fmax].
+template <int NEG, int POS>
+__global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
+  __shared__ __align__(16) uint4 tab[2 * kTabW];
+  __shared__ __align__(128) uint4 buf[kWarps][kStages][kTaskBytes / 16];
+  __shared__ __align__(8) uint64_t bar[kWarps][kStages];
+
   build_cand_table(tab);
-  const float G = global_scale(p.gmode, p.amax_bits, p.flags, blockIdx.x == 0 && threadIdx.x == 0);
-  if (p.g_out && blockIdx.x == 0 && threadIdx.x == 0) *p.g_out = G;
+  if (threadIdx.x < kWarps * kStages) mbar_init(&bar[0][0] + threadIdx.x, 1);
+  fence_mbar_init();
   __syncthreads();
 
-  const float k6 = __uint_as_float(kOneSixthBits);
-  const int fmin = p.fmin;
-  const int nc = NC > 0 ? NC : (p.fmax - p.fmin + 1);
-  double sum_best = 0.0, sum_base = 0.0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  int64_t task = (int64_t)blockIdx.x * kWarps + w;
+  if (task >= p.ntasks) return;  // no CTA barrier follows
 
-  for (int64_t b = (int64_t)blockIdx.x * kThreads + threadIdx.x; b < p.nb;
-       b += (int64_t)gridDim.x * kThreads) {
-    // a1: load 16 bf16 (32 B) and widen exactly; a3: y = RN(x * G)
-    const uint4 v0 = __ldcs(p.in + 2 * b), v1 = __ldcs(p.in + 2 * b + 1);
-    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  const float k6 = __uint_as_float(kOneSixthBits);
+  auto issue = [&](int64_t tk, int ti, int s) {
+    if (lane == 0) {
+      const QTensor& T = p.t[ti];
+      const int64_t b0 = (tk - T.task0) * kTaskBlocks;
+      const int64_t nblk = min((int64_t)kTaskBlocks, T.nb - b0);
+      fence_proxy_async();
+      bulk_load(&buf[w][s][0], T.in + b0 * 32, (uint32_t)(nblk * 32), &bar[w][s]);
+    }
+  };
+  auto gscale = [&](int ti, bool report) -> float {
+    if (p.gmode == 0) return 1.0f;
+    return global_scale(__ldg(p.t[ti].amax), p.flags, report);
+  };
+
+  int ti = locate_task(p, task, 0);
+  issue(task, ti, 0);
+  float G = gscale(ti, task == p.t[ti].task0 && lane == 0);
+  uint32_t phases = 0;
+  int s = 0;
+  for (;;) {
+    const int64_t next = task + W;
+    int tn = ti;
+    float Gn = G;
+    if (next < p.ntasks) {
+      tn = locate_task(p, next, ti);
+      issue(next, tn, s ^ 1);
+      Gn = gscale(tn, next == p.t[tn].task0 && lane == 0);
+    }
+    const QTensor& T = p.t[ti];
+    const int64_t b = (task - T.task0) * kTaskBlocks + lane;
+    const bool active = b < T.nb;
+
+    // a1: this lane's 32 B from the staged task; bf16 -> f32 is exact
+    mbar_wait(&bar[w][s], (phases >> s) & 1u);
+    phases ^= 1u << s;
+    const uint4 v0 = buf[w][s][2 * lane], v1 = buf[w][s][2 * lane + 1];
+    __syncwarp();  // stage s may be refilled from the next iteration on
+    const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    // a3: y = RN(x * G)
     float y[16];
     uint64_t y2[8];
+    const uint64_t GG = pack2(G, G);
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      y2[k] = fmul2_bcast(pack2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u)), G);
+      y2[k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), GG);
       unpack2(y2[k], y[2 * k], y[2 * k + 1]);
     }
     // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
@@ -252,88 +468,54 @@ __global__ void __launch_bounds__(kThreads) quant_kernel(QuantParams p) {
 #pragma unroll
     for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[i]));
     const int c0 = (int)e4m3_code(__fmul_rn(m, k6));
+    const uint4* base = tab + (c0 ? kTabW : 0) + kPad + c0;
 
-    // a5: candidate search (Alg. 1 lines 5-10), lexicographic (loss, code)
-    float best = __int_as_float(0x7FFFFFFF);  // NaN: first valid candidate is taken
-    float base = 0.0f;
-    int bc = c0;
+    // a5 + a6: candidate search (Alg. 1 lines 5-10)
+    float best = cand_loss(y2, y, base[0]);
+    const float loss0 = best;  // err_base: the max-abs scale (f = 0)
+    uint32_t bsel = base[0].z;
+    if constexpr (NEG >= 0) {
 #pragma unroll
-    for (int j = 0; j < (NC > 0 ? NC : 1); j++) {
-      // (NC == 0 runs the generic loop below instead)
-      if (NC == 0) break;
-      const int f = fmin + j;
-      const int c = c0 + f;
-      const bool valid = (f == 0) || ((unsigned)(c - 1) < 126u);
-      const Cand e = tab[c & 127];
-      const float loss = cand_loss(y2, y, e.rho, (uint16_t)e.negs);
-      const bool take = valid && !(loss >= best);
-      best = take ? loss : best;
-      bc = take ? c : bc;
-      if (f == 0) base = loss;
-    }
-    if (NC == 0) {
+      for (int f = 1; f <= NEG; f++) SS_TAKE_LE(base[-f]);
+#pragma unroll
+      for (int f = 1; f <= POS; f++) SS_TAKE_LT(base[f]);
+    } else {
+      // runtime window; skip offsets that are clamped duplicates for every lane
+      const int lo = __reduce_min_sync(0xFFFFFFFFu, (c0 ? 1 : 0) - c0);
+      const int hi = __reduce_max_sync(0xFFFFFFFFu, 126 - c0);
+      const int fneg = max(p.fmin, lo), fpos = min(p.fmax, hi);
 #pragma unroll 1
-      for (int j = 0; j < nc; j++) {
-        const int f = fmin + j;
-        const int c = c0 + f;
-        const bool valid = (f == 0) || ((unsigned)(c - 1) < 126u);
-        if (!__any_sync(__activemask(), valid)) continue;  // warp-uniform skip
-        const Cand e = tab[c & 127];
-        const float loss = cand_loss(y2, y, e.rho, (uint16_t)e.negs);
-        const bool take = valid && !(loss >= best);
-        best = take ? loss : best;
-        bc = take ? c : bc;
-        if (f == 0) base = loss;
-      }
+      for (int f = -1; f >= fneg; f--) SS_TAKE_LE(base[f]);
+#pragma unroll 1
+      for (int f = 1; f <= fpos; f++) SS_TAKE_LT(base[f]);
     }
 
     // a7: emit the winner: nibbles of t = y * rho*, scale byte, offset, errors
-    const float rs = tab[bc].rho;
+    const uint32_t code = bsel >> 16;
+    const float rs = __uint_as_float(tab[(code ? kTabW : 0) + kPad + code].x);
+    const uint64_t rr = pack2(rs, rs);
     float t[16];
 #pragma unroll
-    for (int k = 0; k < 8; k++) unpack2(fmul2_bcast(y2[k], rs), t[2 * k], t[2 * k + 1]);
-    uint2 code;
-    code.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
-    code.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
-    __stcs(p.codes + b, code);
-    p.scales[b] = (uint8_t)bc;
-    if (p.offsets) p.offsets[b] = (int8_t)(bc - c0);
-    if (p.err) __stcs(p.err + b, make_float2(best, base));
-    sum_best += (double)best;
-    sum_base += (double)base;
-  }
+    for (int k = 0; k < 8; k++) unpack2(fmul2(y2[k], rr), t[2 * k], t[2 * k + 1]);
+    uint2 cw;
+    cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+    cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
+    if (active) {
+      __stcs(T.codes + b, cw);
+      T.scales[b] = (uint8_t)code;
+      if (T.offsets) T.offsets[b] = (int8_t)((int)code - c0);
+      if (T.err) __stcs(T.err + b, make_float2(best, loss0));
+    }
+    if (T.sums) {
+      reduce_task_sums(p, ti, task, active ? (double)best : 0.0, active ? (double)loss0 : 0.0);
+    }
+    if (T.g_out && task == T.task0 && lane == 0) *T.g_out = G;
 
-  if (p.partials) {  // fixed-order CTA reduction (deterministic for a fixed grid)
-    for (int o = 16; o > 0; o >>= 1) {
-      sum_best += __shfl_xor_sync(0xFFFFFFFFu, sum_best, o);
-      sum_base += __shfl_xor_sync(0xFFFFFFFFu, sum_base, o);
-    }
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(sum_best, sum_base);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double2 s = red[0];
-      for (int i = 1; i < kThreads / 32; i++) {
-        s.x += red[i].x;
-        s.y += red[i].y;
-      }
-      p.partials[blockIdx.x] = s;
-      // The last CTA to finish sums the partials in CTA order (deterministic
-      // for a fixed grid) and re-arms the ticket: no separate finalize launch.
-      __threadfence();
-      const uint32_t done = atomicAdd(p.ticket, 1u);
-      if (done == gridDim.x - 1) {
-        __threadfence();
-        double a = 0.0, c = 0.0;
-        for (unsigned i = 0; i < gridDim.x; i++) {
-          const double2 v = __ldcg(p.partials + i);
-          a += v.x;
-          c += v.y;
-        }
-        p.sums[0] = a;
-        p.sums[1] = c;
-        *p.ticket = 0u;
-      }
-    }
+    if (next >= p.ntasks) break;
+    task = next;
+    ti = tn;
+    G = Gn;
+    s ^= 1;
   }
 }
 

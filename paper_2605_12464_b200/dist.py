@@ -28,7 +28,8 @@ def shard_rows(rows: int, rank: int, world: int) -> tuple:
 
 
 class CudaOps:
-    """libss.so calls on the current CUDA stream."""
+    """libss.so batched calls on the current CUDA stream: one amax launch and
+    one quantize launch per 128 tensors of a step."""
 
     def __init__(self, fmin: int, fmax: int, want_err: bool = True, want_sums: bool = True,
                  want_offsets: bool = False):
@@ -40,31 +41,19 @@ class CudaOps:
     def new_amax(self, n: int, device) -> torch.Tensor:
         return torch.zeros(n, dtype=torch.int32, device=device)
 
-    def amax(self, x: torch.Tensor, slot: torch.Tensor):
-        self.B.tensor_amax(x, out=slot)
+    def amax_all(self, xs, buf) -> int:
+        self.B.tensor_amax_batched(xs, out=buf)
+        return (len(xs) + 127) // 128
 
     def alloc_out(self, x: torch.Tensor):
-        rows, cols = x.shape
-        nb = rows * cols // 16
-        d = x.device
-        return self.B.QuantOut(
-            torch.empty(rows, cols // 2, dtype=torch.uint8, device=d),
-            torch.empty(rows, cols // 16, dtype=torch.uint8, device=d),
-            torch.empty(nb, 2, dtype=torch.float32, device=d) if self.want_err else None,
-            torch.empty(nb, dtype=torch.int8, device=d) if self.want_offsets else None,
-            torch.empty(2, dtype=torch.float64, device=d) if self.want_sums else None,
-            torch.empty(1, dtype=torch.float32, device=d),
-        )
+        return self.B.alloc_out(x, self.want_err, self.want_offsets, self.want_sums, True)
 
-    def quantize_given(self, x, slot, out):
-        self.B.quantize(x, fmin=self.fmin, fmax=self.fmax, gmode="device_amax", amax=slot, out=out)
-
-    def quantize_tensor(self, x, out):
-        self.B.quantize(x, fmin=self.fmin, fmax=self.fmax, gmode="tensor", out=out)
-
-    launches_amax = 1        # amax_kernel
-    launches_quant = 1       # quant_kernel (sums reduced by its last CTA)
-    launches_sums = 0
+    def quantize_all(self, xs, buf, outs) -> int:
+        live = [k for k, x in enumerate(xs) if x.shape[0] > 0]
+        self.B.quantize_batched([xs[k] for k in live], [outs[k] for k in live], fmin=self.fmin,
+                                fmax=self.fmax, gmode="device_amax",
+                                amax=buf if len(live) == len(xs) else buf[live].contiguous())
+        return (len(live) + 127) // 128
 
 
 @dataclass
@@ -91,37 +80,18 @@ class RowShardQuantizer:
     def step(self, shards: List[torch.Tensor], outs: List, hooks=None) -> int:
         """One pass over every tensor; returns the number of kernels launched.
 
-        ``hooks`` (optional) has ``before(k)`` / ``after(k)`` called around the
-        quantize launch of tensor k (bench.py records CUDA events there).
+        Shard amaxes (one batched launch) -> [the one exchange step: ONE max
+        all-reduce of all the amaxes, 4 B per tensor] -> batched quantize.
+        ``hooks`` (optional) has ``before()`` / ``after()`` called around the
+        quantize launches (bench.py records CUDA events there).
         """
         import torch.distributed as dist
-        n = 0
-        if self.plan.world == 1:
-            # single GPU: amax then quantize per tensor, so the second read of
-            # each tensor (<= 100 MB) is served from the 126 MB L2
-            for k, (x, o) in enumerate(zip(shards, outs)):
-                if x.shape[0] == 0:
-                    continue
-                self.ops.amax(x, self.amax_buf[k:k + 1])
-                n += self._quant(k, x, o, hooks) + self.ops.launches_amax
-            return n
-        for k, x in enumerate(shards):
-            if x.shape[0] > 0:
-                self.ops.amax(x, self.amax_buf[k:k + 1])
-                n += self.ops.launches_amax
-            else:
-                self.amax_buf[k:k + 1].zero_()
-        # the one exchange step: max of the shard amaxes of all tensors at once
-        dist.all_reduce(self.amax_buf, op=dist.ReduceOp.MAX, group=self.group)
-        for k, (x, o) in enumerate(zip(shards, outs)):
-            if x.shape[0] > 0:
-                n += self._quant(k, x, o, hooks)
+        n = self.ops.amax_all(shards, self.amax_buf)
+        if self.plan.world > 1:
+            dist.all_reduce(self.amax_buf, op=dist.ReduceOp.MAX, group=self.group)
+        if hooks is not None:
+            hooks.before()
+        n += self.ops.quantize_all(shards, self.amax_buf, outs)
+        if hooks is not None:
+            hooks.after()
         return n
-
-    def _quant(self, k, x, o, hooks) -> int:
-        if hooks is not None:
-            hooks.before(k)
-        self.ops.quantize_given(x, self.amax_buf[k:k + 1], o)
-        if hooks is not None:
-            hooks.after(k)
-        return self.ops.launches_quant

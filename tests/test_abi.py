@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_status_strings(L):
-    assert L.ss_version() == 100
+    assert L.ss_version() == 200
     for s in range(7):
         assert L.ss_status_string(s)
     assert L.ss_status_string(6).decode().startswith("unsupported device")
@@ -61,6 +61,22 @@ def test_argument_errors_are_synchronous(L):
     assert L.ss_quantize_nvfp4_ex(ctypes.byref(a)) == B.SS_ERR_INVALID_ARG
     assert L.ss_tensor_amax(P(base), -5, P(base), 0, None) == B.SS_ERR_INVALID_ARG
     assert L.ss_dequantize_nvfp4(P(base), P(base), 4, 20, None, P(base), None) == B.SS_ERR_INVALID_ARG
+    # batched forms: bad shape / window / missing amax / misalignment, all before any launch
+    io = (B.TensorIO * 2)()
+    io[0] = B.TensorIO(base, 4, 32, None, base, base, None, None, None, None)
+    io[1] = B.TensorIO(base, 4, 24, None, base, base, None, None, None, None)
+    assert L.ss_quantize_nvfp4_batched(io, 2, -8, 8, 1, None) == B.SS_ERR_INVALID_ARG
+    io[1] = B.TensorIO(base, 4, 32, None, base, base, None, None, None, None)
+    assert L.ss_quantize_nvfp4_batched(io, 2, 1, 8, 1, None) == B.SS_ERR_INVALID_ARG
+    assert L.ss_quantize_nvfp4_batched(io, 2, -8, 8, 2, None) == B.SS_ERR_INVALID_ARG
+    io[1] = B.TensorIO(base + 2, 4, 32, None, base, base, None, None, None, None)
+    assert L.ss_quantize_nvfp4_batched(io, 2, -8, 8, 1, None) == B.SS_ERR_ALIGNMENT
+    ptrs = (P * 2)(base, base + 8)
+    ns = (ctypes.c_int64 * 2)(64, 64)
+    assert L.ss_tensor_amax_batched(ptrs, ns, 2, P(base), 0, None) == B.SS_ERR_ALIGNMENT
+    ns[1] = -1
+    ptrs[1] = base
+    assert L.ss_tensor_amax_batched(ptrs, ns, 2, P(base), 0, None) == B.SS_ERR_INVALID_ARG
 
 
 @pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) is None and
@@ -74,6 +90,9 @@ def test_no_fallback_without_device(L):
     st = L.ss_quantize_nvfp4(P(base), 2, 32, 8, 1, P(base + 1024), P(base + 2048), None, None)
     assert st == B.SS_ERR_UNSUPPORTED_DEVICE
     assert L.ss_tensor_amax(P(base), 64, P(base + 1024), 0, None) == B.SS_ERR_UNSUPPORTED_DEVICE
+    io = (B.TensorIO * 1)(B.TensorIO(base, 2, 32, None, base + 1024, base + 2048, None, None, None,
+                                     None))
+    assert L.ss_quantize_nvfp4_batched(io, 1, -8, 8, 1, None) == B.SS_ERR_UNSUPPORTED_DEVICE
 
 
 def test_binding_raises_not_falls_back():

@@ -24,9 +24,6 @@ FMIN, FMAX = -8, 8
 
 class OracleOps:
     """Same interface as dist.CudaOps, backed by the oracle on CPU tensors."""
-    launches_amax = 1
-    launches_quant = 1
-    launches_sums = 0
 
     def __init__(self):
         import oracle
@@ -35,16 +32,22 @@ class OracleOps:
     def new_amax(self, n, device):
         return torch.zeros(n, dtype=torch.int32)
 
-    def amax(self, x, slot):
-        slot.fill_(self.o.tensor_amax(x))
+    def amax_all(self, xs, buf):
+        for k, x in enumerate(xs):
+            buf[k] = self.o.tensor_amax(x) if x.numel() else 0
+        return 1
 
     def alloc_out(self, x):
         return {}
 
-    def quantize_given(self, x, slot, out):
-        r = self.o.quantize(x, x.shape[0], x.shape[1], FMIN, FMAX, "given",
-                            amax_bits=int(slot.item()) & 0xFFFFFFFF)
-        out.update(codes=r.codes, scales=r.scales, err=r.err, G=r.G)
+    def quantize_all(self, xs, buf, outs):
+        for x, slot, out in zip(xs, buf, outs):
+            if x.shape[0] == 0:
+                continue
+            r = self.o.quantize(x, x.shape[0], x.shape[1], FMIN, FMAX, "given",
+                                amax_bits=int(slot.item()) & 0xFFFFFFFF)
+            out.update(codes=r.codes, scales=r.scales, err=r.err, G=r.G)
+        return 1
 
 
 def _tensors():

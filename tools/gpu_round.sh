@@ -1,15 +1,26 @@
 #!/bin/bash
-# One gpurun session: GPU tests, a bench line, the ncu launch list and one
-# full ncu capture of the quantize kernel.  Usage (from the repo root):
-#   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh TAG'
+# One gpurun session: GPU tests, kernel sweep, a bench line, the ncu launch
+# list of our kernels and one full ncu capture of the quantize kernel.
+#   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh TAG [steps]'
 TAG=${1:-r01}
+STEPS=${2:-all}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
-nvidia-smi > gpurun_out/nvsmi_$TAG.txt 2>&1; nproc >> gpurun_out/nvsmi_$TAG.txt; lscpu | head -20 >> gpurun_out/nvsmi_$TAG.txt
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke_$TAG.log
-timeout 900 python bench.py --steps 5 --warmup 3 --out gpurun_out/bench_$TAG.json > gpurun_out/bench_$TAG.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_$TAG.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_launch_$TAG.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:quant_kernel -s 20 -c 1 -o gpurun_out/quant_full_$TAG python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_full_$TAG.log 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:amax_kernel -s 20 -c 1 -o gpurun_out/amax_full_$TAG python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_amax_$TAG.log 2>&1
+(nvidia-smi; nproc; lscpu | head -20) > gpurun_out/host_$TAG.txt 2>&1
+has() { [[ "$STEPS" == all || ",$STEPS," == *",$1,"* ]]; }
+if has test; then
+  timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke_$TAG.log
+fi
+if has kbench; then
+  timeout 1200 python tools/kbench.py run --variants ${KB_VARIANTS:-base,mb3,mb5} > gpurun_out/kbench_$TAG.jsonl 2> gpurun_out/kbench_$TAG.err
+fi
+if has bench; then
+  timeout 900 python bench.py --steps 5 --warmup 3 --out gpurun_out/bench_$TAG.json > gpurun_out/bench_$TAG.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_$TAG.log
+fi
+if has ncu; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"quant_kernel|amax_kernel" -c 40 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --profile --steps 2 --warmup 1 > gpurun_out/ncu_launch_$TAG.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:quant_kernel -s 3 -c 1 -o gpurun_out/quant_full_$TAG python tools/kbench.py one --variants base --layers 2 --reps 1 --windows=-8:8 > gpurun_out/ncu_full_$TAG.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:amax_kernel -s 3 -c 1 -o gpurun_out/amax_full_$TAG python tools/kbench.py one --variants base --layers 2 --reps 1 --windows=-8:8 > gpurun_out/ncu_amax_$TAG.log 2>&1
+fi
 echo done

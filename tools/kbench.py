@@ -1,0 +1,104 @@
+#!/usr/bin/env python
+"""Kernel tuning sweep: time the batched amax and quantize launches of libss
+builds (variants compiled with different -D flags) on a fixed synthetic batch.
+
+    python tools/kbench.py build                 # here (CPU): compile the variants
+    python tools/kbench.py run [--variants a,b]  # on the GPU box: one JSON line per case
+
+Each variant runs in its own process (SS_LIB_VARIANT selects libss_<v>.so).
+Timing: CUDA events on the launching stream, 3 warm-ups, median of 10; the
+batch (first LAYERS layers of the Qwen3-8B workload, > 1 GB) exceeds L2.
+Not the driver's bench: that is bench.py.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+VARIANTS = {
+    "base": [],
+    "mb3": ["SS_MIN_BLOCKS=3"],
+    "mb5": ["SS_MIN_BLOCKS=5"],
+}
+WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
+
+
+def build(names):
+    from paper_2605_12464_b200 import build as b
+    for v in names:
+        if v == "base":
+            b.build()
+        else:
+            b.build(variant=v, defines=VARIANTS[v])
+        print("built", v, flush=True)
+
+
+def run_one(variant, layers, windows, reps):
+    import torch
+    import ssgen
+    if variant != "base":
+        os.environ["SS_LIB_VARIANT"] = variant
+    import paper_2605_12464_b200 as ss
+    dev = torch.device("cuda", 0)
+    specs = ssgen.workload("c2_qwen3_8b_weights")[: 7 * layers]
+    xs = [ssgen.generate(s.kind, s.rows, s.cols, seed=ssgen.workloads.BASE_SEED, tid=s.tid,
+                         device=dev) for s in specs]
+    n = sum(x.numel() for x in xs)
+    outs = [ss.alloc_out(x, want_offsets=False) for x in xs]
+    amax = torch.zeros(len(xs), dtype=torch.int32, device=dev)
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ts.sort()
+        return ts[len(ts) // 2]
+
+    t_amax = timed(lambda: ss.tensor_amax_batched(xs, out=amax))
+    print(json.dumps({"variant": variant, "kernel": "amax", "ms": t_amax, "elements": n,
+                      "hbm_gbs": 2 * n / t_amax / 1e6}), flush=True)
+    for fmin, fmax in windows:
+        t = timed(lambda: ss.quantize_batched(xs, outs, fmin=fmin, fmax=fmax, gmode="device_amax",
+                                              amax=amax))
+        print(json.dumps({"variant": variant, "kernel": "quant", "window": [fmin, fmax], "ms": t,
+                          "elements": n, "gelem_s": n / t / 1e6, "bf16_gbs": 2 * n / t / 1e6,
+                          "bytes_gbs": 3.0625 * n / t / 1e6}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", choices=["build", "run", "one"])
+    ap.add_argument("--variants", default=",".join(VARIANTS))
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--windows", default=None, help="e.g. -8:8,0:0")
+    a = ap.parse_args()
+    names = a.variants.split(",")
+    wins = WINDOWS if not a.windows else [tuple(int(v) for v in w.split(":"))
+                                           for w in a.windows.split(",")]
+    if a.mode == "build":
+        build(names)
+    elif a.mode == "one":
+        run_one(names[0], a.layers, wins, a.reps)
+    else:
+        for v in names:
+            cmd = [sys.executable, __file__, "one", "--variants", v, "--layers", str(a.layers),
+                   "--reps", str(a.reps), "--windows", ",".join("%d:%d" % w for w in wins)]
+            subprocess.run(cmd, timeout=900)
+
+
+if __name__ == "__main__":
+    main()
