@@ -194,6 +194,27 @@ SS_API ss_status ss_quantize_nvfp4_host(const void* h_in_bf16, int64_t rows, int
                                  int f_max, int global_scale_mode, uint8_t* h_codes,
                                  uint8_t* h_scales, float* h_err);
 
+/* One tensor of ss_quantize_nvfp4_host_batched: HOST buffers. */
+typedef struct {
+  const void* h_in_bf16;        /* [rows][cols] bf16                                        */
+  int64_t rows, cols;           /* rows >= 0, cols % 16 == 0                                */
+  uint8_t* h_codes;             /* [rows][cols/2] u8                                        */
+  uint8_t* h_scales;            /* [rows][cols/16] u8                                       */
+  float* h_err;                 /* nullable: [nb][2] f32 {err_best, err_base}               */
+} ss_host_tensor_io;
+
+/*
+ * End to end from HOST memory for a list of tensors (the e2e leg of bench.py
+ * at N = 1): tensor k is copied in, its amax (SS_GLOBAL_TENSOR: each tensor's
+ * own G) and quantization run, and its outputs are copied out, while tensor
+ * k+1 is already being copied in and tensor k-1 copied out: three internal
+ * streams and a ring of library-owned device slots, each sized for the
+ * largest tensor.  Host buffers should be pinned.  Synchronous.  Results are
+ * bit-identical to ss_quantize_nvfp4_batched.
+ */
+SS_API ss_status ss_quantize_nvfp4_host_batched(const ss_host_tensor_io* tensors, int count,
+                                         int f_min, int f_max, int global_scale_mode);
+
 /* Synchronizes `stream`, returns and clears the sticky device flags of this
  * (device, stream) workspace: bit 0 = non-finite input seen (SS_ERR_NONFINITE),
  * bit 1 = global scale out of range (SS_ERR_RANGE). */

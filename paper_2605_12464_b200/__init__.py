@@ -19,6 +19,7 @@ from ._binding import (  # noqa: F401
     quantize,
     quantize_batched,
     quantize_host,
+    quantize_host_batched,
     quantize_simple,
     status_string,
     tensor_amax,
@@ -26,6 +27,6 @@ from ._binding import (  # noqa: F401
 )
 
 __all__ = [
-    "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host",
+    "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host", "quantize_host_batched",
     "device_status", "status_string", "SSError", "QuantOut", "GMODES",
 ]

@@ -48,6 +48,17 @@ class TensorIO(ctypes.Structure):
     ]
 
 
+class HostTensorIO(ctypes.Structure):
+    _fields_ = [
+        ("h_in_bf16", ctypes.c_void_p),
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("h_codes", ctypes.c_void_p),
+        ("h_scales", ctypes.c_void_p),
+        ("h_err", ctypes.c_void_p),
+    ]
+
+
 class QuantArgs(ctypes.Structure):
     _fields_ = [
         ("in_bf16", ctypes.c_void_p),
@@ -95,6 +106,8 @@ def lib():
             L.ss_dequantize_nvfp4.argtypes = [P, P, i64, i64, P, P, P]
             L.ss_quantize_nvfp4_host.restype = I
             L.ss_quantize_nvfp4_host.argtypes = [P, i64, i64, I, I, I, P, P, P]
+            L.ss_quantize_nvfp4_host_batched.restype = I
+            L.ss_quantize_nvfp4_host_batched.argtypes = [ctypes.POINTER(HostTensorIO), I, I, I, I]
             L.ss_get_device_status.restype = I
             L.ss_get_device_status.argtypes = [ctypes.POINTER(ctypes.c_int), P]
             _lib = L
@@ -248,6 +261,21 @@ def quantize_host(h_x, rows: int, cols: int, fmin: int, fmax: int, gmode: str,
     _check(lib().ss_quantize_nvfp4_host(_ptr(h_x), rows, cols, int(fmin), int(fmax), GMODES[gmode],
                                         _ptr(h_codes), _ptr(h_scales), _ptr(h_err)),
            "ss_quantize_nvfp4_host")
+
+
+def quantize_host_batched(h_xs, h_codes, h_scales, h_errs=None, radius=None, fmin=None,
+                          fmax=None, gmode: str = "tensor"):
+    """End to end from host memory for a list of tensors (ss_quantize_nvfp4_host_batched);
+    synchronous.  Host tensors should be pinned."""
+    lo, hi = _window(radius, fmin, fmax)
+    n = len(h_xs)
+    arr = (HostTensorIO * max(n, 1))()
+    for i, x in enumerate(h_xs):
+        rows, cols = x.shape
+        arr[i] = HostTensorIO(_ptr(x), rows, cols, _ptr(h_codes[i]), _ptr(h_scales[i]),
+                              _ptr(h_errs[i]) if h_errs is not None else None)
+    _check(lib().ss_quantize_nvfp4_host_batched(arr, n, lo, hi, GMODES[gmode]),
+           "ss_quantize_nvfp4_host_batched")
 
 
 def device_status(stream=None) -> int:

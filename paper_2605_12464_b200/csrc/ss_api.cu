@@ -26,15 +26,13 @@ using ss::QuantBatch;
 // ---- per-(device, stream) workspace -----------------------------------------
 struct Workspace {
   uint32_t* flags = nullptr;     // sticky status flags (1 word)
-  uint32_t* tick2 = nullptr;     // [kMaxTensors] per-tensor tickets (zero, self re-arming)
+  uint32_t* tick = nullptr;      // [kMaxTensors] per-tensor tickets (zero, self re-arming)
   uint32_t* amax = nullptr;      // SS_GLOBAL_TENSOR slots
   int64_t amax_cap = 0;
   double2* part1 = nullptr;      // per-task partial sums
   int64_t part1_cap = 0;
-  double2* part2 = nullptr;      // per-group partial sums
+  double2* part2 = nullptr;      // per-segment partial sums
   int64_t part2_cap = 0;
-  uint32_t* tick1 = nullptr;     // per-group tickets (zero, self re-arming)
-  int64_t group_cap = 0;
 };
 
 std::mutex g_mu;
@@ -98,7 +96,7 @@ ss_status get_ws(int dev, void* stream, Workspace** out) {
     if (cudaMalloc(&p, bytes) != cudaSuccess) return SS_ERR_CUDA;
     if (cudaMemset(p, 0, bytes) != cudaSuccess) return SS_ERR_CUDA;
     w.flags = reinterpret_cast<uint32_t*>(p);
-    w.tick2 = w.flags + 1;
+    w.tick = w.flags + 1;
   }
   *out = &w;
   return SS_OK;
@@ -192,8 +190,21 @@ int occupancy(QuantKernel k) {
 }
 
 inline int64_t tasks_of(int64_t nb) { return (nb + ss::kTaskBlocks - 1) / ss::kTaskBlocks; }
-inline int64_t groups_of(int64_t nb) {
-  return (tasks_of(nb) + ss::kGroupTasks - 1) / ss::kGroupTasks;
+inline int64_t segs_of(int64_t nb) {
+  return (tasks_of(nb) + ss::kSegTasks - 1) / ss::kSegTasks;
+}
+
+int sums_grid(int sms) {
+  static int occ = 0;
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ss::sums_kernel, ss::kThreads, 0) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      occ = 4;
+    }
+    occ = std::max(occ, 1);
+  }
+  return sms * occ;
 }
 
 ss_status validate_io(const ss_tensor_io& t, int gmode) {
@@ -227,7 +238,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   if (ss_status s = get_ws(dev, stream, &ws)) return s;
 
   // sizes of the largest launch (workspace grown once, before any launch)
-  int64_t max_tasks = 0, max_groups = 0;
+  int64_t max_tasks = 0, max_segs = 0;
   bool any_sums = false;
   {
     int64_t tk = 0, gr = 0;
@@ -237,22 +248,21 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       if (nb == 0) continue;
       if (in_batch == ss::kMaxTensors) {
         max_tasks = std::max(max_tasks, tk);
-        max_groups = std::max(max_groups, gr);
+        max_segs = std::max(max_segs, gr);
         tk = gr = 0;
         in_batch = 0;
       }
       tk += tasks_of(nb);
-      gr += groups_of(nb);
+      gr += segs_of(nb);
       in_batch++;
       any_sums |= io[i].d_err_sums != nullptr;
     }
     max_tasks = std::max(max_tasks, tk);
-    max_groups = std::max(max_groups, gr);
+    max_segs = std::max(max_segs, gr);
   }
   if (any_sums) {
     if (ss_status s = grow_dev(&ws->part1, &ws->part1_cap, max_tasks, false, cs)) return s;
-    if (ss_status s = grow_dev(&ws->part2, &ws->part2_cap, max_groups, false, cs)) return s;
-    if (ss_status s = grow_dev(&ws->tick1, &ws->group_cap, max_groups, true, cs)) return s;
+    if (ss_status s = grow_dev(&ws->part2, &ws->part2_cap, max_segs, false, cs)) return s;
   }
 
   // SS_GLOBAL_TENSOR: the amax pass of every tensor first (a2)
@@ -283,9 +293,9 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.gmode = gmode == SS_GLOBAL_NONE ? 0 : 1;
     b.part1 = ws->part1;
     b.part2 = ws->part2;
-    b.tick1 = ws->tick1;
-    b.tick2 = ws->tick2;
+    b.tick = ws->tick;
     b.flags = ws->flags;
+    bool sums = false;
     int64_t tk = 0, gr = 0;
     for (; i < count && b.n < ss::kMaxTensors; i++) {
       const ss_tensor_io& t = io[i];
@@ -305,16 +315,23 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       q.amax = amax[i];
       q.nb = nb;
       q.task0 = tk;
-      q.group0 = gr;
+      q.seg0 = gr;
       tk += tasks_of(nb);
-      gr += groups_of(nb);
+      gr += segs_of(nb);
+      sums |= t.d_err_sums != nullptr;
     }
     if (b.n == 0) break;
     b.ntasks = tk;
+    b.nsegs = gr;
     const int64_t want = (tk + ss::kWarps - 1) / ss::kWarps;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, slots));
     k<<<grid, ss::kThreads, 0, cs>>>(b);
     if (ss_status s = launch_status()) return s;
+    if (sums) {
+      const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(gr, sums_grid(info.sms)));
+      ss::sums_kernel<<<g2, ss::kThreads, 0, cs>>>(b);
+      if (ss_status s = launch_status()) return s;
+    }
   }
   return SS_OK;
 }
@@ -357,6 +374,18 @@ ss_status grow(void** p, size_t* cap, size_t need) {
   *cap = need;
   return SS_OK;
 }
+
+// Ring of whole-tensor device slots for the batched host pipeline.
+struct HostRing {
+  static constexpr int kSlots = 3;
+  void* mem = nullptr;
+  size_t slot_bytes = 0;
+  uint32_t* amax = nullptr;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  cudaEvent_t in_ready[kSlots], out_ready[kSlots], slot_free[kSlots];
+};
+std::mutex g_ring_mu;
+std::map<int, HostRing> g_rings;
 
 }  // namespace
 
@@ -554,6 +583,99 @@ ss_status ss_quantize_nvfp4_host(const void* h_in, int64_t rows, int64_t cols, i
   cudaError_t e2 = cudaStreamSynchronize(hp.s_d2h);
   cudaError_t e3 = cudaStreamSynchronize(hp.s_h2d);
   return done((e1 || e2 || e3) ? SS_ERR_CUDA : SS_OK);
+}
+
+ss_status ss_quantize_nvfp4_host_batched(const ss_host_tensor_io* t, int count, int f_min,
+                                         int f_max, int global_scale_mode) {
+  if (count < 0 || (count > 0 && !t) || f_min > 0 || f_max < 0) return SS_ERR_INVALID_ARG;
+  if (global_scale_mode != SS_GLOBAL_NONE && global_scale_mode != SS_GLOBAL_TENSOR)
+    return SS_ERR_INVALID_ARG;
+  int64_t max_n = 0;
+  bool any_err = false;
+  for (int i = 0; i < count; i++) {
+    if (t[i].rows < 0 || t[i].cols < 0 || t[i].cols % 16 != 0) return SS_ERR_INVALID_ARG;
+    const int64_t n = t[i].rows * t[i].cols;
+    if (n > 0 && (!t[i].h_in_bf16 || !t[i].h_codes || !t[i].h_scales)) return SS_ERR_INVALID_ARG;
+    max_n = std::max(max_n, n);
+    any_err |= t[i].h_err != nullptr;
+  }
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  if (count == 0 || max_n == 0) return SS_OK;
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  HostRing& R = g_rings[dev];
+  if (!R.s_h2d) {
+    if (cudaStreamCreateWithFlags(&R.s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&R.s_comp, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&R.s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+      return SS_ERR_CUDA;
+    for (int k = 0; k < HostRing::kSlots; k++)
+      if (cudaEventCreateWithFlags(&R.in_ready[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&R.out_ready[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&R.slot_free[k], cudaEventDisableTiming) != cudaSuccess)
+        return SS_ERR_CUDA;
+  }
+  const size_t per_slot = (size_t)max_n * 2 + (size_t)max_n / 2 + (size_t)max_n / 16 +
+                          (any_err ? (size_t)max_n / 2 : 0) + 256;
+  if (per_slot > R.slot_bytes) {
+    cudaStreamSynchronize(R.s_h2d);
+    cudaStreamSynchronize(R.s_comp);
+    cudaStreamSynchronize(R.s_d2h);
+    if (R.mem) cudaFree(R.mem);
+    R.mem = nullptr;
+    R.slot_bytes = 0;
+    if (cudaMalloc(&R.mem, per_slot * HostRing::kSlots) != cudaSuccess) return SS_ERR_CUDA;
+    R.slot_bytes = per_slot;
+  }
+  if (!R.amax && cudaMalloc(&R.amax, 4 * HostRing::kSlots) != cudaSuccess) return SS_ERR_CUDA;
+  const bool tensor = global_scale_mode == SS_GLOBAL_TENSOR;
+  for (int i = 0; i < count; i++) {
+    const int64_t n = t[i].rows * t[i].cols, nb = n / 16;
+    if (n == 0) continue;
+    const int k = i % HostRing::kSlots;
+    char* base = reinterpret_cast<char*>(R.mem) + (size_t)k * R.slot_bytes;
+    void* d_in = base;
+    uint8_t* d_codes = reinterpret_cast<uint8_t*>(base + (((size_t)n * 2 + 255) & ~(size_t)255));
+    uint8_t* d_scales = d_codes + nb * 8;
+    float* d_err = t[i].h_err ? reinterpret_cast<float*>(
+                                    (reinterpret_cast<uintptr_t>(d_scales + nb) + 7) & ~(uintptr_t)7)
+                              : nullptr;
+    // the slot's previous tensor must be fully copied out before reuse
+    if (cudaStreamWaitEvent(R.s_h2d, R.slot_free[k], 0) != cudaSuccess) return SS_ERR_CUDA;
+    if (cudaMemcpyAsync(d_in, t[i].h_in_bf16, (size_t)n * 2, cudaMemcpyHostToDevice, R.s_h2d) !=
+        cudaSuccess)
+      return SS_ERR_CUDA;
+    cudaEventRecord(R.in_ready[k], R.s_h2d);
+    cudaStreamWaitEvent(R.s_comp, R.in_ready[k], 0);
+    ss_tensor_io io;
+    std::memset(&io, 0, sizeof(io));
+    io.in_bf16 = d_in;
+    io.rows = t[i].rows;
+    io.cols = t[i].cols;
+    io.d_amax_bits = R.amax + k;
+    io.out_codes = d_codes;
+    io.out_scales = d_scales;
+    io.out_err = d_err;
+    if (tensor) {
+      const void* p = d_in;
+      if (ss_status s = amax_launch(&p, &n, R.amax + k, 1, false, R.s_comp, info.sms)) return s;
+    }
+    if (ss_status s = quantize_core(&io, 1, f_min, f_max,
+                                    tensor ? SS_GLOBAL_DEVICE_AMAX : SS_GLOBAL_NONE, R.s_comp))
+      return s;
+    cudaEventRecord(R.out_ready[k], R.s_comp);
+    cudaStreamWaitEvent(R.s_d2h, R.out_ready[k], 0);
+    cudaMemcpyAsync(t[i].h_codes, d_codes, (size_t)nb * 8, cudaMemcpyDeviceToHost, R.s_d2h);
+    cudaMemcpyAsync(t[i].h_scales, d_scales, (size_t)nb, cudaMemcpyDeviceToHost, R.s_d2h);
+    if (d_err)
+      cudaMemcpyAsync(t[i].h_err, d_err, (size_t)nb * 8, cudaMemcpyDeviceToHost, R.s_d2h);
+    if (cudaEventRecord(R.slot_free[k], R.s_d2h) != cudaSuccess) return SS_ERR_CUDA;
+  }
+  cudaError_t e1 = cudaStreamSynchronize(R.s_h2d);
+  cudaError_t e2 = cudaStreamSynchronize(R.s_comp);
+  cudaError_t e3 = cudaStreamSynchronize(R.s_d2h);
+  return (e1 || e2 || e3) ? SS_ERR_CUDA : SS_OK;
 }
 
 }  // extern "C"

@@ -27,7 +27,10 @@
 #include <stdint.h>
 
 #ifndef SS_MIN_BLOCKS
-#define SS_MIN_BLOCKS 4
+#define SS_MIN_BLOCKS 5
+#endif
+#ifndef SS_AMAX_MODE
+#define SS_AMAX_MODE 1   // 0: 32 KiB chunk per CTA iteration; 1: grid-stride, 4 loads in flight
 #endif
 
 namespace ss {
@@ -36,10 +39,8 @@ constexpr int kWarps = 8;                     // warps per CTA
 constexpr int kThreads = 32 * kWarps;
 constexpr int kTaskBlocks = 32;               // NVFP4 blocks per warp task (one per lane)
 constexpr int kTaskBytes = kTaskBlocks * 32;  // 1 KiB of bf16 input per task
-constexpr int kStages = 2;                    // per-warp smem buffers
-constexpr int kPad = 126;                     // candidate-table padding (|f| <= 126)
-constexpr int kTabW = 127 + 2 * kPad;         // entries per half-table
-constexpr int kGroupTasks = 256;              // level-1 group of the error-sum reduction
+constexpr int kStages = 4;                    // per-warp smem buffers (tasks in flight)
+constexpr int kSegTasks = 4096;               // tasks per CTA of the error-sum kernel
 constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
 constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
 constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk (32 KiB)
@@ -158,21 +159,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------------
-// Candidate table.  Two halves of kTabW entries; entry i of a half stands for
-// the unclamped candidate code k = i - kPad:
+// Candidate table.  Two halves of TabW = 127 + 2*Pad entries (Pad = the
+// largest |f| of the kernel's window); entry i of a half stands for the
+// unclamped candidate code k = i - Pad:
 //   half 0 (used when c0 == 0): code = 0 for k <= 0 (the zero-scale candidate,
 //            R3), else min(k, 126);
 //   half 1 (c0 >= 1):           code = clamp(k, 1, 126).
-// A block's candidates are base[f] with base = half + kPad + c0, so
+// A block's candidates are base[f] with base = half + Pad + c0, so
 // out-of-range offsets become duplicates of the nearest valid code, which
 // never change the lexicographic (loss, code) minimum (R2, R4): no branches.
 // Entry = {rho, rho, (-s as f16) | code << 16, 0} with rho = RN(1/s) (R7);
 // code 0 has rho = 0 and -s = -0.
 // ---------------------------------------------------------------------------
+template <int Pad>
 __device__ __forceinline__ void build_cand_table(uint4* tab) {
-  for (int i = threadIdx.x; i < 2 * kTabW; i += blockDim.x) {
-    const int half = i / kTabW;
-    const int k = i - half * kTabW - kPad;
+  constexpr int TabW = 127 + 2 * Pad;
+  for (int i = threadIdx.x; i < 2 * TabW; i += blockDim.x) {
+    const int half = i / TabW;
+    const int k = i - half * TabW - Pad;
     int code = half == 0 ? (k <= 0 ? 0 : k) : (k < 1 ? 1 : k);
     code = code > 126 ? 126 : code;
     uint4 e;
@@ -218,7 +222,7 @@ struct QTensor {
   const uint32_t* amax;     // gmode given: FP32 bits of the tensor amax
   int64_t nb;               // NVFP4 blocks
   int64_t task0;            // first global task of this tensor
-  int64_t group0;           // first global level-1 group of this tensor
+  int64_t seg0;             // first global segment (error-sum kernel CTA) of this tensor
 };
 
 struct QuantBatch {
@@ -226,10 +230,10 @@ struct QuantBatch {
   int fmin, fmax;           // window (runtime loop variant only)
   int gmode;                // 0: G = 1; 1: G from t[i].amax
   int64_t ntasks;           // total tasks of the batch
+  int64_t nsegs;            // total error-sum segments of the batch
   double2* part1;           // per task {sum best, sum base}   (when any sums wanted)
-  double2* part2;           // per level-1 group
-  uint32_t* tick1;          // per group, zero and self re-arming
-  uint32_t* tick2;          // per tensor, zero and self re-arming
+  double2* part2;           // per segment
+  uint32_t* tick;           // per tensor, zero and self re-arming
   uint32_t* flags;
   QTensor t[kMaxTensors];
 };
@@ -262,12 +266,13 @@ __device__ __forceinline__ int locate_task(const QuantBatch& p, int64_t k, int f
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) amax_kernel(const __grid_constant__ AmaxBatch p) {
   const int lane = threadIdx.x & 31;
+  const uint32_t M = 0x7FFF7FFFu;
   int ti = 0;
+#if SS_AMAX_MODE == 0
   for (int64_t ch = blockIdx.x; ch < p.nchunks; ch += gridDim.x) {
     while (ti + 1 < p.n && p.t[ti + 1].chunk0 <= ch) ti++;
     const ATensor& T = p.t[ti];
     const int64_t v0 = (ch - T.chunk0) * kAmaxChunk + threadIdx.x;
-    const uint32_t M = 0x7FFF7FFFu;
     uint32_t m = 0;
     uint4 v[kAmaxVecs];
 #pragma unroll
@@ -279,7 +284,6 @@ __global__ void __launch_bounds__(kThreads) amax_kernel(const __grid_constant__ 
     for (int k = 0; k < kAmaxVecs; k++)
       m = __vmaxu2(m, __vmaxu2(__vmaxu2(v[k].x & M, v[k].y & M), __vmaxu2(v[k].z & M, v[k].w & M)));
     uint32_t r = max(m & 0xFFFFu, m >> 16);
-    // trailing elements: handled by the chunk that holds the last vector
     if (T.ntail && (ch - T.chunk0) == (T.nvec / kAmaxChunk) && threadIdx.x < T.ntail) {
       const uint16_t* tail = reinterpret_cast<const uint16_t*>(T.in + T.nvec);
       r = max(r, (uint32_t)(tail[threadIdx.x] & 0x7FFFu));
@@ -287,11 +291,46 @@ __global__ void __launch_bounds__(kThreads) amax_kernel(const __grid_constant__ 
     r = __reduce_max_sync(0xFFFFFFFFu, r);
     if (lane == 0 && r) atomicMax(T.out, r << 16);  // bf16 bits -> FP32 bits (exact)
   }
+#else
+  // Tensors one after another; within a tensor every thread strides over the
+  // whole grid with 4 independent 16-B loads in flight (the classic streaming
+  // pattern: consecutive warps read consecutive 512 B).
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (ti = 0; ti < p.n; ti++) {
+    const ATensor& T = p.t[ti];
+    uint32_t m = 0;
+    int64_t i = g;
+    for (; i + 3 * stride < T.nvec; i += 4 * stride) {
+      const uint4 a = __ldcs(T.in + i), b = __ldcs(T.in + i + stride);
+      const uint4 c = __ldcs(T.in + i + 2 * stride), d = __ldcs(T.in + i + 3 * stride);
+      const uint32_t x0 = __vmaxu2(__vmaxu2(a.x & M, a.y & M), __vmaxu2(a.z & M, a.w & M));
+      const uint32_t x1 = __vmaxu2(__vmaxu2(b.x & M, b.y & M), __vmaxu2(b.z & M, b.w & M));
+      const uint32_t x2 = __vmaxu2(__vmaxu2(c.x & M, c.y & M), __vmaxu2(c.z & M, c.w & M));
+      const uint32_t x3 = __vmaxu2(__vmaxu2(d.x & M, d.y & M), __vmaxu2(d.z & M, d.w & M));
+      m = __vmaxu2(m, __vmaxu2(__vmaxu2(x0, x1), __vmaxu2(x2, x3)));
+    }
+    for (; i < T.nvec; i += stride) {
+      const uint4 a = __ldcs(T.in + i);
+      m = __vmaxu2(m, __vmaxu2(__vmaxu2(a.x & M, a.y & M), __vmaxu2(a.z & M, a.w & M)));
+    }
+    uint32_t r = max(m & 0xFFFFu, m >> 16);
+    if (g < T.ntail) {
+      const uint16_t* tail = reinterpret_cast<const uint16_t*>(T.in + T.nvec);
+      r = max(r, (uint32_t)(tail[g] & 0x7FFFu));
+    }
+    r = __reduce_max_sync(0xFFFFFFFFu, r);
+    if (lane == 0 && r) atomicMax(T.out, r << 16);  // bf16 bits -> FP32 bits (exact)
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
-// Error sums: deterministic two-level reduction finished by the last warp of
-// each level (ticket counters), in a fixed order independent of the grid.
+// Error sums.  The quantize kernel stores one {sum best, sum base} partial per
+// warp task (a fixed lane tree); sums_kernel then reduces each tensor's task
+// partials in a fixed order: CTA k sums segment k (kSegTasks tasks) and the
+// last CTA of a tensor (ticket counter) sums the tensor's segment partials.
+// Deterministic for any grid of either kernel.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -299,55 +338,57 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ void reduce_task_sums(const QuantBatch& p, int ti, int64_t task, double sb,
-                                              double sc) {
-  const int lane = threadIdx.x & 31;
-  const QTensor& T = p.t[ti];
-  sb = warp_sum(sb);
-  sc = warp_sum(sc);
-  const int64_t lt = task - T.task0;
-  const int64_t ntask_t = (T.nb + kTaskBlocks - 1) / kTaskBlocks;
-  const int64_t g = lt / kGroupTasks;
-  const int64_t ng = (ntask_t + kGroupTasks - 1) / kGroupTasks;
-  const int gsize = (int)min((int64_t)kGroupTasks, ntask_t - g * kGroupTasks);
-  uint32_t last = 0;
-  if (lane == 0) {
-    p.part1[task] = make_double2(sb, sc);
-    __threadfence();
-    last = atomicAdd(p.tick1 + T.group0 + g, 1u) == (uint32_t)(gsize - 1);
-  }
-  if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
-  __threadfence();
-  const double2* src = p.part1 + T.task0 + g * kGroupTasks;
+// Fixed-order CTA sum of n double2 values at src (thread-strided, then tree).
+__device__ __forceinline__ double2 cta_sum(const double2* src, int64_t n, double2* red) {
   double a = 0.0, c = 0.0;
-  for (int i = lane; i < gsize; i += 32) {
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) {
     const double2 v = __ldcg(src + i);
     a += v.x;
     c += v.y;
   }
   a = warp_sum(a);
   c = warp_sum(c);
-  last = 0;
-  if (lane == 0) {
-    p.part2[T.group0 + g] = make_double2(a, c);
-    p.tick1[T.group0 + g] = 0u;  // re-arm
-    __threadfence();
-    last = atomicAdd(p.tick2 + ti, 1u) == (uint32_t)(ng - 1);
-  }
-  if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
-  __threadfence();
-  a = c = 0.0;
-  for (int64_t i = lane; i < ng; i += 32) {
-    const double2 v = __ldcg(p.part2 + T.group0 + i);
-    a += v.x;
-    c += v.y;
-  }
-  a = warp_sum(a);
-  c = warp_sum(c);
-  if (lane == 0) {
-    T.sums[0] = a;
-    T.sums[1] = c;
-    p.tick2[ti] = 0u;  // re-arm
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(a, c);
+  __syncthreads();
+  double2 r = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kWarps; w++) {
+      r.x += red[w].x;
+      r.y += red[w].y;
+    }
+  return r;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kThreads) sums_kernel(const __grid_constant__ QuantBatch p) {
+  __shared__ double2 red[kWarps];
+  __shared__ uint32_t last;
+  int ti = 0;
+  for (int64_t sg = blockIdx.x; sg < p.nsegs; sg += gridDim.x) {
+    while (ti + 1 < p.n && p.t[ti + 1].seg0 <= sg) ti++;
+    const QTensor& T = p.t[ti];
+    if (!T.sums) continue;  // CTA-uniform
+    const int64_t ntask = (T.nb + kTaskBlocks - 1) / kTaskBlocks;
+    const int64_t nseg = (ntask + kSegTasks - 1) / kSegTasks;
+    const int64_t k = sg - T.seg0;
+    const int64_t t0 = k * kSegTasks;
+    const double2 r = cta_sum(p.part1 + T.task0 + t0, min((int64_t)kSegTasks, ntask - t0), red);
+    if (threadIdx.x == 0) {
+      p.part2[sg] = r;
+      __threadfence();
+      last = atomicAdd(p.tick + ti, 1u) == (uint32_t)(nseg - 1);
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      const double2 f = cta_sum(p.part2 + T.seg0, nseg, red);
+      if (threadIdx.x == 0) {
+        T.sums[0] = f.x;
+        T.sums[1] = f.y;
+        p.tick[ti] = 0u;  // re-arm
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -401,11 +442,13 @@ __device__ __forceinline__ float cand_loss(const uint64_t (&y2)[8], const float 
 // NEG/POS >= 0: compile-time window [-NEG, POS]; NEG < 0: runtime [fmin, fmax].
 template <int NEG, int POS>
 __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
-  __shared__ __align__(16) uint4 tab[2 * kTabW];
+  constexpr int Pad = NEG < 0 ? 126 : (NEG > POS ? NEG : POS);
+  constexpr int TabW = 127 + 2 * Pad;
+  __shared__ __align__(16) uint4 tab[2 * TabW];
   __shared__ __align__(128) uint4 buf[kWarps][kStages][kTaskBytes / 16];
   __shared__ __align__(8) uint64_t bar[kWarps][kStages];
 
-  build_cand_table(tab);
+  build_cand_table<Pad>(tab);
   if (threadIdx.x < kWarps * kStages) mbar_init(&bar[0][0] + threadIdx.x, 1);
   fence_mbar_init();
   __syncthreads();
@@ -430,8 +473,17 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     return global_scale(__ldg(p.t[ti].amax), p.flags, report);
   };
 
+  // prologue: tasks task, task+W, ..., task+(kStages-1)W in flight
   int ti = locate_task(p, task, 0);
-  issue(task, ti, 0);
+  {
+    int tj = ti;
+    for (int k = 0; k < kStages; k++) {
+      const int64_t tk = task + k * W;
+      if (tk >= p.ntasks) break;
+      tj = locate_task(p, tk, tj);
+      issue(tk, tj, k);
+    }
+  }
   float G = gscale(ti, task == p.t[ti].task0 && lane == 0);
   uint32_t phases = 0;
   int s = 0;
@@ -441,7 +493,6 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     float Gn = G;
     if (next < p.ntasks) {
       tn = locate_task(p, next, ti);
-      issue(next, tn, s ^ 1);
       Gn = gscale(tn, next == p.t[tn].task0 && lane == 0);
     }
     const QTensor& T = p.t[ti];
@@ -452,7 +503,11 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     mbar_wait(&bar[w][s], (phases >> s) & 1u);
     phases ^= 1u << s;
     const uint4 v0 = buf[w][s][2 * lane], v1 = buf[w][s][2 * lane + 1];
-    __syncwarp();  // stage s may be refilled from the next iteration on
+    __syncwarp();  // every lane has read stage s: refill it with task + kStages * W
+    {
+      const int64_t far = task + (int64_t)kStages * W;
+      if (far < p.ntasks) issue(far, locate_task(p, far, tn), s);
+    }
     const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     // a3: y = RN(x * G)
     float y[16];
@@ -468,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 #pragma unroll
     for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[i]));
     const int c0 = (int)e4m3_code(__fmul_rn(m, k6));
-    const uint4* base = tab + (c0 ? kTabW : 0) + kPad + c0;
+    const uint4* base = tab + (c0 ? TabW : 0) + Pad + c0;
 
     // a5 + a6: candidate search (Alg. 1 lines 5-10)
     float best = cand_loss(y2, y, base[0]);
@@ -492,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 
     // a7: emit the winner: nibbles of t = y * rho*, scale byte, offset, errors
     const uint32_t code = bsel >> 16;
-    const float rs = __uint_as_float(tab[(code ? kTabW : 0) + kPad + code].x);
+    const float rs = __uint_as_float(tab[(code ? TabW : 0) + Pad + code].x);
     const uint64_t rr = pack2(rs, rs);
     float t[16];
 #pragma unroll
@@ -506,8 +561,10 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       if (T.offsets) T.offsets[b] = (int8_t)((int)code - c0);
       if (T.err) __stcs(T.err + b, make_float2(best, loss0));
     }
-    if (T.sums) {
-      reduce_task_sums(p, ti, task, active ? (double)best : 0.0, active ? (double)loss0 : 0.0);
+    if (T.sums) {  // per-task partial (fixed lane tree); reduced by sums_kernel
+      const double sb = warp_sum(active ? (double)best : 0.0);
+      const double sc = warp_sum(active ? (double)loss0 : 0.0);
+      if (lane == 0) p.part1[task] = make_double2(sb, sc);
     }
     if (T.g_out && task == T.task0 && lane == 0) *T.g_out = G;
 
@@ -515,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     task = next;
     ti = tn;
     G = Gn;
-    s ^= 1;
+    s = s + 1 == kStages ? 0 : s + 1;
   }
 }
 

@@ -298,3 +298,18 @@ def test_tensor_amax_batched(ss, oracle_lib):
     got = a.cpu().numpy().view(np.uint32)
     for k, x in enumerate(xs):
         assert got[k] == (oracle_lib.tensor_amax(x) if x.numel() else 0)
+
+
+def test_host_batched_entry_point(ss, oracle_lib):
+    xs = _batch_tensors() + [ssgen.generate("weight_outlier", 700, 512, seed=8, tid=640)]
+    hx = [x.pin_memory() for x in xs]
+    hc = [torch.empty(x.shape[0], x.shape[1] // 2, dtype=torch.uint8).pin_memory() for x in xs]
+    hs = [torch.empty(x.shape[0], x.shape[1] // 16, dtype=torch.uint8).pin_memory() for x in xs]
+    he = [torch.empty(x.numel() // 16, 2, dtype=torch.float32).pin_memory() for x in xs]
+    for gmode in ("tensor", "none"):
+        ss.quantize_host_batched(hx, hc, hs, he, fmin=-2, fmax=6, gmode=gmode)
+        for x, c, s, e in zip(xs, hc, hs, he):
+            ref = oracle_lib.quantize(x, x.shape[0], x.shape[1], -2, 6, gmode)
+            assert np.array_equal(c.numpy(), ref.codes)
+            assert np.array_equal(s.numpy(), ref.scales)
+            assert np.array_equal(e.numpy().view(np.uint32), ref.err.view(np.uint32))

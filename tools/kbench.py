@@ -23,8 +23,9 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "mb3": ["SS_MIN_BLOCKS=3"],
-    "mb5": ["SS_MIN_BLOCKS=5"],
+    "mb4": ["SS_MIN_BLOCKS=4"],
+    "mb6": ["SS_MIN_BLOCKS=6"],
+    "amax0": ["SS_AMAX_MODE=0"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
 
