@@ -9,9 +9,12 @@
 // of 32 consecutive NVFP4 blocks (1 KiB of bf16), one block per lane.  A
 // launch covers a BATCH of up to kMaxTensors tensors whose tasks are numbered
 // consecutively, so one persistent grid walks every tensor of a step with no
-// per-tensor tail.  Each warp double-buffers its tasks in shared memory with
-// 1-D bulk async copies (cp.async.bulk, the TMA bulk path) completed on a
-// per-warp mbarrier, so no CTA-wide barrier exists after the prologue.
+// per-tensor tail.  Each warp keeps kStages tasks in flight in shared memory:
+// every lane stages its own 32-B block with two 16-B LDGSTS (cp.async) and
+// reads back only its own bytes, so no barrier of any kind exists after the
+// prologue.  (Per-warp 1-D TMA bulk copies were measured first: beyond ~64
+// outstanding bulk operations per SM their throughput collapses to ~2.4 TB/s,
+// tools/probes/bwprobe.cu; per-lane LDGSTS streams at the full 7.3 TB/s.)
 //
 // Inner loop per PAIR of elements and candidate (3 issue slots per
 // element-candidate; the candidate's {rho, rho, -s | code<<16} comes from one
@@ -124,38 +127,18 @@ __device__ __forceinline__ float f16_to_f32(uint16_t h) {
   return f;
 }
 
-// ---- shared-memory bulk copies (TMA bulk path) and mbarriers ---------------
+// ---- shared-memory staging -------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+// Per-lane asynchronous 16-B global -> shared copies (LDGSTS), grouped.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-// Arm `bar` for `bytes` and start the bulk copy global -> shared (one thread).
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  const uint32_t b = smem_u32(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(b)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "SS_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra SS_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -264,65 +247,54 @@ __device__ __forceinline__ int locate_task(const QuantBatch& p, int64_t k, int f
 // Amax kernel: unsigned max of |x| bf16 bit patterns (exact, NaN-propagating).
 // One 32 KiB chunk per CTA iteration, 8 independent 16-B loads per thread.
 // ---------------------------------------------------------------------------
+// CTA b owns the contiguous global chunk range [b*per, (b+1)*per) (chunk =
+// kAmaxChunk 16-B vectors of one tensor, kAmaxVecs independent coalesced loads
+// per thread).  The running max is kept per thread while the tensor stays the
+// same and reduced (warp redux + smem) into ONE atomicMax per (CTA, tensor).
 __global__ void __launch_bounds__(kThreads) amax_kernel(const __grid_constant__ AmaxBatch p) {
-  const int lane = threadIdx.x & 31;
+  __shared__ uint32_t red[kWarps];
   const uint32_t M = 0x7FFF7FFFu;
+  const int64_t per = (p.nchunks + gridDim.x - 1) / gridDim.x;
+  const int64_t c_lo = (int64_t)blockIdx.x * per;
+  const int64_t c_hi = min(p.nchunks, c_lo + per);
+  if (c_lo >= c_hi) return;  // CTA-uniform
   int ti = 0;
-#if SS_AMAX_MODE == 0
-  for (int64_t ch = blockIdx.x; ch < p.nchunks; ch += gridDim.x) {
-    while (ti + 1 < p.n && p.t[ti + 1].chunk0 <= ch) ti++;
+  while (ti + 1 < p.n && p.t[ti + 1].chunk0 <= c_lo) ti++;
+  uint32_t m = 0;
+  for (int64_t ch = c_lo; ch < c_hi; ch++) {
     const ATensor& T = p.t[ti];
     const int64_t v0 = (ch - T.chunk0) * kAmaxChunk + threadIdx.x;
-    uint32_t m = 0;
     uint4 v[kAmaxVecs];
 #pragma unroll
     for (int k = 0; k < kAmaxVecs; k++) {
       const int64_t i = v0 + (int64_t)k * kThreads;
       v[k] = i < T.nvec ? __ldcs(T.in + i) : make_uint4(0, 0, 0, 0);
     }
+    uint32_t mm = m;
 #pragma unroll
     for (int k = 0; k < kAmaxVecs; k++)
-      m = __vmaxu2(m, __vmaxu2(__vmaxu2(v[k].x & M, v[k].y & M), __vmaxu2(v[k].z & M, v[k].w & M)));
-    uint32_t r = max(m & 0xFFFFu, m >> 16);
+      mm = __vmaxu2(mm, __vmaxu2(__vmaxu2(v[k].x & M, v[k].y & M), __vmaxu2(v[k].z & M, v[k].w & M)));
+    m = mm;
+    // trailing elements: handled by the chunk that holds the last vector
     if (T.ntail && (ch - T.chunk0) == (T.nvec / kAmaxChunk) && threadIdx.x < T.ntail) {
       const uint16_t* tail = reinterpret_cast<const uint16_t*>(T.in + T.nvec);
-      r = max(r, (uint32_t)(tail[threadIdx.x] & 0x7FFFu));
+      m = __vmaxu2(m, (uint32_t)(tail[threadIdx.x] & 0x7FFFu));
     }
-    r = __reduce_max_sync(0xFFFFFFFFu, r);
-    if (lane == 0 && r) atomicMax(T.out, r << 16);  // bf16 bits -> FP32 bits (exact)
+    const bool flush = ch + 1 == c_hi || (ti + 1 < p.n && p.t[ti + 1].chunk0 <= ch + 1);
+    if (flush) {  // CTA-uniform
+      uint32_t r = __reduce_max_sync(0xFFFFFFFFu, max(m & 0xFFFFu, m >> 16));
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = r;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 1; w < kWarps; w++) r = max(r, red[w]);
+        r = max(r, red[0]);
+        if (r) atomicMax(T.out, r << 16);  // bf16 bits -> FP32 bits (exact)
+      }
+      __syncthreads();
+      m = 0;
+      while (ti + 1 < p.n && p.t[ti + 1].chunk0 <= ch + 1) ti++;
+    }
   }
-#else
-  // Tensors one after another; within a tensor every thread strides over the
-  // whole grid with 4 independent 16-B loads in flight (the classic streaming
-  // pattern: consecutive warps read consecutive 512 B).
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  for (ti = 0; ti < p.n; ti++) {
-    const ATensor& T = p.t[ti];
-    uint32_t m = 0;
-    int64_t i = g;
-    for (; i + 3 * stride < T.nvec; i += 4 * stride) {
-      const uint4 a = __ldcs(T.in + i), b = __ldcs(T.in + i + stride);
-      const uint4 c = __ldcs(T.in + i + 2 * stride), d = __ldcs(T.in + i + 3 * stride);
-      const uint32_t x0 = __vmaxu2(__vmaxu2(a.x & M, a.y & M), __vmaxu2(a.z & M, a.w & M));
-      const uint32_t x1 = __vmaxu2(__vmaxu2(b.x & M, b.y & M), __vmaxu2(b.z & M, b.w & M));
-      const uint32_t x2 = __vmaxu2(__vmaxu2(c.x & M, c.y & M), __vmaxu2(c.z & M, c.w & M));
-      const uint32_t x3 = __vmaxu2(__vmaxu2(d.x & M, d.y & M), __vmaxu2(d.z & M, d.w & M));
-      m = __vmaxu2(m, __vmaxu2(__vmaxu2(x0, x1), __vmaxu2(x2, x3)));
-    }
-    for (; i < T.nvec; i += stride) {
-      const uint4 a = __ldcs(T.in + i);
-      m = __vmaxu2(m, __vmaxu2(__vmaxu2(a.x & M, a.y & M), __vmaxu2(a.z & M, a.w & M)));
-    }
-    uint32_t r = max(m & 0xFFFFu, m >> 16);
-    if (g < T.ntail) {
-      const uint16_t* tail = reinterpret_cast<const uint16_t*>(T.in + T.nvec);
-      r = max(r, (uint32_t)(tail[g] & 0x7FFFu));
-    }
-    r = __reduce_max_sync(0xFFFFFFFFu, r);
-    if (lane == 0 && r) atomicMax(T.out, r << 16);  // bf16 bits -> FP32 bits (exact)
-  }
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -446,11 +418,8 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   constexpr int TabW = 127 + 2 * Pad;
   __shared__ __align__(16) uint4 tab[2 * TabW];
   __shared__ __align__(128) uint4 buf[kWarps][kStages][kTaskBytes / 16];
-  __shared__ __align__(8) uint64_t bar[kWarps][kStages];
 
   build_cand_table<Pad>(tab);
-  if (threadIdx.x < kWarps * kStages) mbar_init(&bar[0][0] + threadIdx.x, 1);
-  fence_mbar_init();
   __syncthreads();
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -459,13 +428,16 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   if (task >= p.ntasks) return;  // no CTA barrier follows
 
   const float k6 = __uint_as_float(kOneSixthBits);
+  // Stage s of this warp holds one task: lane l copies its own block (2 x 16 B,
+  // LDGSTS) and later reads back only what it copied, so no cross-lane sync
+  // is needed; one commit group per stage (empty groups past the end).
   auto issue = [&](int64_t tk, int ti, int s) {
-    if (lane == 0) {
-      const QTensor& T = p.t[ti];
-      const int64_t b0 = (tk - T.task0) * kTaskBlocks;
-      const int64_t nblk = min((int64_t)kTaskBlocks, T.nb - b0);
-      fence_proxy_async();
-      bulk_load(&buf[w][s][0], T.in + b0 * 32, (uint32_t)(nblk * 32), &bar[w][s]);
+    const QTensor& T = p.t[ti];
+    const int64_t b = (tk - T.task0) * kTaskBlocks + lane;
+    if (b < T.nb) {
+      const uint8_t* src = T.in + b * 32;
+      cp_async16(&buf[w][s][2 * lane], src);
+      cp_async16(&buf[w][s][2 * lane + 1], src + 16);
     }
   };
   auto gscale = [&](int ti, bool report) -> float {
@@ -479,13 +451,14 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     int tj = ti;
     for (int k = 0; k < kStages; k++) {
       const int64_t tk = task + k * W;
-      if (tk >= p.ntasks) break;
-      tj = locate_task(p, tk, tj);
-      issue(tk, tj, k);
+      if (tk < p.ntasks) {
+        tj = locate_task(p, tk, tj);
+        issue(tk, tj, k);
+      }
+      cp_async_commit();
     }
   }
   float G = gscale(ti, task == p.t[ti].task0 && lane == 0);
-  uint32_t phases = 0;
   int s = 0;
   for (;;) {
     const int64_t next = task + W;
@@ -500,13 +473,12 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     const bool active = b < T.nb;
 
     // a1: this lane's 32 B from the staged task; bf16 -> f32 is exact
-    mbar_wait(&bar[w][s], (phases >> s) & 1u);
-    phases ^= 1u << s;
+    cp_async_wait<kStages - 1>();  // this lane's copy of stage s has landed
     const uint4 v0 = buf[w][s][2 * lane], v1 = buf[w][s][2 * lane + 1];
-    __syncwarp();  // every lane has read stage s: refill it with task + kStages * W
-    {
+    {  // refill stage s with task + kStages * W (always commit: uniform group count)
       const int64_t far = task + (int64_t)kStages * W;
       if (far < p.ntasks) issue(far, locate_task(p, far, tn), s);
+      cp_async_commit();
     }
     const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     // a3: y = RN(x * G)
