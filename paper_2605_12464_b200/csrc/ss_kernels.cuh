@@ -32,6 +32,9 @@
 #ifndef SS_MIN_BLOCKS
 #define SS_MIN_BLOCKS 5
 #endif
+#ifndef SS_BPL
+#define SS_BPL 2         // NVFP4 blocks per lane per warp task
+#endif
 #ifndef SS_AMAX_MODE
 #define SS_AMAX_MODE 1   // 0: 32 KiB chunk per CTA iteration; 1: grid-stride, 4 loads in flight
 #endif
@@ -40,9 +43,10 @@ namespace ss {
 
 constexpr int kWarps = 8;                     // warps per CTA
 constexpr int kThreads = 32 * kWarps;
-constexpr int kTaskBlocks = 32;               // NVFP4 blocks per warp task (one per lane)
-constexpr int kTaskBytes = kTaskBlocks * 32;  // 1 KiB of bf16 input per task
-constexpr int kStages = 4;                    // per-warp smem buffers (tasks in flight)
+constexpr int kBPL = SS_BPL;                  // NVFP4 blocks per lane per task
+constexpr int kTaskBlocks = 32 * kBPL;        // NVFP4 blocks per warp task
+constexpr int kTaskBytes = kTaskBlocks * 32;  // bf16 input bytes per task
+constexpr int kStages = kBPL >= 4 ? 2 : 4 / kBPL;  // per-warp smem buffers (tasks in flight)
 constexpr int kSegTasks = 4096;               // tasks per CTA of the error-sum kernel
 constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
 constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
@@ -428,16 +432,22 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   if (task >= p.ntasks) return;  // no CTA barrier follows
 
   const float k6 = __uint_as_float(kOneSixthBits);
-  // Stage s of this warp holds one task: lane l copies its own block (2 x 16 B,
-  // LDGSTS) and later reads back only what it copied, so no cross-lane sync
-  // is needed; one commit group per stage (empty groups past the end).
+  // Stage s of this warp holds one task.  Lane l copies its own blocks
+  // l, l+32, ... (2 x 16-B LDGSTS each) and later reads back only what it
+  // copied, so no cross-lane sync is needed; one commit group per stage
+  // (empty groups past the end keep the group count uniform).
   auto issue = [&](int64_t tk, int ti, int s) {
     const QTensor& T = p.t[ti];
-    const int64_t b = (tk - T.task0) * kTaskBlocks + lane;
-    if (b < T.nb) {
-      const uint8_t* src = T.in + b * 32;
-      cp_async16(&buf[w][s][2 * lane], src);
-      cp_async16(&buf[w][s][2 * lane + 1], src + 16);
+    const int64_t b0 = (tk - T.task0) * kTaskBlocks;
+    const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
+    const uint8_t* src = T.in + b0 * 32;
+#pragma unroll
+    for (int u = 0; u < kBPL; u++) {
+      const int j = u * 32 + lane;
+      if (j < nblk) {
+        cp_async16(&buf[w][s][2 * j], src + j * 32);
+        cp_async16(&buf[w][s][2 * j + 1], src + j * 32 + 16);
+      }
     }
   };
   auto gscale = [&](int ti, bool report) -> float {
@@ -469,76 +479,88 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       Gn = gscale(tn, next == p.t[tn].task0 && lane == 0);
     }
     const QTensor& T = p.t[ti];
-    const int64_t b = (task - T.task0) * kTaskBlocks + lane;
-    const bool active = b < T.nb;
+    const int64_t b0 = (task - T.task0) * kTaskBlocks;   // first block of the task
+    const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
 
-    // a1: this lane's 32 B from the staged task; bf16 -> f32 is exact
-    cp_async_wait<kStages - 1>();  // this lane's copy of stage s has landed
-    const uint4 v0 = buf[w][s][2 * lane], v1 = buf[w][s][2 * lane + 1];
+    cp_async_wait<kStages - 1>();  // this lane's copies of stage s have landed
+    uint2* codes = T.codes + b0;
+    uint8_t* scales = T.scales + b0;
+    int8_t* offsets = T.offsets ? T.offsets + b0 : nullptr;
+    float2* err = T.err ? T.err + b0 : nullptr;
+    double sb = 0.0, sc = 0.0;
+    const uint64_t GG = pack2(G, G);
+
+#pragma unroll 1
+    for (int u = 0; u < kBPL; u++) {
+      const int j = u * 32 + lane;
+      const bool active = j < nblk;
+      // a1 + a3: bf16 -> f32 is exact; y = RN(x * G)
+      const uint4 v0 = buf[w][s][2 * j], v1 = buf[w][s][2 * j + 1];
+      const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      float y[16];
+      uint64_t y2[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        y2[k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), GG);
+        unpack2(y2[k], y[2 * k], y[2 * k + 1]);
+      }
+      // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
+      float m = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[i]));
+      const int c0 = (int)e4m3_code(__fmul_rn(m, k6));
+      const uint4* base = tab + (c0 ? TabW : 0) + Pad + c0;
+
+      // a5 + a6: candidate search (Alg. 1 lines 5-10)
+      float best = cand_loss(y2, y, base[0]);
+      const float loss0 = best;  // err_base: the max-abs scale (f = 0)
+      uint32_t bsel = base[0].z;
+      if constexpr (NEG >= 0) {
+#pragma unroll
+        for (int f = 1; f <= NEG; f++) SS_TAKE_LE(base[-f]);
+#pragma unroll
+        for (int f = 1; f <= POS; f++) SS_TAKE_LT(base[f]);
+      } else {
+        // runtime window; skip offsets that are clamped duplicates for every lane
+        const int lo = __reduce_min_sync(0xFFFFFFFFu, (c0 ? 1 : 0) - c0);
+        const int hi = __reduce_max_sync(0xFFFFFFFFu, 126 - c0);
+        const int fneg = max(p.fmin, lo), fpos = min(p.fmax, hi);
+#pragma unroll 1
+        for (int f = -1; f >= fneg; f--) SS_TAKE_LE(base[f]);
+#pragma unroll 1
+        for (int f = 1; f <= fpos; f++) SS_TAKE_LT(base[f]);
+      }
+
+      // a7: emit the winner: nibbles of t = y * rho*, scale byte, offset, errors
+      const uint32_t code = bsel >> 16;
+      const float rs = __uint_as_float(tab[(code ? TabW : 0) + Pad + code].x);
+      const uint64_t rr = pack2(rs, rs);
+      float t[16];
+#pragma unroll
+      for (int k = 0; k < 8; k++) unpack2(fmul2(y2[k], rr), t[2 * k], t[2 * k + 1]);
+      uint2 cw;
+      cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+      cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
+      if (active) {
+        __stcs(codes + j, cw);
+        scales[j] = (uint8_t)code;
+        if (offsets) offsets[j] = (int8_t)((int)code - c0);
+        if (err) __stcs(err + j, make_float2(best, loss0));
+        sb += (double)best;
+        sc += (double)loss0;
+      }
+    }
     {  // refill stage s with task + kStages * W (always commit: uniform group count)
       const int64_t far = task + (int64_t)kStages * W;
       if (far < p.ntasks) issue(far, locate_task(p, far, tn), s);
       cp_async_commit();
     }
-    const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    // a3: y = RN(x * G)
-    float y[16];
-    uint64_t y2[8];
-    const uint64_t GG = pack2(G, G);
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      y2[k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), GG);
-      unpack2(y2[k], y[2 * k], y[2 * k + 1]);
-    }
-    // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
-    float m = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[i]));
-    const int c0 = (int)e4m3_code(__fmul_rn(m, k6));
-    const uint4* base = tab + (c0 ? TabW : 0) + Pad + c0;
-
-    // a5 + a6: candidate search (Alg. 1 lines 5-10)
-    float best = cand_loss(y2, y, base[0]);
-    const float loss0 = best;  // err_base: the max-abs scale (f = 0)
-    uint32_t bsel = base[0].z;
-    if constexpr (NEG >= 0) {
-#pragma unroll
-      for (int f = 1; f <= NEG; f++) SS_TAKE_LE(base[-f]);
-#pragma unroll
-      for (int f = 1; f <= POS; f++) SS_TAKE_LT(base[f]);
-    } else {
-      // runtime window; skip offsets that are clamped duplicates for every lane
-      const int lo = __reduce_min_sync(0xFFFFFFFFu, (c0 ? 1 : 0) - c0);
-      const int hi = __reduce_max_sync(0xFFFFFFFFu, 126 - c0);
-      const int fneg = max(p.fmin, lo), fpos = min(p.fmax, hi);
-#pragma unroll 1
-      for (int f = -1; f >= fneg; f--) SS_TAKE_LE(base[f]);
-#pragma unroll 1
-      for (int f = 1; f <= fpos; f++) SS_TAKE_LT(base[f]);
-    }
-
-    // a7: emit the winner: nibbles of t = y * rho*, scale byte, offset, errors
-    const uint32_t code = bsel >> 16;
-    const float rs = __uint_as_float(tab[(code ? TabW : 0) + Pad + code].x);
-    const uint64_t rr = pack2(rs, rs);
-    float t[16];
-#pragma unroll
-    for (int k = 0; k < 8; k++) unpack2(fmul2(y2[k], rr), t[2 * k], t[2 * k + 1]);
-    uint2 cw;
-    cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
-    cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
-    if (active) {
-      __stcs(T.codes + b, cw);
-      T.scales[b] = (uint8_t)code;
-      if (T.offsets) T.offsets[b] = (int8_t)((int)code - c0);
-      if (T.err) __stcs(T.err + b, make_float2(best, loss0));
-    }
     if (T.sums) {  // per-task partial (fixed lane tree); reduced by sums_kernel
-      const double sb = warp_sum(active ? (double)best : 0.0);
-      const double sc = warp_sum(active ? (double)loss0 : 0.0);
+      sb = warp_sum(sb);
+      sc = warp_sum(sc);
       if (lane == 0) p.part1[task] = make_double2(sb, sc);
     }
-    if (T.g_out && task == T.task0 && lane == 0) *T.g_out = G;
+    if (T.g_out && b0 == 0 && lane == 0) *T.g_out = G;
 
     if (next >= p.ntasks) break;
     task = next;

@@ -23,9 +23,9 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
+    "bpl1": ["SS_BPL=1"],
     "mb4": ["SS_MIN_BLOCKS=4"],
-    "mb6": ["SS_MIN_BLOCKS=6"],
-    "amax0": ["SS_AMAX_MODE=0"],
+    "bpl1mb4": ["SS_BPL=1", "SS_MIN_BLOCKS=4"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
 
