@@ -35,6 +35,9 @@
 #ifndef SS_BPL
 #define SS_BPL 2         // NVFP4 blocks per lane per warp task
 #endif
+#ifndef SS_ILP
+#define SS_ILP 1         // blocks whose candidate loops are interleaved per lane (divides SS_BPL)
+#endif
 #ifndef SS_AMAX_MODE
 #define SS_AMAX_MODE 1   // 0: 32 KiB chunk per CTA iteration; 1: grid-stride, 4 loads in flight
 #endif
@@ -44,6 +47,8 @@ namespace ss {
 constexpr int kWarps = 8;                     // warps per CTA
 constexpr int kThreads = 32 * kWarps;
 constexpr int kBPL = SS_BPL;                  // NVFP4 blocks per lane per task
+constexpr int kILP = SS_ILP;                  // of which interleaved in registers
+static_assert(kBPL % kILP == 0, "SS_ILP must divide SS_BPL");
 constexpr int kTaskBlocks = 32 * kBPL;        // NVFP4 blocks per warp task
 constexpr int kTaskBytes = kTaskBlocks * 32;  // bf16 input bytes per task
 constexpr int kStages = kBPL >= 4 ? 2 : 4 / kBPL;  // per-warp smem buffers (tasks in flight)
@@ -415,6 +420,25 @@ __device__ __forceinline__ float cand_loss(const uint64_t (&y2)[8], const float 
     bsel = t_ ? e_.z : bsel;                      \
   }
 
+// ILP variants: the same candidate offset f for kILP blocks (each with its own
+// c0, table base, best and selection) so their dependency chains interleave.
+#define SS_TAKE_LE_ILP(F)                                    \
+  _Pragma("unroll") for (int h = 0; h < kILP; h++) {         \
+    const uint4 e_ = base[h][F];                             \
+    const float l_ = cand_loss(y2[h], y[h], e_);             \
+    const bool t_ = l_ <= best[h];                           \
+    best[h] = t_ ? l_ : best[h];                             \
+    bsel[h] = t_ ? e_.z : bsel[h];                           \
+  }
+#define SS_TAKE_LT_ILP(F)                                    \
+  _Pragma("unroll") for (int h = 0; h < kILP; h++) {         \
+    const uint4 e_ = base[h][F];                             \
+    const float l_ = cand_loss(y2[h], y[h], e_);             \
+    const bool t_ = l_ < best[h];                            \
+    best[h] = t_ ? l_ : best[h];                             \
+    bsel[h] = t_ ? e_.z : bsel[h];                           \
+  }
+
 // NEG/POS >= 0: compile-time window [-NEG, POS]; NEG < 0: runtime [fmin, fmax].
 template <int NEG, int POS>
 __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
@@ -491,63 +515,83 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     const uint64_t GG = pack2(G, G);
 
 #pragma unroll 1
-    for (int u = 0; u < kBPL; u++) {
-      const int j = u * 32 + lane;
-      const bool active = j < nblk;
-      // a1 + a3: bf16 -> f32 is exact; y = RN(x * G)
-      const uint4 v0 = buf[w][s][2 * j], v1 = buf[w][s][2 * j + 1];
-      const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      float y[16];
-      uint64_t y2[8];
+    for (int u0 = 0; u0 < kBPL; u0 += kILP) {
+      float y[kILP][16];
+      uint64_t y2[kILP][8];
+      int c0[kILP];
+      const uint4* base[kILP];
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        y2[k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), GG);
-        unpack2(y2[k], y[2 * k], y[2 * k + 1]);
+      for (int h = 0; h < kILP; h++) {
+        const int j = (u0 + h) * 32 + lane;
+        // a1 + a3: bf16 -> f32 is exact; y = RN(x * G)
+        const uint4 v0 = buf[w][s][2 * j], v1 = buf[w][s][2 * j + 1];
+        const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          y2[h][k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), GG);
+          unpack2(y2[h][k], y[h][2 * k], y[h][2 * k + 1]);
+        }
+        // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
+        float m = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[h][i]));
+        c0[h] = (int)e4m3_code(__fmul_rn(m, k6));
+        base[h] = tab + (c0[h] ? TabW : 0) + Pad + c0[h];
       }
-      // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
-      float m = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[i]));
-      const int c0 = (int)e4m3_code(__fmul_rn(m, k6));
-      const uint4* base = tab + (c0 ? TabW : 0) + Pad + c0;
 
       // a5 + a6: candidate search (Alg. 1 lines 5-10)
-      float best = cand_loss(y2, y, base[0]);
-      const float loss0 = best;  // err_base: the max-abs scale (f = 0)
-      uint32_t bsel = base[0].z;
+      float best[kILP], loss0[kILP];
+      uint32_t bsel[kILP];
+#pragma unroll
+      for (int h = 0; h < kILP; h++) {
+        best[h] = cand_loss(y2[h], y[h], base[h][0]);
+        loss0[h] = best[h];  // err_base: the max-abs scale (f = 0)
+        bsel[h] = base[h][0].z;
+      }
       if constexpr (NEG >= 0) {
 #pragma unroll
-        for (int f = 1; f <= NEG; f++) SS_TAKE_LE(base[-f]);
+        for (int f = 1; f <= NEG; f++) SS_TAKE_LE_ILP(-f)
 #pragma unroll
-        for (int f = 1; f <= POS; f++) SS_TAKE_LT(base[f]);
+        for (int f = 1; f <= POS; f++) SS_TAKE_LT_ILP(f)
       } else {
         // runtime window; skip offsets that are clamped duplicates for every lane
-        const int lo = __reduce_min_sync(0xFFFFFFFFu, (c0 ? 1 : 0) - c0);
-        const int hi = __reduce_max_sync(0xFFFFFFFFu, 126 - c0);
+        int cmin = c0[0], cmax = c0[0];
+#pragma unroll
+        for (int h = 1; h < kILP; h++) {
+          cmin = min(cmin, c0[h]);
+          cmax = max(cmax, c0[h]);
+        }
+        const int lo = __reduce_min_sync(0xFFFFFFFFu, (cmax ? 1 : 0) - cmax);
+        const int hi = __reduce_max_sync(0xFFFFFFFFu, 126 - cmin);
         const int fneg = max(p.fmin, lo), fpos = min(p.fmax, hi);
 #pragma unroll 1
-        for (int f = -1; f >= fneg; f--) SS_TAKE_LE(base[f]);
+        for (int f = -1; f >= fneg; f--) SS_TAKE_LE_ILP(f)
 #pragma unroll 1
-        for (int f = 1; f <= fpos; f++) SS_TAKE_LT(base[f]);
+        for (int f = 1; f <= fpos; f++) SS_TAKE_LT_ILP(f)
       }
 
       // a7: emit the winner: nibbles of t = y * rho*, scale byte, offset, errors
-      const uint32_t code = bsel >> 16;
-      const float rs = __uint_as_float(tab[(code ? TabW : 0) + Pad + code].x);
-      const uint64_t rr = pack2(rs, rs);
-      float t[16];
 #pragma unroll
-      for (int k = 0; k < 8; k++) unpack2(fmul2(y2[k], rr), t[2 * k], t[2 * k + 1]);
-      uint2 cw;
-      cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
-      cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
-      if (active) {
-        __stcs(codes + j, cw);
-        scales[j] = (uint8_t)code;
-        if (offsets) offsets[j] = (int8_t)((int)code - c0);
-        if (err) __stcs(err + j, make_float2(best, loss0));
-        sb += (double)best;
-        sc += (double)loss0;
+      for (int h = 0; h < kILP; h++) {
+        const int j = (u0 + h) * 32 + lane;
+        const bool active = j < nblk;
+        const uint32_t code = bsel[h] >> 16;
+        const float rs = __uint_as_float(tab[(code ? TabW : 0) + Pad + code].x);
+        const uint64_t rr = pack2(rs, rs);
+        float t[16];
+#pragma unroll
+        for (int k = 0; k < 8; k++) unpack2(fmul2(y2[h][k], rr), t[2 * k], t[2 * k + 1]);
+        uint2 cw;
+        cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+        cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
+        if (active) {
+          __stcs(codes + j, cw);
+          scales[j] = (uint8_t)code;
+          if (offsets) offsets[j] = (int8_t)((int)code - c0[h]);
+          if (err) __stcs(err + j, make_float2(best[h], loss0[h]));
+          sb += (double)best[h];
+          sc += (double)loss0[h];
+        }
       }
     }
     {  // refill stage s with task + kStages * W (always commit: uniform group count)

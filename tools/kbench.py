@@ -23,9 +23,10 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "bpl1": ["SS_BPL=1"],
     "mb4": ["SS_MIN_BLOCKS=4"],
-    "bpl1mb4": ["SS_BPL=1", "SS_MIN_BLOCKS=4"],
+    "ilp2mb4": ["SS_ILP=2", "SS_MIN_BLOCKS=4"],
+    "ilp2mb3": ["SS_ILP=2", "SS_MIN_BLOCKS=3"],
+    "ilp2mb2": ["SS_ILP=2", "SS_MIN_BLOCKS=2"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
 

@@ -1,0 +1,136 @@
+// pipeprobe.cu — issue/pipe rates on B200 of the instructions in the
+// ScaleSearch inner loop (FMUL2, FFMA2, FHFMA, F2FP e2m1 pack/unpack) alone
+// and in mixes, to fix which pipe bounds the candidate loop.
+// 8 independent dependency chains per thread, 32 warps per SM, clock64 per
+// CTA; prints warp-instructions per SM-cycle (4.0 = one per SMSP per cycle).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipeprobe pipeprobe.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#define N 16384
+#define NCH 8
+
+__device__ __forceinline__ uint64_t p2(float a, float b) {
+  uint64_t r;
+  asm volatile("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// OP: 0 FMUL2, 1 FFMA2, 2 FHFMA, 3 pack+unpack chain (2 F2FP), 4 FFMA (3-reg),
+//     5 pair sequence (FMUL2, pack, unpack, 2 FHFMA, FFMA2), 6 FHFMA+FFMA2 (2:1),
+//     7 pack+unpack+FHFMA (chain through FHFMA)
+template <int OP>
+__global__ void __launch_bounds__(256) k(float* sink, float seed, long long* cyc) {
+  float x[NCH], y[NCH];
+  uint64_t X[NCH];
+  uint32_t h[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    x[c] = seed + threadIdx.x * 1e-3f + c;
+    y[c] = 0.5f + c * 0.01f;
+    X[c] = p2(x[c], y[c]);
+    h[c] = 0x3C003C00u + c;
+  }
+  const uint64_t R = p2(0.999f, 1.001f);
+  const uint16_t ns = 0xBC00;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < N; it++) {
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+      if (OP == 0) {
+        asm volatile("mul.rn.f32x2 %0, %0, %1;" : "+l"(X[c]) : "l"(R));
+      } else if (OP == 1) {
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(X[c]) : "l"(R));
+      } else if (OP == 2) {
+        asm volatile("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(x[c]) : "h"((uint16_t)h[c]), "h"(ns));
+      } else if (OP == 3) {
+        asm volatile("{\n.reg .b8 q;\ncvt.rn.satfinite.e2m1x2.f32 q, %1, %1;\ncvt.rn.f16x2.e2m1x2 %0, q;\n}"
+                     : "=r"(h[c]) : "f"(__uint_as_float(h[c])));
+      } else if (OP == 4) {
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(y[c]), "f"(y[(c + 1) & 7]));
+      } else if (OP == 5) {
+        uint64_t T;
+        asm volatile("mul.rn.f32x2 %0, %1, %2;" : "=l"(T) : "l"(X[c]), "l"(R));
+        float t0f, t1f;
+        asm volatile("mov.b64 {%0,%1}, %2;" : "=f"(t0f), "=f"(t1f) : "l"(T));
+        uint32_t q;
+        asm volatile("{\n.reg .b8 b;\ncvt.rn.satfinite.e2m1x2.f32 b, %2, %1;\ncvt.rn.f16x2.e2m1x2 %0, b;\n}"
+                     : "=r"(q) : "f"(t0f), "f"(t1f));
+        float d0, d1;
+        asm volatile("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d0) : "h"((uint16_t)q), "h"(ns), "f"(t0f));
+        asm volatile("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d1) : "h"((uint16_t)(q >> 16)), "h"(ns), "f"(t1f));
+        uint64_t D = p2(d0, d1);
+        asm volatile("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(X[c]) : "l"(D));
+      } else if (OP == 6) {
+        asm volatile("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(x[c]) : "h"((uint16_t)h[c]), "h"(ns));
+        asm volatile("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(y[c]) : "h"((uint16_t)h[c]), "h"(ns));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(X[c]) : "l"(R));
+      } else if (OP == 7) {
+        uint32_t q;
+        asm volatile("{\n.reg .b8 b;\ncvt.rn.satfinite.e2m1x2.f32 b, %1, %1;\ncvt.rn.f16x2.e2m1x2 %0, b;\n}"
+                     : "=r"(q) : "f"(x[c]));
+        asm volatile("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(x[c]) : "h"((uint16_t)q), "h"(ns));
+      }
+    }
+  }
+  long long t1 = clock64();
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; c++) acc += x[c] + y[c] + __uint_as_float((uint32_t)X[c]) + __uint_as_float(h[c]);
+  if (acc == 1.2345f) sink[threadIdx.x] = acc;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int OP>
+void run(const char* name, double inst_per_chain_iter, int sms, float* sink, long long* cyc) {
+  const int ctas_per_sm = 4;  // 32 warps per SM (256 threads x 4)
+  const int grid = sms * ctas_per_sm;
+  // 50 KB of dynamic shared memory caps residency at 4 CTAs (32 warps) per SM,
+  // so all `grid` CTAs run concurrently, 4 per SM
+  cudaFuncSetAttribute(k<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms = 0.f;
+  for (int rep = 0; rep < 3; rep++) {
+    cudaEventRecord(e0);
+    k<OP><<<grid, 256, 50 * 1024>>>(sink, 1.0f, cyc);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  long long* h = new long long[grid];
+  cudaMemcpy(h, cyc, 8 * grid, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < grid; i++) avg += h[i];
+  avg /= grid;
+  // warp-instructions per SM over the timed loop
+  const double inst = (double)N * NCH * inst_per_chain_iter * 8 /*warps*/ * ctas_per_sm;
+  // wall time at the 1965 MHz boost clock (includes launch + prologue, ~1%)
+  const double sm_cycles = ms * 1e-3 * 1.965e9;
+  printf("{\"case\": \"%s\", \"warp_inst_per_sm_cycle_wall\": %.3f, \"per_clock64\": %.3f, "
+         "\"ms\": %.4f, \"clock64_per_ns\": %.3f}\n",
+         name, inst / sm_cycles, inst / avg, ms, avg / (ms * 1e6));
+  fflush(stdout);
+  delete[] h;
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  float* sink;
+  long long* cyc;
+  cudaMalloc(&sink, 4096);
+  cudaMalloc(&cyc, 8 * 4096);
+  run<0>("FMUL2", 1, sms, sink, cyc);
+  run<1>("FFMA2", 1, sms, sink, cyc);
+  run<2>("FHFMA", 1, sms, sink, cyc);
+  run<3>("F2FP_pack+unpack", 2, sms, sink, cyc);
+  run<4>("FFMA", 1, sms, sink, cyc);
+  run<5>("pair_seq(FMUL2,pack,unpack,2FHFMA,FFMA2)", 6, sms, sink, cyc);
+  run<6>("2FHFMA+FFMA2", 3, sms, sink, cyc);
+  run<7>("pack+unpack+FHFMA", 3, sms, sink, cyc);
+  return 0;
+}
