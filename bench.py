@@ -238,18 +238,19 @@ class QuantEvents:
 
 def c_eff_of(torch, outs, shards, fmin, fmax, max_tensors=8):
     """Mean number of VALID candidates per block (the algorithmic work; SURVEY
-    §8(d)), counted from c0 = c* - f* of an untimed pass with offsets."""
+    §8(d)): f in [fmin, fmax] with 1 <= c0 + f <= 126, plus the zero-scale
+    candidate when c0 == 0 (R2, R3), with c0 = c* - f* from an
+    untimed pass that also emits the offsets."""
     import paper_2605_12464_b200 as ss
-    tot, cnt = 0.0, 0
+    tot, cnt = 0, 0
     for x in shards[:max_tensors]:
         if x.shape[0] == 0:
             continue
         o = ss.quantize(x, fmin=fmin, fmax=fmax, gmode="tensor", want_err=False)
         c0 = o.scales.reshape(-1).to(torch.int32) - o.offsets.to(torch.int32)
-        f = torch.arange(fmin, fmax + 1, device=x.device, dtype=torch.int32)
-        c = c0[:, None] + f[None, :]
-        valid = ((c >= 1) & (c <= 126)) | ((f[None, :] == 0) & (c0[:, None] == 0))
-        tot += valid.sum().item()
+        hi = torch.clamp(126 - c0, max=fmax)
+        lo = torch.clamp(1 - c0, min=fmin)
+        tot += int((torch.clamp(hi - lo + 1, min=0) + (c0 == 0).to(torch.int32)).sum())
         cnt += c0.numel()
         del o
     return tot / max(cnt, 1)
@@ -262,10 +263,17 @@ def run_ours(a, rank, world, local_rank):
     import paper_2605_12464_b200 as ss
     from paper_2605_12464_b200.dist import CudaOps, RowShardQuantizer, ShardPlan
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one process per GPU; SS_DIST_BACKEND=gloo lets several ranks share one
+    # device for testing the sharded path on a 1-GPU box (the product uses NCCL)
+    backend = os.environ.get("SS_DIST_BACKEND", "nccl")
+    dev_idx = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     ss.lib()
     specs = ssgen.workload(a.workload)
     plan = ShardPlan([(s.rows, s.cols) for s in specs], rank, world)
@@ -285,7 +293,7 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local_rank) if not a.no_clocks else None
+    clocks = ClockSampler(dev_idx) if not a.no_clocks else None
     if clocks:
         clocks.start()
         time.sleep(0.3)

@@ -38,6 +38,9 @@
 #ifndef SS_ILP
 #define SS_ILP 1         // blocks whose candidate loops are interleaved per lane (divides SS_BPL)
 #endif
+#ifndef SS_CILP
+#define SS_CILP 2        // candidates whose loss loops are interleaved (fixed windows)
+#endif
 #ifndef SS_AMAX_MODE
 #define SS_AMAX_MODE 1   // 0: 32 KiB chunk per CTA iteration; 1: grid-stride, 4 loads in flight
 #endif
@@ -78,6 +81,7 @@ __device__ __forceinline__ uint64_t pack2u(uint32_t lo, uint32_t hi) {
 __device__ __forceinline__ void unpack2(uint64_t v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
+#ifndef SS_SCALAR_FP32
 __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -88,6 +92,21 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
+#else  // tuning variant: the same arithmetic as scalar FMUL / FFMA pairs
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  float a0, a1, b0, b1;
+  unpack2(a, a0, a1);
+  unpack2(b, b0, b1);
+  return pack2(__fmul_rn(a0, b0), __fmul_rn(a1, b1));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  float a0, a1, b0, b1, c0, c1;
+  unpack2(a, a0, a1);
+  unpack2(b, b0, b1);
+  unpack2(c, c0, c1);
+  return pack2(__fmaf_rn(a0, b0, c0), __fmaf_rn(a1, b1, c1));
+}
+#endif
 // E2M1 nibbles of (lo, hi) -> f16x2 (q_lo, q_hi).
 __device__ __forceinline__ uint32_t e2m1_round_f16x2(float lo, float hi) {
   uint32_t h;
@@ -398,30 +417,50 @@ __device__ __forceinline__ float cand_loss(const uint64_t (&y2)[8], const float 
   return __fadd_rn(a, b);
 }
 
+// Losses of CN candidates with their pair loops interleaved (independent
+// FFMA2 accumulation chains); each loss is computed exactly as cand_loss.
+template <int CN>
+__device__ __forceinline__ void cand_loss_n(const uint64_t (&y2)[8], const float (&y)[16],
+                                            const uint4 (&e)[CN], float (&loss)[CN]) {
+  uint64_t acc[CN];
+#pragma unroll
+  for (int c = 0; c < CN; c++) acc[c] = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+#pragma unroll
+    for (int c = 0; c < CN; c++) {
+      float t0, t1;
+      unpack2(fmul2(y2[k], pack2u(e[c].x, e[c].y)), t0, t1);
+      const uint32_t q = e2m1_round_f16x2(t0, t1);
+      const uint16_t negs = (uint16_t)(e[c].z & 0xFFFFu);
+      const float d0 = fhfma((uint16_t)(q & 0xFFFFu), negs, y[2 * k]);
+      const float d1 = fhfma((uint16_t)(q >> 16), negs, y[2 * k + 1]);
+      const uint64_t d = pack2(d0, d1);
+      acc[c] = ffma2(d, d, acc[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CN; c++) {
+    float a, b;
+    unpack2(acc[c], a, b);
+    loss[c] = __fadd_rn(a, b);
+  }
+}
+
+// Scan position i of a fixed window [-NEG, POS] (R4 order, see below):
+// i = 0 -> f = 0; 1..NEG -> f = -i; NEG+1.. -> f = i - NEG.
+template <int NEG>
+__device__ __forceinline__ constexpr int scan_offset(int i) {
+  return i == 0 ? 0 : (i <= NEG ? -i : i - NEG);
+}
+
 // Candidate order (equivalent to Alg. 1's ascending strict-< scan, R4): f = 0
 // first (it is also err_base), then f = -1, -2, ... with "<=" (ties move to
 // the smaller code), then f = 1, 2, ... with strict "<" (ties keep the
 // smaller code).  Clamped duplicates carry the same code, so they never
 // change the result.
-#define SS_TAKE_LE(E)                             \
-  {                                               \
-    const uint4 e_ = (E);                         \
-    const float l_ = cand_loss(y2, y, e_);        \
-    const bool t_ = l_ <= best;                   \
-    best = t_ ? l_ : best;                        \
-    bsel = t_ ? e_.z : bsel;                      \
-  }
-#define SS_TAKE_LT(E)                             \
-  {                                               \
-    const uint4 e_ = (E);                         \
-    const float l_ = cand_loss(y2, y, e_);        \
-    const bool t_ = l_ < best;                    \
-    best = t_ ? l_ : best;                        \
-    bsel = t_ ? e_.z : bsel;                      \
-  }
-
-// ILP variants: the same candidate offset f for kILP blocks (each with its own
-// c0, table base, best and selection) so their dependency chains interleave.
+// Runtime-window updates: the same candidate offset f for the kILP blocks of
+// a lane (each with its own c0, table base, best and selection).
 #define SS_TAKE_LE_ILP(F)                                    \
   _Pragma("unroll") for (int h = 0; h < kILP; h++) {         \
     const uint4 e_ = base[h][F];                             \
@@ -542,18 +581,44 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       // a5 + a6: candidate search (Alg. 1 lines 5-10)
       float best[kILP], loss0[kILP];
       uint32_t bsel[kILP];
-#pragma unroll
-      for (int h = 0; h < kILP; h++) {
-        best[h] = cand_loss(y2[h], y[h], base[h][0]);
-        loss0[h] = best[h];  // err_base: the max-abs scale (f = 0)
-        bsel[h] = base[h][0].z;
-      }
       if constexpr (NEG >= 0) {
+        // scan positions 0 .. NEG+POS in chunks of CI interleaved candidates;
+        // the selection updates are applied in scan order afterwards
+        constexpr int NC = 1 + NEG + POS;
+        constexpr int CI = SS_CILP < NC ? SS_CILP : NC;
 #pragma unroll
-        for (int f = 1; f <= NEG; f++) SS_TAKE_LE_ILP(-f)
+        for (int h = 0; h < kILP; h++) {
 #pragma unroll
-        for (int f = 1; f <= POS; f++) SS_TAKE_LT_ILP(f)
+          for (int i0 = 0; i0 < NC; i0 += CI) {
+            uint4 e[CI];
+            float l[CI];
+#pragma unroll
+            for (int c = 0; c < CI; c++)
+              e[c] = base[h][scan_offset<NEG>(i0 + c < NC ? i0 + c : NC - 1)];
+            cand_loss_n<CI>(y2[h], y[h], e, l);
+#pragma unroll
+            for (int c = 0; c < CI; c++) {
+              const int i = i0 + c;
+              if (i >= NC) break;
+              if (i == 0) {
+                best[h] = l[c];
+                loss0[h] = l[c];  // err_base: the max-abs scale (f = 0)
+                bsel[h] = e[c].z;
+              } else {
+                const bool t_ = i <= NEG ? l[c] <= best[h] : l[c] < best[h];
+                best[h] = t_ ? l[c] : best[h];
+                bsel[h] = t_ ? e[c].z : bsel[h];
+              }
+            }
+          }
+        }
       } else {
+#pragma unroll
+        for (int h = 0; h < kILP; h++) {
+          best[h] = cand_loss(y2[h], y[h], base[h][0]);
+          loss0[h] = best[h];  // err_base: the max-abs scale (f = 0)
+          bsel[h] = base[h][0].z;
+        }
         // runtime window; skip offsets that are clamped duplicates for every lane
         int cmin = c0[0], cmax = c0[0];
 #pragma unroll

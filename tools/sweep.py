@@ -1,0 +1,174 @@
+#!/usr/bin/env python
+"""Per-config measurements on one B200 for BASELINE.json's five configs
+(SURVEY §8(d)): quantize-only and end-to-end (amax + quantize) throughput,
+ALU / HBM roofline fractions, valid-candidate count, and the MSE cut.
+
+    python tools/sweep.py [--configs c1,c2,c3,c4,c5] [--out gpurun_out/sweep.jsonl]
+
+Timing: CUDA events on the launching stream, 2 warm-ups, median of 5 runs.
+C1 (33.5 MB) is rotated over 40 copies (> L2) between runs; the others
+exceed L2.  The driver's bench line is bench.py; this is the table behind
+DESIGN.md §11.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+RADII_C3 = list(range(0, 17))
+RADII_C5 = [0, 1, 2, 3, 4, 6, 8, 12, 16, 32, 64, 126]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), float(m["sm_max_mhz"])
+    except Exception:
+        return 6650.0, 1965.0
+
+
+def med(ts):
+    ts = sorted(ts)
+    return ts[len(ts) // 2]
+
+
+def measure(torch, ss, groups, fmin, fmax, reps=5):
+    """groups: list of tensor lists (rotated between runs).  Returns timings and stats."""
+    outs = [[ss.alloc_out(x) for x in g] for g in groups]
+    amax = [torch.zeros(len(g), dtype=torch.int32, device=g[0].device) for g in groups]
+
+    def q_only(i):
+        ss.quantize_batched(groups[i], outs[i], fmin=fmin, fmax=fmax, gmode="device_amax", amax=amax[i])
+
+    def e2e(i):
+        ss.tensor_amax_batched(groups[i], out=amax[i])
+        q_only(i)
+
+    for i in range(len(groups)):
+        ss.tensor_amax_batched(groups[i], out=amax[i])
+    res = {}
+    for name, fn in (("quant", q_only), ("amax_quant", e2e)):
+        for w in range(2):
+            fn(w % len(groups))
+        ts = []
+        for r in range(reps):
+            i = r % len(groups)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn(i)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        res[name] = med(ts)
+    # statistics from group 0: valid candidates, x-domain SSE, f* histogram
+    g, o = groups[0], outs[0]
+    tot_valid, tot_blocks, s_best, s_base = 0, 0, 0.0, 0.0
+    hist = torch.zeros(253, dtype=torch.int64, device=g[0].device)
+    for x, oo in zip(g, o):
+        c0 = oo.scales.reshape(-1).to(torch.int32) - oo.offsets.to(torch.int32)
+        # valid candidates of a block: f in [fmin, fmax] with 1 <= c0 + f <= 126,
+        # plus the zero-scale candidate when c0 == 0 (R2, R3)
+        hi = torch.clamp(126 - c0, max=fmax)
+        lo = torch.clamp(1 - c0, min=fmin)
+        valid = torch.clamp(hi - lo + 1, min=0) + (c0 == 0).to(torch.int32)
+        tot_valid += int(valid.sum())
+        tot_blocks += c0.numel()
+        G2 = float(oo.G.item()) ** 2
+        s = oo.sums.cpu().tolist()
+        s_best += s[0] / G2
+        s_base += s[1] / G2
+        hist += torch.bincount(oo.offsets.to(torch.int64) + 126, minlength=253)
+        del valid, c0
+    n = sum(x.numel() for x in g)
+    h = hist.cpu().tolist()
+    return res, n, tot_valid / max(tot_blocks, 1), s_best, s_base, {str(k - 126): v for k, v in enumerate(h) if v}
+
+
+def report(cfg, fmin, fmax, res, n, ceff, s_best, s_base, hist, hbm, mhz, extra=None):
+    alu_peak = 148 * 128 * mhz * 1e6
+    tq = res["quant"] * 1e-3
+    te = res["amax_quant"] * 1e-3
+    ops = (4.0 * ceff + 2.0) * n
+    bytes_q = 3.0625 * n
+    t_roof = max(bytes_q / (hbm * 1e9), ops / alu_peak)
+    line = {"config": cfg, "window": [fmin, fmax], "elements": n, "c_eff": ceff,
+            "quant_ms": res["quant"], "amax_quant_ms": res["amax_quant"],
+            "quant_bf16_gbs": 2 * n / tq / 1e9, "e2e_bf16_gbs": 2 * n / te / 1e9,
+            "bound": "alu" if ops / alu_peak > bytes_q / (hbm * 1e9) else "hbm",
+            "roofline_frac": t_roof / tq, "alu_frac": ops / alu_peak / tq,
+            "hbm_frac": bytes_q / (hbm * 1e9) / tq,
+            "mse_cut_pct": 100.0 * (1 - s_best / s_base) if s_base > 0 else 0.0,
+            "mse_base": s_base / n, "mse_best": s_best / n}
+    if hist is not None and len(hist) <= 40:
+        line["fstar_hist"] = hist
+    if extra:
+        line.update(extra)
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    import torch
+    import ssgen
+    import paper_2605_12464_b200 as ss
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--c5-gib", default="1,8")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    hbm, mhz = peaks()
+    dev = torch.device("cuda", 0)
+    lines = []
+    seed = ssgen.workloads.BASE_SEED
+
+    def gen(specs):
+        return [ssgen.generate(s.kind, s.rows, s.cols, seed=seed, tid=s.tid, device=dev) for s in specs]
+
+    cfgs = a.configs.split(",")
+    if "c1" in cfgs:
+        x = gen(ssgen.workload("c1_gauss4096"))
+        groups = [[x[0].clone()] for _ in range(40)]
+        del x
+        for w in [(-8, 8), (0, 0), (-1, 1), (-2, 6), (-126, 126)]:
+            lines.append(report("c1_gauss4096", *w, *measure(torch, ss, groups, *w), hbm, mhz))
+        del groups
+        torch.cuda.empty_cache()
+    if "c2" in cfgs:
+        xs = gen(ssgen.workload("c2_qwen3_8b_weights"))
+        for w in [(-8, 8), (-2, 6), (0, 0)]:
+            lines.append(report("c2_qwen3_8b_weights", *w, *measure(torch, ss, [xs], *w, reps=3), hbm, mhz))
+        del xs
+        torch.cuda.empty_cache()
+    if "c3" in cfgs:
+        xs = gen(ssgen.workload("c3_act_student_t"))
+        for r in RADII_C3:
+            lines.append(report("c3_act_student_t", -r, r, *measure(torch, ss, [xs], -r, r), hbm, mhz))
+        del xs
+        torch.cuda.empty_cache()
+    if "c4" in cfgs:
+        xs = gen(ssgen.workload("c4_llama70b_kv"))
+        lines.append(report("c4_llama70b_kv", -8, 8, *measure(torch, ss, [xs], -8, 8, reps=3), hbm, mhz))
+        del xs
+        torch.cuda.empty_cache()
+    if "c5" in cfgs:
+        for gib in [int(v) for v in a.c5_gib.split(",")]:
+            xs = gen(ssgen.workload("c5_gauss_%dgib" % gib))
+            for r in RADII_C5:
+                lines.append(report("c5_gauss_%dgib" % gib, -r, r,
+                                    *measure(torch, ss, [xs], -r, r, reps=3), hbm, mhz))
+            del xs
+            torch.cuda.empty_cache()
+    if a.out:
+        with open(a.out, "w") as f:
+            for ln in lines:
+                f.write(json.dumps(ln) + "\n")
+
+
+if __name__ == "__main__":
+    main()
