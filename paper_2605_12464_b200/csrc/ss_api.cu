@@ -27,6 +27,7 @@ using ss::QuantBatch;
 struct Workspace {
   uint32_t* flags = nullptr;     // sticky status flags (1 word)
   uint32_t* tick = nullptr;      // [kMaxTensors] per-tensor tickets (zero, self re-arming)
+  uint32_t* ctr = nullptr;       // [kCounters + 1] scheduler counters (zero, self re-arming)
   uint32_t* amax = nullptr;      // SS_GLOBAL_TENSOR slots
   int64_t amax_cap = 0;
   double2* part1 = nullptr;      // per-task partial sums
@@ -92,11 +93,12 @@ ss_status get_ws(int dev, void* stream, Workspace** out) {
   Workspace& w = g_ws[std::make_pair(dev, stream)];
   if (!w.flags) {
     void* p = nullptr;
-    const size_t bytes = sizeof(uint32_t) * (1 + ss::kMaxTensors);
+    const size_t bytes = sizeof(uint32_t) * (1 + ss::kMaxTensors + ss::kCounters + 1);
     if (cudaMalloc(&p, bytes) != cudaSuccess) return SS_ERR_CUDA;
     if (cudaMemset(p, 0, bytes) != cudaSuccess) return SS_ERR_CUDA;
     w.flags = reinterpret_cast<uint32_t*>(p);
     w.tick = w.flags + 1;
+    w.ctr = w.tick + ss::kMaxTensors;
   }
   *out = &w;
   return SS_OK;
@@ -294,6 +296,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.part1 = ws->part1;
     b.part2 = ws->part2;
     b.tick = ws->tick;
+    b.ctr = ws->ctr;
     b.flags = ws->flags;
     bool sums = false;
     int64_t tk = 0, gr = 0;

@@ -56,6 +56,7 @@ constexpr int kTaskBlocks = 32 * kBPL;        // NVFP4 blocks per warp task
 constexpr int kTaskBytes = kTaskBlocks * 32;  // bf16 input bytes per task
 constexpr int kStages = kBPL >= 4 ? 2 : 4 / kBPL;  // per-warp smem buffers (tasks in flight)
 constexpr int kSegTasks = 4096;               // tasks per CTA of the error-sum kernel
+constexpr int kCounters = 256;                // task counters of the dynamic scheduler
 constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
 constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
 constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk (32 KiB)
@@ -245,6 +246,7 @@ struct QuantBatch {
   double2* part1;           // per task {sum best, sum base}   (when any sums wanted)
   double2* part2;           // per segment
   uint32_t* tick;           // per tensor, zero and self re-arming
+  uint32_t* ctr;            // [kCounters + 1] task counters + done count, zero and self re-arming
   uint32_t* flags;
   QTensor t[kMaxTensors];
 };
@@ -490,9 +492,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   __syncthreads();
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t W = (int64_t)gridDim.x * kWarps;
-  int64_t task = (int64_t)blockIdx.x * kWarps + w;
-  if (task >= p.ntasks) return;  // no CTA barrier follows
+  const int gw = blockIdx.x * kWarps + w;
 
   const float k6 = __uint_as_float(kOneSixthBits);
   // Stage s of this warp holds one task.  Lane l copies its own blocks
@@ -517,30 +517,45 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     if (p.gmode == 0) return 1.0f;
     return global_scale(__ldg(p.t[ti].amax), p.flags, report);
   };
+  // Dynamic scheduling: counter c hands out tasks c, c + kCounters, ... ; warp
+  // gw draws from counter gw % kCounters, so warps the arbiter favours simply
+  // take more tasks and every warp finishes at about the same time.  Each
+  // warp's tasks increase, so the tensor lookup only moves forward.
+  const int cidx = gw % kCounters;
+  bool exhausted = false;
+  auto grab = [&]() -> int64_t {
+    if (exhausted) return -1;
+    uint32_t idx = 0;
+    if (lane == 0) idx = atomicAdd(p.ctr + cidx, 1u);
+    idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
+    const int64_t t = cidx + (int64_t)idx * kCounters;
+    if (t >= p.ntasks) {
+      exhausted = true;
+      return -1;
+    }
+    return t;
+  };
 
-  // prologue: tasks task, task+W, ..., task+(kStages-1)W in flight
-  int ti = locate_task(p, task, 0);
-  {
-    int tj = ti;
-    for (int k = 0; k < kStages; k++) {
-      const int64_t tk = task + k * W;
-      if (tk < p.ntasks) {
-        tj = locate_task(p, tk, tj);
-        issue(tk, tj, k);
-      }
-      cp_async_commit();
+  // prologue: kStages tasks in flight
+  int64_t q_task[kStages];
+  int q_ti[kStages];
+  int tj = 0;
+#pragma unroll
+  for (int k = 0; k < kStages; k++) {
+    const int64_t t = grab();
+    if (t >= 0) {
+      tj = locate_task(p, t, tj);
+      issue(t, tj, k);
     }
+    q_task[k] = t;
+    q_ti[k] = tj;
+    cp_async_commit();
   }
-  float G = gscale(ti, task == p.t[ti].task0 && lane == 0);
   int s = 0;
-  for (;;) {
-    const int64_t next = task + W;
-    int tn = ti;
-    float Gn = G;
-    if (next < p.ntasks) {
-      tn = locate_task(p, next, ti);
-      Gn = gscale(tn, next == p.t[tn].task0 && lane == 0);
-    }
+  while (q_task[0] >= 0) {
+    const int64_t task = q_task[0];
+    const int ti = q_ti[0];
+    const float G = gscale(ti, task == p.t[ti].task0 && lane == 0);
     const QTensor& T = p.t[ti];
     const int64_t b0 = (task - T.task0) * kTaskBlocks;   // first block of the task
     const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
@@ -659,10 +674,20 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         }
       }
     }
-    {  // refill stage s with task + kStages * W (always commit: uniform group count)
-      const int64_t far = task + (int64_t)kStages * W;
-      if (far < p.ntasks) issue(far, locate_task(p, far, tn), s);
+    {  // refill stage s with the next task drawn (always commit: uniform group count)
+      const int64_t t = grab();
+      if (t >= 0) {
+        tj = locate_task(p, t, tj);
+        issue(t, tj, s);
+      }
       cp_async_commit();
+#pragma unroll
+      for (int k = 0; k + 1 < kStages; k++) {
+        q_task[k] = q_task[k + 1];
+        q_ti[k] = q_ti[k + 1];
+      }
+      q_task[kStages - 1] = t;
+      q_ti[kStages - 1] = tj;
     }
     if (T.sums) {  // per-task partial (fixed lane tree); reduced by sums_kernel
       sb = warp_sum(sb);
@@ -671,11 +696,15 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     }
     if (T.g_out && b0 == 0 && lane == 0) *T.g_out = G;
 
-    if (next >= p.ntasks) break;
-    task = next;
-    ti = tn;
-    G = Gn;
     s = s + 1 == kStages ? 0 : s + 1;
+  }
+  // the last warp of the grid to finish re-arms the counters for the next launch
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(p.ctr + kCounters, 1u) == gridDim.x * kWarps - 1) {
+      for (int c = 0; c < kCounters; c++) p.ctr[c] = 0u;
+      p.ctr[kCounters] = 0u;
+    }
   }
 }
 

@@ -53,7 +53,8 @@ class CudaOps:
         self.B.quantize_batched([xs[k] for k in live], [outs[k] for k in live], fmin=self.fmin,
                                 fmax=self.fmax, gmode="device_amax",
                                 amax=buf if len(live) == len(xs) else buf[live].contiguous())
-        return (len(live) + 127) // 128
+        launches = (len(live) + 127) // 128
+        return launches * (2 if self.want_sums else 1)  # quant_kernel (+ sums_kernel)
 
 
 @dataclass

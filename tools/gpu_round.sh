@@ -19,8 +19,15 @@ if has bench; then
   timeout 900 python bench.py --steps 5 --warmup 3 --out gpurun_out/bench_$TAG.json > gpurun_out/bench_$TAG.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_$TAG.log
 fi
 if has ncu; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"quant_kernel|amax_kernel" -c 40 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --profile --steps 2 --warmup 1 > gpurun_out/ncu_launch_$TAG.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"quant_kernel|amax_kernel|sums_kernel" -c 40 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --profile --steps 2 --warmup 1 > gpurun_out/ncu_launch_$TAG.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:quant_kernel -s 3 -c 1 -o gpurun_out/quant_full_$TAG python tools/kbench.py one --variants base --layers 2 --reps 1 --windows=-8:8 > gpurun_out/ncu_full_$TAG.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:amax_kernel -s 3 -c 1 -o gpurun_out/amax_full_$TAG python tools/kbench.py one --variants base --layers 2 --reps 1 --windows=-8:8 > gpurun_out/ncu_amax_$TAG.log 2>&1
+fi
+if has sweep; then
+  timeout 1500 python tools/sweep.py --out gpurun_out/sweep_$TAG.jsonl > gpurun_out/sweep_$TAG.log 2>&1; echo "sweep exit $?" >> gpurun_out/sweep_$TAG.log
+fi
+if has mrank; then
+  # the sharded bench path with 2 ranks sharing the one GPU (gloo carries the amax all-reduce)
+  SS_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 1 --workload c1_gauss4096 --no-cpu-baseline --out gpurun_out/bench_mrank_$TAG.json > gpurun_out/bench_mrank_$TAG.log 2>&1; echo "mrank exit $?" >> gpurun_out/bench_mrank_$TAG.log
 fi
 echo done

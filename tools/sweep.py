@@ -5,7 +5,8 @@ ALU / HBM roofline fractions, valid-candidate count, and the MSE cut.
 
     python tools/sweep.py [--configs c1,c2,c3,c4,c5] [--out gpurun_out/sweep.jsonl]
 
-Timing: CUDA events on the launching stream, 2 warm-ups, median of 5 runs.
+Timing: CUDA events on the launching stream around `reps` back-to-back calls
+(2 warm-ups first).
 C1 (33.5 MB) is rotated over 40 copies (> L2) between runs; the others
 exceed L2.  The driver's bench line is bench.py; this is the table behind
 DESIGN.md §11.
@@ -56,16 +57,17 @@ def measure(torch, ss, groups, fmin, fmax, reps=5):
     for name, fn in (("quant", q_only), ("amax_quant", e2e)):
         for w in range(2):
             fn(w % len(groups))
-        ts = []
+        torch.cuda.synchronize()
+        # `reps` calls back to back between one event pair (rotating the input
+        # groups): the host enqueues ahead of the device, so host overhead per
+        # call is hidden whenever a call's device time exceeds it
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
         for r in range(reps):
-            i = r % len(groups)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            fn(i)
-            b.record()
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        res[name] = med(ts)
+            fn(r % len(groups))
+        b.record()
+        torch.cuda.synchronize()
+        res[name] = a.elapsed_time(b) / reps
     # statistics from group 0: valid candidates, x-domain SSE, f* histogram
     g, o = groups[0], outs[0]
     tot_valid, tot_blocks, s_best, s_base = 0, 0, 0.0, 0.0
@@ -133,10 +135,10 @@ def main():
     cfgs = a.configs.split(",")
     if "c1" in cfgs:
         x = gen(ssgen.workload("c1_gauss4096"))
-        groups = [[x[0].clone()] for _ in range(40)]
+        groups = [[x[0].clone()] for _ in range(40)]   # 1.34 GB rotated > L2
         del x
         for w in [(-8, 8), (0, 0), (-1, 1), (-2, 6), (-126, 126)]:
-            lines.append(report("c1_gauss4096", *w, *measure(torch, ss, groups, *w), hbm, mhz))
+            lines.append(report("c1_gauss4096", *w, *measure(torch, ss, groups, *w, reps=80), hbm, mhz))
         del groups
         torch.cuda.empty_cache()
     if "c2" in cfgs:
