@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -303,6 +304,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     for (; i < count && b.n < ss::kMaxTensors; i++) {
       const ss_tensor_io& t = io[i];
       const int64_t nb = t.rows * t.cols / 16;
+      // the kernel indexes tasks with 32 bits: close the batch before overflow
+      if (b.n > 0 && tk + tasks_of(nb) > (int64_t)INT32_MAX - ss::kCounters) break;
       if (nb == 0) {
         if (t.d_err_sums && cudaMemsetAsync(t.d_err_sums, 0, 16, cs) != cudaSuccess) return SS_ERR_CUDA;
         continue;

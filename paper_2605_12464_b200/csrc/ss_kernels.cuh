@@ -499,11 +499,12 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   // l, l+32, ... (2 x 16-B LDGSTS each) and later reads back only what it
   // copied, so no cross-lane sync is needed; one commit group per stage
   // (empty groups past the end keep the group count uniform).
-  auto issue = [&](int64_t tk, int ti, int s) {
+  // Task indices are 32-bit: a batch holds < 2^31 tasks (2^41 elements).
+  auto issue = [&](int tk, int ti, int s) {
     const QTensor& T = p.t[ti];
-    const int64_t b0 = (tk - T.task0) * kTaskBlocks;
+    const int b0 = (tk - (int)T.task0) * kTaskBlocks;
     const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
-    const uint8_t* src = T.in + b0 * 32;
+    const uint8_t* src = T.in + (int64_t)b0 * 32;
 #pragma unroll
     for (int u = 0; u < kBPL; u++) {
       const int j = u * 32 + lane;
@@ -523,13 +524,14 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   // warp's tasks increase, so the tensor lookup only moves forward.
   const int cidx = gw % kCounters;
   bool exhausted = false;
-  auto grab = [&]() -> int64_t {
+  const int ntasks = (int)p.ntasks;
+  auto grab = [&]() -> int {
     if (exhausted) return -1;
     uint32_t idx = 0;
     if (lane == 0) idx = atomicAdd(p.ctr + cidx, 1u);
     idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
     const int64_t t = cidx + (int64_t)idx * kCounters;
-    if (t >= p.ntasks) {
+    if (t >= ntasks) {
       exhausted = true;
       return -1;
     }
@@ -537,12 +539,12 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   };
 
   // prologue: kStages tasks in flight
-  int64_t q_task[kStages];
+  int q_task[kStages];
   int q_ti[kStages];
   int tj = 0;
 #pragma unroll
   for (int k = 0; k < kStages; k++) {
-    const int64_t t = grab();
+    const int t = grab();
     if (t >= 0) {
       tj = locate_task(p, t, tj);
       issue(t, tj, k);
@@ -552,12 +554,18 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     cp_async_commit();
   }
   int s = 0;
+  // global scale of the current task's tensor, recomputed when the tensor changes
+  int cur_ti = -1;
+  float G = 1.0f;
   while (q_task[0] >= 0) {
-    const int64_t task = q_task[0];
+    const int task = q_task[0];
     const int ti = q_ti[0];
-    const float G = gscale(ti, task == p.t[ti].task0 && lane == 0);
     const QTensor& T = p.t[ti];
-    const int64_t b0 = (task - T.task0) * kTaskBlocks;   // first block of the task
+    if (ti != cur_ti) {  // warp-uniform
+      cur_ti = ti;
+      G = gscale(ti, task == (int)T.task0 && lane == 0);
+    }
+    const int b0 = (task - (int)T.task0) * kTaskBlocks;   // first block of the task
     const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
 
     cp_async_wait<kStages - 1>();  // this lane's copies of stage s have landed
@@ -675,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       }
     }
     {  // refill stage s with the next task drawn (always commit: uniform group count)
-      const int64_t t = grab();
+      const int t = grab();
       if (t >= 0) {
         tj = locate_task(p, t, tj);
         issue(t, tj, s);

@@ -23,8 +23,7 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "scalar": ["SS_SCALAR_FP32=1"],
-    "scalarmb4": ["SS_SCALAR_FP32=1", "SS_MIN_BLOCKS=4"],
+    "mb4": ["SS_MIN_BLOCKS=4"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
 
