@@ -169,10 +169,10 @@ class QuantResult:
     err: np.ndarray      # [rows*cols/16][2] f32
     sums: np.ndarray     # [2] f64
     n_eval: int
-    G: float
+    G: float             # [rows] np.float32 array in mode "row"
 
 
-GMODES = {"none": 0, "tensor": 1, "given": 2}
+GMODES = {"none": 0, "tensor": 1, "given": 2, "row": 3}
 
 
 def quantize(x, rows: int, cols: int, fmin: int, fmax: int, gmode="tensor",
@@ -187,17 +187,25 @@ def quantize(x, rows: int, cols: int, fmin: int, fmax: int, gmode="tensor",
     err = np.empty((nb, 2), np.float32)
     sums = np.zeros(2, np.float64)
     neval = np.zeros(1, np.int64)
-    G = np.zeros(1, np.float32)
+    G = np.zeros(rows if gm == 3 else 1, np.float32)
     ab = None if amax_bits is None else np.array([amax_bits], np.uint32)
     _check(lib().so_quantize(_ptr(x), rows, cols, int(fmin), int(fmax), gm, _ptr(ab),
                              _ptr(codes), _ptr(scales), _ptr(offs), _ptr(err), _ptr(sums),
                              _ptr(neval), _ptr(G), int(threads)))
-    return QuantResult(codes, scales, offs, err, sums, int(neval[0]), float(G[0]))
+    return QuantResult(codes, scales, offs, err, sums, int(neval[0]),
+                       G.copy() if gm == 3 else float(G[0]))
 
 
-def dequantize(codes, scales, rows: int, cols: int, G: float = 1.0) -> np.ndarray:
-    codes = np.ascontiguousarray(codes, np.uint8)
-    scales = np.ascontiguousarray(scales, np.uint8)
+def dequantize(codes, scales, rows: int, cols: int, G=1.0) -> np.ndarray:
+    """bf16 bit patterns of xhat; G is a scalar or a per-row array (mode "row")."""
+    codes = np.ascontiguousarray(codes, np.uint8).reshape(rows, cols // 2)
+    scales = np.ascontiguousarray(scales, np.uint8).reshape(rows, cols // 16)
     out = np.empty((rows, cols), np.uint16)
-    _check(lib().so_dequantize(_ptr(codes), _ptr(scales), rows, cols, ctypes.c_float(G), _ptr(out)))
+    if np.ndim(G) == 0:
+        _check(lib().so_dequantize(_ptr(codes), _ptr(scales), rows, cols, ctypes.c_float(G), _ptr(out)))
+        return out
+    for r in range(rows):
+        c, sc, o = codes[r].copy(), scales[r].copy(), np.empty(cols, np.uint16)
+        _check(lib().so_dequantize(_ptr(c), _ptr(sc), 1, cols, ctypes.c_float(float(G[r])), _ptr(o)))
+        out[r] = o
     return out

@@ -228,28 +228,59 @@ int so_quantize(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int fma
                 uint8_t* scales, int8_t* offsets, float* err, double* sums,
                 int64_t* n_eval, float* G_out, int threads) {
   if (rows < 0 || cols < 0 || cols % 16 != 0 || fmin > 0 || fmax < 0) return 1;
-  if (gmode < 0 || gmode > 2 || (gmode == 2 && !amax_bits_in)) return 1;
+  if (gmode < 0 || gmode > 3 || (gmode == 2 && !amax_bits_in)) return 1;
   if (fmin < -126) fmin = -126;
   if (fmax > 126) fmax = 126;
-  uint32_t amax_bits = 0;
-  if (gmode == 1) {
-    int st = so_tensor_amax(x, rows * cols, &amax_bits);
-    if (st) return st;
-  } else if (gmode == 2) {
-    amax_bits = *amax_bits_in;
-  }
-  float G;
-  int st = so_global_scale(gmode, amax_bits, &G);
-  if (st) return st;
-  if (G_out) *G_out = G;
-
   const int64_t nbr = cols / 16, nb = rows * nbr;
+  /* Gr[r] = the global scale of row r.  Modes 0-2: one G for the tensor.
+   * Mode 3 (ROW, "after per-row scaling"): every row is
+   * its own tensor in the sense of mode 1, G_r = RN(2688 / max_k |x_rk|). */
+  float* Gr = (float*)malloc(sizeof(float) * (rows > 0 ? rows : 1));
   float* e = (float*)malloc(sizeof(float) * 2 * (nb > 0 ? nb : 1));
   int32_t* ne = (int32_t*)malloc(sizeof(int32_t) * (nb > 0 ? nb : 1));
-  if (!e || !ne) {
+  if (!Gr || !e || !ne) {
+    free(Gr);
     free(e);
     free(ne);
     return 1;
+  }
+  if (gmode == 3) {
+    for (int64_t r = 0; r < rows; r++) {
+      uint32_t ab = 0;
+      int st = so_tensor_amax(x + r * cols, cols, &ab);
+      if (!st) st = so_global_scale(1, ab, &Gr[r]);
+      if (st) {
+        free(Gr);
+        free(e);
+        free(ne);
+        return st;
+      }
+    }
+    if (G_out)
+      for (int64_t r = 0; r < rows; r++) G_out[r] = Gr[r];
+  } else {
+    uint32_t amax_bits = 0;
+    if (gmode == 1) {
+      int st = so_tensor_amax(x, rows * cols, &amax_bits);
+      if (st) {
+        free(Gr);
+        free(e);
+        free(ne);
+        return st;
+      }
+    } else if (gmode == 2) {
+      amax_bits = *amax_bits_in;
+    }
+    float G;
+    int st = so_global_scale(gmode, amax_bits, &G);
+    if (st) {
+      free(Gr);
+      free(e);
+      free(ne);
+      return st;
+    }
+    if (G_out) *G_out = G;
+    for (int64_t r = 0; r < rows; r++) Gr[r] = G;
   }
 #ifdef _OPENMP
   if (threads <= 0) threads = omp_get_num_procs();
@@ -261,7 +292,7 @@ int so_quantize(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int fma
       float y[16];
       for (int i = 0; i < 16; i++) /* y = x * G (mode NONE: y = x exactly) */
         y[i] = (gmode == 0) ? bf16_to_float(x[r * cols + bj * 16 + i])
-                            : bf16_to_float(x[r * cols + bj * 16 + i]) * G;
+                            : bf16_to_float(x[r * cols + bj * 16 + i]) * Gr[r];
       so_block_result res;
       so_search_block(y, fmin, fmax, &res);
       for (int j = 0; j < 8; j++)
@@ -287,6 +318,7 @@ int so_quantize(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int fma
     sums[1] = s0;
   }
   if (n_eval) *n_eval = total;
+  free(Gr);
   free(e);
   free(ne);
   return 0;

@@ -52,14 +52,16 @@ int so_global_scale(int gmode, uint32_t amax_bits, float* G);
 
 /* Whole-tensor quantization: x is [rows][cols] bf16 row-major, cols % 16 == 0.
  * gmode: 0 NONE, 1 TENSOR (amax of this tensor), 2 GIVEN (use *amax_bits_in,
- * e.g. the max over all row shards).  Outputs (nullable except codes/scales):
+ * e.g. the max over all row shards), 3 ROW (each row is its own tensor of
+ * mode 1: G_r from the row amax; G_out then has `rows` entries).
+ * Outputs (nullable except codes/scales):
  *   codes   [rows][cols/2]  u8, low nibble = even element (R15)
  *   scales  [rows][cols/16] u8 E4M3 code
  *   offsets [rows*cols/16]  i8 f* = c* - c0
  *   err     [rows*cols/16][2] f32 {err_best, err_base} (y-domain SSE)
  *   sums    [2] f64 {sum err_best, sum err_base} in block order
  *   n_eval  [1] i64 total candidates evaluated
- *   G_out   [1] f32 global scale used
+ *   G_out   [1] f32 global scale used ([rows] in mode 3)
  * threads <= 0 means "all cores".  Blocks are independent; threads only split
  * rows and never change any arithmetic or summation order. */
 int so_quantize(const uint16_t* x_bf16, int64_t rows, int64_t cols, int fmin,
