@@ -73,9 +73,25 @@ typedef enum {
 enum {
   SS_GLOBAL_NONE = 0,        /* G = 1: y = x (the paper's §4.1 synthetic setting)      */
   SS_GLOBAL_TENSOR = 1,      /* G from the amax of THIS tensor (one extra HBM read pass)      */
-  SS_GLOBAL_DEVICE_AMAX = 2  /* G from *d_amax_bits supplied by the caller, e.g. the NCCL max  */
+  SS_GLOBAL_DEVICE_AMAX = 2, /* G from *d_amax_bits supplied by the caller, e.g. the NCCL max  */
                              /* over all row shards of a tensor                */
+  SS_GLOBAL_ROW = 3          /* per-row G_r = RN(2688 / max|x_r|) ("after per-row scaling",  */
+                             /* P:313): d_global_scale is REQUIRED and        */
+                             /* receives [rows] f32; each row is its own tensor of mode 1    */
 };
+
+/* Scale-factor layouts (R15, R15b). */
+enum {
+  SS_SCALE_LINEAR = 0,       /* [rows][cols/16] u8 row-major                                   */
+  SS_SCALE_SWIZZLED = 1      /* the block-scaled tensor-core layout (cuBLAS/CUTLASS sm_100     */
+                             /* "128x4" scale-factor atom): 512-B tiles of 128 rows x 4 scale  */
+                             /* columns, tiles row-band-major, inside a tile byte             */
+                             /* (r%32)*16 + ((r/32)%4)*4 + j%4; rows padded to 128 and scale  */
+                             /* columns to 4 with zero bytes.  Size: ss_scale_bytes()         */
+};
+
+/* Bytes of the scale buffer of a [rows][cols] tensor in `scale_layout`. */
+SS_API int64_t ss_scale_bytes(int64_t rows, int64_t cols, int scale_layout);
 
 /* Human-readable name of a status code (static string). */
 SS_API const char* ss_status_string(int status);
@@ -141,8 +157,10 @@ typedef struct {
   double* d_err_sums;           /* nullable: device f64[2] = {sum err_best, sum err_base},  */
                                 /* overwritten; fixed-order two-level reduction of per-32-  */
                                 /* block partials: deterministic for any grid               */
-  float* d_global_scale;        /* nullable: device f32 receives G (for dequantization)     */
+  float* d_global_scale;        /* nullable: device f32 receives G (for dequantization);    */
+                                /* SS_GLOBAL_ROW: required, [rows] f32                     */
   void* stream;
+  int scale_layout;             /* SS_SCALE_* (0 = linear)                                  */
 } ss_quant_args;
 
 SS_API ss_status ss_quantize_nvfp4_ex(const ss_quant_args* args);
@@ -157,7 +175,9 @@ typedef struct {
   float* out_err;               /* nullable: [nb][2] f32 {err_best, err_base}, 8-B aligned  */
   int8_t* out_offset;           /* nullable: [nb] f* = c* - c0                               */
   double* d_err_sums;           /* nullable: device f64[2] of THIS tensor, overwritten      */
-  float* d_global_scale;        /* nullable: device f32 receives this tensor's G            */
+  float* d_global_scale;        /* nullable: device f32 receives this tensor's G;           */
+                                /* SS_GLOBAL_ROW: required, [rows] f32                     */
+  int scale_layout;             /* SS_SCALE_* (0 = linear)                                  */
 } ss_tensor_io;
 
 /*
@@ -214,6 +234,20 @@ typedef struct {
  */
 SS_API ss_status ss_quantize_nvfp4_host_batched(const ss_host_tensor_io* tensors, int count,
                                          int f_min, int f_max, int global_scale_mode);
+
+/* Dequantization with per-row global scales and / or the swizzled layout. */
+typedef struct {
+  const uint8_t* codes;         /* [rows][cols/2] u8, 8-B aligned                           */
+  const uint8_t* scales;        /* layout per scale_layout                                  */
+  int64_t rows, cols;
+  const float* d_global_scale;  /* nullable (G = 1); [1] or, with g_per_row, [rows]         */
+  int g_per_row;
+  int scale_layout;             /* SS_SCALE_*                                               */
+  void* out_bf16;               /* [rows][cols] bf16, 16-B aligned                          */
+  void* stream;
+} ss_dequant_args;
+
+SS_API ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* args);
 
 /* Synchronizes `stream`, returns and clears the sticky device flags of this
  * (device, stream) workspace: bit 0 = non-finite input seen (SS_ERR_NONFINITE),

@@ -9,6 +9,7 @@ from ._binding import (  # noqa: F401
     FLAG_NONFINITE,
     FLAG_RANGE,
     GMODES,
+    SCALE_LAYOUTS,
     LIB_PATH,
     QuantOut,
     SSError,
@@ -21,6 +22,7 @@ from ._binding import (  # noqa: F401
     quantize_host,
     quantize_host_batched,
     quantize_simple,
+    scale_bytes,
     status_string,
     tensor_amax,
     tensor_amax_batched,
@@ -28,5 +30,5 @@ from ._binding import (  # noqa: F401
 
 __all__ = [
     "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host", "quantize_host_batched",
-    "device_status", "status_string", "SSError", "QuantOut", "GMODES",
+    "device_status", "scale_bytes", "SCALE_LAYOUTS", "status_string", "SSError", "QuantOut", "GMODES",
 ]

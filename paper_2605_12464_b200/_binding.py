@@ -19,7 +19,8 @@ LIB_PATH = os.path.join(PKG, "libss%s.so" % (("_" + os.environ["SS_LIB_VARIANT"]
 
 SS_OK, SS_ERR_INVALID_ARG, SS_ERR_ALIGNMENT, SS_ERR_CUDA = 0, 1, 2, 3
 SS_ERR_NONFINITE, SS_ERR_RANGE, SS_ERR_UNSUPPORTED_DEVICE = 4, 5, 6
-GMODES = {"none": 0, "tensor": 1, "device_amax": 2}
+GMODES = {"none": 0, "tensor": 1, "device_amax": 2, "row": 3}
+SCALE_LAYOUTS = {"linear": 0, "swizzled": 1}
 FLAG_NONFINITE, FLAG_RANGE = 1, 2
 
 _lock = threading.Lock()
@@ -45,6 +46,7 @@ class TensorIO(ctypes.Structure):
         ("out_offset", ctypes.c_void_p),
         ("d_err_sums", ctypes.c_void_p),
         ("d_global_scale", ctypes.c_void_p),
+        ("scale_layout", ctypes.c_int),
     ]
 
 
@@ -75,6 +77,21 @@ class QuantArgs(ctypes.Structure):
         ("d_err_sums", ctypes.c_void_p),
         ("d_global_scale", ctypes.c_void_p),
         ("stream", ctypes.c_void_p),
+        ("scale_layout", ctypes.c_int),
+    ]
+
+
+class DequantArgs(ctypes.Structure):
+    _fields_ = [
+        ("codes", ctypes.c_void_p),
+        ("scales", ctypes.c_void_p),
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("d_global_scale", ctypes.c_void_p),
+        ("g_per_row", ctypes.c_int),
+        ("scale_layout", ctypes.c_int),
+        ("out_bf16", ctypes.c_void_p),
+        ("stream", ctypes.c_void_p),
     ]
 
 
@@ -102,6 +119,10 @@ def lib():
             L.ss_quantize_nvfp4_batched.argtypes = [ctypes.POINTER(TensorIO), I, I, I, I, P]
             L.ss_quantize_nvfp4_ex.restype = I
             L.ss_quantize_nvfp4_ex.argtypes = [ctypes.POINTER(QuantArgs)]
+            L.ss_dequantize_nvfp4_ex.restype = I
+            L.ss_dequantize_nvfp4_ex.argtypes = [ctypes.POINTER(DequantArgs)]
+            L.ss_scale_bytes.restype = i64
+            L.ss_scale_bytes.argtypes = [i64, i64, I]
             L.ss_dequantize_nvfp4.restype = I
             L.ss_dequantize_nvfp4.argtypes = [P, P, i64, i64, P, P, P]
             L.ss_quantize_nvfp4_host.restype = I
@@ -167,7 +188,8 @@ def tensor_amax(x, out=None, accumulate: bool = False, stream=None):
 
 def quantize(x, radius=None, fmin=None, fmax=None, gmode: str = "tensor", amax=None,
              want_err: bool = True, want_offsets: bool = True, want_sums: bool = True,
-             want_g: bool = True, out: Optional[QuantOut] = None, stream=None) -> QuantOut:
+             want_g: bool = True, out: Optional[QuantOut] = None, scale_layout: str = "linear",
+             stream=None) -> QuantOut:
     """ScaleSearch NVFP4 quantization of a [rows][cols] bf16 CUDA tensor (ss_quantize_nvfp4_ex)."""
     import torch
     assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous() and x.dim() == 2
@@ -177,9 +199,10 @@ def quantize(x, radius=None, fmin=None, fmax=None, gmode: str = "tensor", amax=N
     if gm == 2 and amax is None:
         raise ValueError("gmode='device_amax' needs amax (device int32/uint32 tensor)")
     if out is None:
-        out = alloc_out(x, want_err, want_offsets, want_sums, want_g)
+        out = alloc_out(x, want_err, want_offsets, want_sums, want_g, scale_layout, gmode)
     a = QuantArgs(_ptr(x), rows, cols, lo, hi, gm, _ptr(amax), _ptr(out.codes), _ptr(out.scales),
-                  _ptr(out.err), _ptr(out.offsets), _ptr(out.sums), _ptr(out.G), _stream_ptr(stream))
+                  _ptr(out.err), _ptr(out.offsets), _ptr(out.sums), _ptr(out.G), _stream_ptr(stream),
+                  SCALE_LAYOUTS[scale_layout])
     _check(lib().ss_quantize_nvfp4_ex(ctypes.byref(a)), "ss_quantize_nvfp4_ex")
     return out
 
@@ -199,23 +222,34 @@ def tensor_amax_batched(xs, out=None, accumulate: bool = False, stream=None):
     return out
 
 
-def alloc_out(x, want_err=True, want_offsets=True, want_sums=True, want_g=True) -> QuantOut:
+def scale_bytes(rows: int, cols: int, scale_layout: str = "linear") -> int:
+    return int(lib().ss_scale_bytes(rows, cols, SCALE_LAYOUTS[scale_layout]))
+
+
+def alloc_out(x, want_err=True, want_offsets=True, want_sums=True, want_g=True,
+              scale_layout: str = "linear", gmode: str = "tensor") -> QuantOut:
+    """Output buffers for ``x``: scales are [rows][cols/16] (linear) or the flat
+    swizzled tile buffer (ss_scale_bytes); G is [1], or [rows] for gmode 'row'."""
     import torch
     rows, cols = x.shape
     nb = rows * cols // 16
     dev = x.device
+    scales = (torch.empty(rows, cols // 16, dtype=torch.uint8, device=dev)
+              if scale_layout == "linear" else
+              torch.empty(scale_bytes(rows, cols, scale_layout), dtype=torch.uint8, device=dev))
     return QuantOut(
         torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev),
-        torch.empty(rows, cols // 16, dtype=torch.uint8, device=dev),
+        scales,
         torch.empty(nb, 2, dtype=torch.float32, device=dev) if want_err else None,
         torch.empty(nb, dtype=torch.int8, device=dev) if want_offsets else None,
         torch.empty(2, dtype=torch.float64, device=dev) if want_sums else None,
-        torch.empty(1, dtype=torch.float32, device=dev) if want_g else None,
+        torch.empty(rows if gmode == "row" else 1, dtype=torch.float32, device=dev)
+        if (want_g or gmode == "row") else None,
     )
 
 
 def quantize_batched(xs, outs, radius=None, fmin=None, fmax=None, gmode: str = "tensor",
-                     amax=None, stream=None):
+                     amax=None, scale_layout: str = "linear", stream=None):
     """All tensors of ``xs`` into ``outs`` (QuantOut each) in one call
     (ss_quantize_nvfp4_batched).  ``amax``: device int32 [len(xs)] for
     gmode='device_amax' (e.g. after the NCCL max all-reduce)."""
@@ -232,7 +266,7 @@ def quantize_batched(xs, outs, radius=None, fmin=None, fmax=None, gmode: str = "
         rows, cols = x.shape
         arr[i] = TensorIO(_ptr(x), rows, cols, amax.data_ptr() + 4 * i if gm == 2 else None,
                           _ptr(o.codes), _ptr(o.scales), _ptr(o.err), _ptr(o.offsets), _ptr(o.sums),
-                          _ptr(o.G))
+                          _ptr(o.G), SCALE_LAYOUTS[scale_layout])
     _check(lib().ss_quantize_nvfp4_batched(arr, n, lo, hi, gm, _stream_ptr(stream)),
            "ss_quantize_nvfp4_batched")
     return outs
@@ -245,13 +279,17 @@ def quantize_simple(x, radius: int, gmode: str, codes, scales, err=None, stream=
                                    _ptr(scales), _ptr(err), _stream_ptr(stream)), "ss_quantize_nvfp4")
 
 
-def dequantize(codes, scales, rows: int, cols: int, G=None, out=None, stream=None):
-    """bf16 [rows][cols] reconstruction (ss_dequantize_nvfp4); G is a device f32[1] or None."""
+def dequantize(codes, scales, rows: int, cols: int, G=None, out=None, stream=None,
+               scale_layout: str = "linear"):
+    """bf16 [rows][cols] reconstruction (ss_dequantize_nvfp4_ex); G is a device
+    f32 [1], a per-row [rows] (gmode 'row'), or None (G = 1)."""
     import torch
     if out is None:
         out = torch.empty(rows, cols, dtype=torch.bfloat16, device=codes.device)
-    _check(lib().ss_dequantize_nvfp4(_ptr(codes), _ptr(scales), rows, cols, _ptr(G), _ptr(out),
-                                     _stream_ptr(stream)), "ss_dequantize_nvfp4")
+    per_row = G is not None and G.numel() == rows and rows > 1
+    a = DequantArgs(_ptr(codes), _ptr(scales), rows, cols, _ptr(G), int(per_row),
+                    SCALE_LAYOUTS[scale_layout], _ptr(out), _stream_ptr(stream))
+    _check(lib().ss_dequantize_nvfp4_ex(ctypes.byref(a)), "ss_dequantize_nvfp4_ex")
     return out
 
 

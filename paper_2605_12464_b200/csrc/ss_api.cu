@@ -215,9 +215,70 @@ ss_status validate_io(const ss_tensor_io& t, int gmode) {
   const int64_t nb = t.rows * t.cols / 16;
   if (nb > 0 && (!t.in_bf16 || !t.out_codes || !t.out_scales)) return SS_ERR_INVALID_ARG;
   if (gmode == SS_GLOBAL_DEVICE_AMAX && !t.d_amax_bits) return SS_ERR_INVALID_ARG;
+  if (gmode == SS_GLOBAL_ROW && nb > 0 && !t.d_global_scale) return SS_ERR_INVALID_ARG;
+  if (t.scale_layout != SS_SCALE_LINEAR && t.scale_layout != SS_SCALE_SWIZZLED)
+    return SS_ERR_INVALID_ARG;
+  if (nb >= ((int64_t)1 << 31)) return SS_ERR_INVALID_ARG;  // 32-bit block index per tensor
   if (!aligned(t.in_bf16, 16) || !aligned(t.out_codes, 8) || !aligned(t.out_err, 8) ||
       !aligned(t.d_err_sums, 8) || !aligned(t.d_amax_bits, 4) || !aligned(t.d_global_scale, 4))
     return SS_ERR_ALIGNMENT;
+  return SS_OK;
+}
+
+int64_t scale_bytes(int64_t rows, int64_t cols, int layout) {
+  const int64_t nbr = cols / 16;
+  if (layout == SS_SCALE_SWIZZLED) return ((rows + 127) / 128) * ((nbr + 3) / 4) * 512;
+  return rows * nbr;
+}
+
+void row_geometry(int64_t cols, uint32_t* nbr, uint32_t* magic, uint32_t* nkt) {
+  *nbr = (uint32_t)std::max<int64_t>(1, cols / 16);
+  *magic = (uint32_t)(0xFFFFFFFFu / *nbr);
+  *nkt = (*nbr + 3) / 4;
+}
+
+int rows_grid(int sms) {
+  static int occ = 0;
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ss::rowscale_kernel, ss::kThreads, 0) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      occ = 4;
+    }
+    occ = std::max(occ, 1);
+  }
+  return sms * occ;
+}
+
+// Per-row global scales of every tensor into its d_global_scale (SS_GLOBAL_ROW).
+ss_status rowscale_launch(const ss_tensor_io* io, int count, uint32_t* flags, cudaStream_t st,
+                          int sms) {
+  int i = 0;
+  while (i < count) {
+    ss::RowBatch b;
+    std::memset(&b, 0, sizeof(b));
+    b.flags = flags;
+    int64_t tasks = 0;
+    for (; i < count && b.n < ss::kMaxTensors; i++) {
+      if (io[i].rows * io[i].cols == 0) continue;
+      ss::RTensor& t = b.t[b.n++];
+      t.in = reinterpret_cast<const uint4*>(io[i].in_bf16);
+      t.g_row = io[i].d_global_scale;
+      t.rows = io[i].rows;
+      t.rowvec = (int32_t)(io[i].cols / 8);
+      int lpr = 1;
+      while (lpr * 2 <= std::min(32, t.rowvec)) lpr *= 2;
+      t.lpr = lpr;
+      t.task0 = tasks;
+      tasks += (t.rows + (32 / lpr) - 1) / (32 / lpr);
+    }
+    if (b.n == 0) break;
+    b.ntasks = tasks;
+    const int64_t want = (tasks + ss::kWarps - 1) / ss::kWarps;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, rows_grid(sms)));
+    ss::rowscale_kernel<<<grid, ss::kThreads, 0, st>>>(b);
+    if (ss_status s = launch_status()) return s;
+  }
   return SS_OK;
 }
 
@@ -226,7 +287,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
                         void* stream) {
   if (count < 0 || (count > 0 && !io)) return SS_ERR_INVALID_ARG;
   if (f_min > 0 || f_max < 0) return SS_ERR_INVALID_ARG;
-  if (gmode < SS_GLOBAL_NONE || gmode > SS_GLOBAL_DEVICE_AMAX) return SS_ERR_INVALID_ARG;
+  if (gmode < SS_GLOBAL_NONE || gmode > SS_GLOBAL_ROW) return SS_ERR_INVALID_ARG;
   for (int i = 0; i < count; i++)
     if (ss_status s = validate_io(io[i], gmode)) return s;
   int dev;
@@ -283,6 +344,17 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       return s;
   } else if (gmode == SS_GLOBAL_DEVICE_AMAX) {
     for (int i = 0; i < count; i++) amax[i] = io[i].d_amax_bits;
+  } else if (gmode == SS_GLOBAL_ROW) {
+    if (ss_status s = rowscale_launch(io, count, ws->flags, cs, info.sms)) return s;
+  }
+  // swizzled scales: zero the padding of partial 128x4 tiles first
+  for (int i = 0; i < count; i++) {
+    const ss_tensor_io& t = io[i];
+    if (t.scale_layout == SS_SCALE_SWIZZLED && t.rows * t.cols > 0 &&
+        (t.rows % 128 != 0 || (t.cols / 16) % 4 != 0) &&
+        cudaMemsetAsync(t.out_scales, 0, (size_t)scale_bytes(t.rows, t.cols, t.scale_layout), cs) !=
+            cudaSuccess)
+      return SS_ERR_CUDA;
   }
 
   QuantKernel k = pick_kernel(fmin, fmax);
@@ -293,7 +365,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     std::memset(&b, 0, sizeof(b));
     b.fmin = fmin;
     b.fmax = fmax;
-    b.gmode = gmode == SS_GLOBAL_NONE ? 0 : 1;
+    b.gmode = gmode == SS_GLOBAL_NONE ? 0 : (gmode == SS_GLOBAL_ROW ? 2 : 1);
     b.part1 = ws->part1;
     b.part2 = ws->part2;
     b.tick = ws->tick;
@@ -319,6 +391,10 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       q.sums = t.d_err_sums;
       q.g_out = t.d_global_scale;
       q.amax = amax[i];
+      q.g_row = gmode == SS_GLOBAL_ROW ? t.d_global_scale : nullptr;
+      if (gmode == SS_GLOBAL_ROW) q.g_out = nullptr;
+      row_geometry(t.cols, &q.nbr, &q.nbr_magic, &q.nkt);
+      q.swz = t.scale_layout == SS_SCALE_SWIZZLED;
       q.nb = nb;
       q.task0 = tk;
       q.seg0 = gr;
@@ -355,6 +431,7 @@ ss_tensor_io io_from_args(const ss_quant_args* a) {
   t.out_offset = a->out_offset;
   t.d_err_sums = a->d_err_sums;
   t.d_global_scale = a->d_global_scale;
+  t.scale_layout = a->scale_layout;
   return t;
 }
 
@@ -410,7 +487,13 @@ const char* ss_status_string(int s) {
   }
 }
 
-int ss_version(void) { return 200; }
+int ss_version(void) { return 300; }
+
+int64_t ss_scale_bytes(int64_t rows, int64_t cols, int scale_layout) {
+  if (rows < 0 || cols < 0 || cols % 16 != 0) return -1;
+  if (scale_layout != SS_SCALE_LINEAR && scale_layout != SS_SCALE_SWIZZLED) return -1;
+  return scale_bytes(rows, cols, scale_layout);
+}
 
 ss_status ss_tensor_amax(const void* in_bf16, int64_t n, uint32_t* d_amax_bits, int accumulate,
                          void* stream) {
@@ -461,23 +544,48 @@ ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int 
   return quantize_core(tensors, count, f_min, f_max, global_scale_mode, stream);
 }
 
-ss_status ss_dequantize_nvfp4(const uint8_t* codes, const uint8_t* scales, int64_t rows,
-                              int64_t cols, const float* d_global_scale, void* out_bf16,
-                              void* stream) {
-  if (rows < 0 || cols < 0 || cols % 16 != 0) return SS_ERR_INVALID_ARG;
-  const int64_t nb = rows * cols / 16;
-  if (nb > 0 && (!codes || !scales || !out_bf16)) return SS_ERR_INVALID_ARG;
-  if (!aligned(codes, 8) || !aligned(out_bf16, 16)) return SS_ERR_ALIGNMENT;
+ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {
+  if (!a) return SS_ERR_INVALID_ARG;
+  if (a->rows < 0 || a->cols < 0 || a->cols % 16 != 0) return SS_ERR_INVALID_ARG;
+  if (a->scale_layout != SS_SCALE_LINEAR && a->scale_layout != SS_SCALE_SWIZZLED)
+    return SS_ERR_INVALID_ARG;
+  const int64_t nb = a->rows * a->cols / 16;
+  if (nb > 0 && (!a->codes || !a->scales || !a->out_bf16)) return SS_ERR_INVALID_ARG;
+  if (a->g_per_row && nb > 0 && !a->d_global_scale) return SS_ERR_INVALID_ARG;
+  if (nb >= ((int64_t)1 << 31)) return SS_ERR_INVALID_ARG;
+  if (!aligned(a->codes, 8) || !aligned(a->out_bf16, 16)) return SS_ERR_ALIGNMENT;
   int dev;
   DeviceInfo info;
   if (ss_status s = device_check(&dev, &info)) return s;
   if (nb == 0) return SS_OK;
+  ss::DequantParams p;
+  p.codes = reinterpret_cast<const uint2*>(a->codes);
+  p.scales = a->scales;
+  p.nb = nb;
+  p.g = a->d_global_scale;
+  p.g_per_row = a->g_per_row;
+  row_geometry(a->cols, &p.nbr, &p.nbr_magic, &p.nkt);
+  p.swz = a->scale_layout == SS_SCALE_SWIZZLED;
+  p.out = reinterpret_cast<uint4*>(a->out_bf16);
   int64_t want = (nb + 255) / 256;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)info.sms * 8));
-  ss::dequant_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const uint2*>(codes), scales, nb, d_global_scale,
-      reinterpret_cast<uint4*>(out_bf16));
+  ss::dequant_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(a->stream)>>>(p);
   return launch_status();
+}
+
+ss_status ss_dequantize_nvfp4(const uint8_t* codes, const uint8_t* scales, int64_t rows,
+                              int64_t cols, const float* d_global_scale, void* out_bf16,
+                              void* stream) {
+  ss_dequant_args a;
+  std::memset(&a, 0, sizeof(a));
+  a.codes = codes;
+  a.scales = scales;
+  a.rows = rows;
+  a.cols = cols;
+  a.d_global_scale = d_global_scale;
+  a.out_bf16 = out_bf16;
+  a.stream = stream;
+  return ss_dequantize_nvfp4_ex(&a);
 }
 
 ss_status ss_get_device_status(int* flags, void* stream) {

@@ -220,6 +220,22 @@ __device__ __forceinline__ float global_scale(uint32_t ab, uint32_t* flags, bool
   return G;
 }
 
+// Row of flat block b (b < 2^31) for nbr blocks per row: multiply-high by
+// floor((2^32-1)/nbr) is exact or one short; one correction step.
+__device__ __forceinline__ uint32_t div_rows(uint32_t b, uint32_t nbr, uint32_t magic) {
+  uint32_t q = __umulhi(b, magic);
+  if (b - q * nbr >= nbr) q++;
+  return q;
+}
+
+// Byte offset of scale (row r, scale column j) in the tensor-core layout of
+// block-scaled MMA (cuBLAS / CUTLASS Sm1xx "128x4" scale-factor atom,
+// R15b): 512-B tiles of 128 rows x 4 scale columns, tiles row-band-major,
+// inside a tile (r % 32) * 16 + ((r / 32) % 4) * 4 + j % 4.
+__device__ __forceinline__ uint32_t swizzled_scale_offset(uint32_t r, uint32_t j, uint32_t nkt) {
+  return ((r >> 7) * nkt + (j >> 2)) * 512u + (r & 31u) * 16u + ((r >> 5) & 3u) * 4u + (j & 3u);
+}
+
 // ---------------------------------------------------------------------------
 // Batch descriptors (kernel parameters; __grid_constant__).
 // ---------------------------------------------------------------------------
@@ -231,16 +247,21 @@ struct QTensor {
   int8_t* offsets;          // nullable [nb]
   double* sums;             // nullable [2]
   float* g_out;             // nullable
-  const uint32_t* amax;     // gmode given: FP32 bits of the tensor amax
+  const uint32_t* amax;     // gmode 1: FP32 bits of the tensor amax
+  const float* g_row;       // gmode 2: per-row global scales [rows]
   int64_t nb;               // NVFP4 blocks
   int64_t task0;            // first global task of this tensor
   int64_t seg0;             // first global segment (error-sum kernel CTA) of this tensor
+  uint32_t nbr;             // blocks per row (cols / 16)
+  uint32_t nbr_magic;       // floor((2^32 - 1) / nbr): row = div_rows(block)
+  uint32_t nkt;             // swizzled layout: ceil(nbr / 4) scale tiles per 128-row band
+  int swz;                  // scale layout: 0 linear [rows][nbr], 1 128x4 swizzled (R15b)
 };
 
 struct QuantBatch {
   int n;                    // tensors in this launch
   int fmin, fmax;           // window (runtime loop variant only)
-  int gmode;                // 0: G = 1; 1: G from t[i].amax
+  int gmode;                // 0: G = 1; 1: G from t[i].amax; 2: per-row G from t[i].g_row
   int64_t ntasks;           // total tasks of the batch
   int64_t nsegs;            // total error-sum segments of the batch
   double2* part1;           // per task {sum best, sum base}   (when any sums wanted)
@@ -515,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     }
   };
   auto gscale = [&](int ti, bool report) -> float {
-    if (p.gmode == 0) return 1.0f;
+    if (p.gmode != 1) return 1.0f;  // 0: G = 1; 2: per-row G, read per block
     return global_scale(__ldg(p.t[ti].amax), p.flags, report);
   };
   // Dynamic scheduling: counter c hands out tasks c, c + kCounters, ... ; warp
@@ -582,15 +603,27 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       uint64_t y2[kILP][8];
       int c0[kILP];
       const uint4* base[kILP];
+      uint32_t row[kILP];
 #pragma unroll
       for (int h = 0; h < kILP; h++) {
         const int j = (u0 + h) * 32 + lane;
+        // row of the block: per-row global scale and swizzled scale layout
+        row[h] = 0;
+        uint64_t Gb = GG;
+        if (T.g_row || T.swz) {  // warp-uniform
+          const uint32_t b = (uint32_t)(b0 + min(j, nblk - 1));
+          row[h] = div_rows(b, T.nbr, T.nbr_magic);
+          if (T.g_row) {
+            const float gr = __ldg(T.g_row + row[h]);
+            Gb = pack2(gr, gr);
+          }
+        }
         // a1 + a3: bf16 -> f32 is exact; y = RN(x * G)
         const uint4 v0 = buf[w][s][2 * j], v1 = buf[w][s][2 * j + 1];
         const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
         for (int k = 0; k < 8; k++) {
-          y2[h][k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), GG);
+          y2[h][k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), Gb);
           unpack2(y2[h][k], y[h][2 * k], y[h][2 * k + 1]);
         }
         // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
@@ -674,7 +707,12 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
         if (active) {
           __stcs(codes + j, cw);
-          scales[j] = (uint8_t)code;
+          if (!T.swz) {
+            scales[j] = (uint8_t)code;
+          } else {
+            const uint32_t b = (uint32_t)(b0 + j);
+            T.scales[swizzled_scale_offset(row[h], b - row[h] * T.nbr, T.nkt)] = (uint8_t)code;
+          }
           if (offsets) offsets[j] = (int8_t)((int)code - c0[h]);
           if (err) __stcs(err + j, make_float2(best[h], loss0[h]));
           sb += (double)best[h];
@@ -702,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       sc = warp_sum(sc);
       if (lane == 0) p.part1[task] = make_double2(sb, sc);
     }
-    if (T.g_out && b0 == 0 && lane == 0) *T.g_out = G;
+    if (T.g_out && b0 == 0 && lane == 0 && p.gmode != 2) *T.g_out = G;
 
     s = s + 1 == kStages ? 0 : s + 1;
   }
@@ -717,17 +755,82 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 }
 
 // ---------------------------------------------------------------------------
+// Per-row global scale (SS_GLOBAL_ROW; "after per-row scaling"):
+// g_row[r] = RN(2688 / max_k |x_rk|), 1 for an all-zero row, flags as the
+// per-tensor scale (R9, R14).  A warp task covers 32 / lpr rows with lpr
+// lanes per row (a power of two <= the row's 16-B vector count, <= 32);
+// lanes stride the row, a segmented xor-shuffle max finishes it.
+// ---------------------------------------------------------------------------
+struct RTensor {
+  const uint4* in;          // [rows][rowvec] 16-B vectors
+  float* g_row;             // [rows] output
+  int64_t rows;
+  int32_t rowvec;           // 16-B vectors per row (cols / 8)
+  int32_t lpr;              // lanes per row
+  int64_t task0;            // first global warp task
+};
+
+struct RowBatch {
+  int n;
+  int64_t ntasks;
+  uint32_t* flags;
+  RTensor t[kMaxTensors];
+};
+
+__global__ void __launch_bounds__(kThreads) rowscale_kernel(const __grid_constant__ RowBatch p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  int ti = 0;
+  for (int64_t task = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); task < p.ntasks; task += W) {
+    while (ti + 1 < p.n && p.t[ti + 1].task0 <= task) ti++;
+    const RTensor& T = p.t[ti];
+    const int lpr = T.lpr;
+    const int64_t r = (task - T.task0) * (32 / lpr) + lane / lpr;
+    const int sub = lane % lpr;
+    uint32_t m = 0;
+    if (r < T.rows) {
+      const uint4* src = T.in + r * T.rowvec;
+      const uint32_t M = 0x7FFF7FFFu;
+      for (int v = sub; v < T.rowvec; v += lpr) {
+        const uint4 a = __ldcs(src + v);
+        m = __vmaxu2(m, __vmaxu2(__vmaxu2(a.x & M, a.y & M), __vmaxu2(a.z & M, a.w & M)));
+      }
+    }
+    uint32_t mx = max(m & 0xFFFFu, m >> 16);
+    for (int o = lpr >> 1; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (sub == 0 && r < T.rows) T.g_row[r] = global_scale(mx << 16, p.flags, true);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Dequantize kernel: xhat = RNE_bf16(RN((q * s) / G)).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) dequant_kernel(const uint2* __restrict__ codes,
-                                                      const uint8_t* __restrict__ scales,
-                                                      int64_t nb, const float* __restrict__ g,
-                                                      uint4* __restrict__ out) {
-  const float G = g ? *g : 1.0f;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+struct DequantParams {
+  const uint2* codes;
+  const uint8_t* scales;
+  int64_t nb;
+  const float* g;           // nullable: G = 1; per tensor [1] or per row [rows]
+  int g_per_row;
+  uint32_t nbr, nbr_magic, nkt;
+  int swz;                  // scale layout (0 linear, 1 swizzled)
+  uint4* out;
+};
+
+__global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DequantParams p) {
+  const float G0 = (p.g && !p.g_per_row) ? *p.g : 1.0f;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < p.nb;
        b += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 cw = __ldcs(codes + b);
-    const float s = f16_to_f32(e4m3_to_f16(scales[b]));
+    const uint2 cw = __ldcs(p.codes + b);
+    float G = G0;
+    uint8_t sc;
+    if (p.g_per_row || p.swz) {
+      const uint32_t r = div_rows((uint32_t)b, p.nbr, p.nbr_magic);
+      if (p.g_per_row) G = p.g[r];
+      sc = p.swz ? p.scales[swizzled_scale_offset(r, (uint32_t)b - r * p.nbr, p.nkt)] : p.scales[b];
+    } else {
+      sc = p.scales[b];
+    }
+    const float s = f16_to_f32(e4m3_to_f16(sc));
     uint32_t o[8];
     const uint32_t words[2] = {cw.x, cw.y};
 #pragma unroll
@@ -746,8 +849,8 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint2* __restrict__ 
         o[h * 4 + k] = r;
       }
     }
-    __stcs(out + 2 * b, make_uint4(o[0], o[1], o[2], o[3]));
-    __stcs(out + 2 * b + 1, make_uint4(o[4], o[5], o[6], o[7]));
+    __stcs(p.out + 2 * b, make_uint4(o[0], o[1], o[2], o[3]));
+    __stcs(p.out + 2 * b + 1, make_uint4(o[4], o[5], o[6], o[7]));
   }
 }
 
