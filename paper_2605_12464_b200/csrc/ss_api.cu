@@ -160,20 +160,22 @@ ss_status amax_launch(const void* const* in, const int64_t* n, uint32_t* out, in
 typedef void (*QuantKernel)(QuantBatch);
 
 template <int NEG, int POS>
-QuantKernel qk() { return ss::quant_kernel<NEG, POS>; }
+QuantKernel qk(bool ri) {
+  return ri ? ss::quant_kernel<NEG, POS, true> : ss::quant_kernel<NEG, POS, false>;
+}
 
-QuantKernel pick_kernel(int fmin, int fmax) {
+QuantKernel pick_kernel(int fmin, int fmax, bool ri) {
   if (fmin == -fmax) {
     switch (fmax) {
-#define SS_SYM(R) case R: return qk<R, R>();
+#define SS_SYM(R) case R: return qk<R, R>(ri);
       SS_SYM(0) SS_SYM(1) SS_SYM(2) SS_SYM(3) SS_SYM(4) SS_SYM(5) SS_SYM(6) SS_SYM(7) SS_SYM(8)
       SS_SYM(9) SS_SYM(10) SS_SYM(11) SS_SYM(12) SS_SYM(13) SS_SYM(14) SS_SYM(15) SS_SYM(16)
 #undef SS_SYM
       default: break;
     }
   }
-  if (fmin == -2 && fmax == 6) return qk<2, 6>();  // the paper's production window
-  return qk<-1, -1>();
+  if (fmin == -2 && fmax == 6) return qk<2, 6>(ri);  // the paper's production window
+  return qk<-1, -1>(ri);
 }
 
 int occupancy(QuantKernel k) {
@@ -357,7 +359,9 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       return SS_ERR_CUDA;
   }
 
-  QuantKernel k = pick_kernel(fmin, fmax);
+  bool ri = gmode == SS_GLOBAL_ROW;
+  for (int i = 0; i < count; i++) ri |= io[i].scale_layout == SS_SCALE_SWIZZLED;
+  QuantKernel k = pick_kernel(fmin, fmax, ri);
   const int64_t slots = (int64_t)info.sms * occupancy(k);
   int i = 0;
   while (i < count) {

@@ -502,7 +502,9 @@ __device__ __forceinline__ constexpr int scan_offset(int i) {
   }
 
 // NEG/POS >= 0: compile-time window [-NEG, POS]; NEG < 0: runtime [fmin, fmax].
-template <int NEG, int POS>
+// RI: the batch needs each block's row (per-row G or the swizzled scale
+// layout); without it those per-block steps are compiled out.
+template <int NEG, int POS, bool RI>
 __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
   constexpr int Pad = NEG < 0 ? 126 : (NEG > POS ? NEG : POS);
   constexpr int TabW = 127 + 2 * Pad;
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         // row of the block: per-row global scale and swizzled scale layout
         row[h] = 0;
         uint64_t Gb = GG;
-        if (T.g_row || T.swz) {  // warp-uniform
+        if (RI && (T.g_row || T.swz)) {  // warp-uniform
           const uint32_t b = (uint32_t)(b0 + min(j, nblk - 1));
           row[h] = div_rows(b, T.nbr, T.nbr_magic);
           if (T.g_row) {
@@ -707,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
         if (active) {
           __stcs(codes + j, cw);
-          if (!T.swz) {
+          if (!RI || !T.swz) {
             scales[j] = (uint8_t)code;
           } else {
             const uint32_t b = (uint32_t)(b0 + j);
