@@ -313,3 +313,31 @@ def test_host_batched_entry_point(ss, oracle_lib):
             assert np.array_equal(c.numpy(), ref.codes)
             assert np.array_equal(s.numpy(), ref.scales)
             assert np.array_equal(e.numpy().view(np.uint32), ref.err.view(np.uint32))
+
+
+def test_cuda_graph_capture_and_replay(ss, oracle_lib):
+    # Once the workspace is warm, a batched amax + quantize step is capturable
+    # (no host sync or allocation inside) and replays bit-exactly.
+    xs = [ssgen.generate("student_t", r, c, seed=12, tid=950 + k)
+          for k, (r, c) in enumerate([(64, 256), (33, 4096), (1, 16)])]
+    xd = [x.cuda() for x in xs]
+    outs = [ss.alloc_out(x) for x in xd]
+    amax = torch.zeros(len(xd), dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ss.tensor_amax_batched(xd, out=amax)                       # warm-up: workspace allocated
+        ss.quantize_batched(xd, outs, radius=8, gmode="device_amax", amax=amax)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ss.tensor_amax_batched(xd, out=amax)
+        ss.quantize_batched(xd, outs, radius=8, gmode="device_amax", amax=amax)
+    for o in outs:
+        o.codes.zero_()
+        o.sums.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for x, o in zip(xs, outs):
+        ref = oracle_lib.quantize(x, *x.shape, -8, 8, "tensor")
+        _cmp(o, ref, *x.shape)
