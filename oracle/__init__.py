@@ -20,5 +20,11 @@ from .oracle import (  # noqa: F401
     global_scale,
     quantize,
     dequantize,
+    FORMATS,
+    e2m3_value,
+    e2m3_encode,
+    ue8m0_value,
+    ue8m0_encode,
+    quantize_fmt,
     OracleError,
 )

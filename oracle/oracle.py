@@ -79,6 +79,18 @@ def lib():
             L.so_quantize.restype = ctypes.c_int
             L.so_quantize.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
                                       P, P, P, P, P, P, P, ctypes.c_int]
+            L.so_e2m3_value.restype = ctypes.c_double
+            L.so_e2m3_value.argtypes = [ctypes.c_int]
+            L.so_e2m3_encode.restype = ctypes.c_int
+            L.so_e2m3_encode.argtypes = [ctypes.c_float]
+            L.so_ue8m0_value.restype = ctypes.c_float
+            L.so_ue8m0_value.argtypes = [ctypes.c_int]
+            L.so_ue8m0_encode.restype = ctypes.c_int
+            L.so_ue8m0_encode.argtypes = [ctypes.c_float]
+            L.so_quantize_fmt.restype = ctypes.c_int
+            L.so_quantize_fmt.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P,
+                                          P, P, ctypes.c_int]
             L.so_dequantize.restype = ctypes.c_int
             L.so_dequantize.argtypes = [P, P, i64, i64, ctypes.c_float, P]
             _LIB = L
@@ -209,3 +221,53 @@ def dequantize(codes, scales, rows: int, cols: int, G=1.0) -> np.ndarray:
         _check(lib().so_dequantize(_ptr(c), _ptr(sc), 1, cols, ctypes.c_float(float(G[r])), _ptr(o)))
         out[r] = o
     return out
+
+
+# ---------------------------------------------------------------------------
+# Other block formats: name -> (value format, scale format, block)
+# ---------------------------------------------------------------------------
+FORMATS = {
+    "nvfp4": (0, 0, 16),        # E2M1 values, UE4M3 scales, 16-blocks
+    "mxfp4": (0, 1, 32),        # E2M1 values, UE8M0 scales, 32-blocks
+    "mxfp6_e2m3": (1, 1, 32),   # E2M3 values, UE8M0 scales, 32-blocks
+    "nvfp6_e2m3": (1, 0, 16),   # E2M3 values, UE4M3 scales, 16-blocks (value sweep)
+}
+
+
+def e2m3_value(code: int) -> float:
+    return lib().so_e2m3_value(int(code))
+
+
+def e2m3_encode(t: float) -> int:
+    return lib().so_e2m3_encode(float(t))
+
+
+def ue8m0_value(code: int) -> float:
+    return lib().so_ue8m0_value(int(code))
+
+
+def ue8m0_encode(v: float) -> int:
+    return lib().so_ue8m0_encode(float(v))
+
+
+def quantize_fmt(x, rows: int, cols: int, fmin: int, fmax: int, fmt="mxfp4", gmode="none",
+                 amax_bits: int | None = None, threads: int = 0) -> QuantResult:
+    """so_quantize_fmt; codes are [rows][cols/2] nibbles (E2M1) or [rows][cols] bytes (E2M3)."""
+    vf, sf, bs = FORMATS[fmt] if isinstance(fmt, str) else fmt
+    x = _as_u16(x).reshape(-1)
+    assert x.size == rows * cols
+    gm = GMODES[gmode] if isinstance(gmode, str) else int(gmode)
+    nb = rows * cols // bs
+    codes = np.empty((rows, cols // 2 if vf == 0 else cols), np.uint8)
+    scales = np.empty((rows, cols // bs), np.uint8)
+    offs = np.empty(nb, np.int8)
+    err = np.empty((nb, 2), np.float32)
+    sums = np.zeros(2, np.float64)
+    neval = np.zeros(1, np.int64)
+    G = np.zeros(rows if gm == 3 else 1, np.float32)
+    ab = None if amax_bits is None else np.array([amax_bits], np.uint32)
+    _check(lib().so_quantize_fmt(_ptr(x), rows, cols, int(fmin), int(fmax), gm, _ptr(ab), vf, sf, bs,
+                                 _ptr(codes), _ptr(scales), _ptr(offs), _ptr(err), _ptr(sums),
+                                 _ptr(neval), _ptr(G), int(threads)))
+    return QuantResult(codes, scales, offs, err, sums, int(neval[0]),
+                       G.copy() if gm == 3 else float(G[0]))

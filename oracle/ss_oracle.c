@@ -354,3 +354,257 @@ int so_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows,
     }
   return 0;
 }
+
+
+/* ====================================================================== */
+/* Other block formats ("the quantization and   */
+/* dequantization algorithms are identical", P:301-308 format study).     */
+/*   value formats: E2M1 (vmax 6) and E2M3 (MXFP6 values, vmax 7.5)        */
+/*   scale formats: UE4M3 (codes 1..126, R2) and UE8M0 (2^(c-127),         */
+/*                  codes 0..254; no zero, no NaN code 255)                */
+/*   block size:    16 or 32                                               */
+/* ====================================================================== */
+
+/* E2M3 (1 sign, 2 exponent bits, bias 1, 3 mantissa bits): code = e<<3|m,
+ * e = 0: m/8; else (1 + m/8) * 2^(e-1).  Largest 7.5. */
+double so_e2m3_value(int code) {
+  int mag = code & 31, e = mag >> 3, m = mag & 7;
+  double v = (e == 0) ? m / 8.0 : ldexp(1.0 + m / 8.0, e - 1);
+  return (code & 32) ? -v : v;
+}
+
+/* round_E2M3: nearest magnitude, ties to the even code, saturating at 7.5,
+ * sign copied from t (as R10/R11 for E2M1). */
+int so_e2m3_encode(float t) {
+  int sign = signbit(t) ? 32 : 0;
+  double a = fabs((double)t);
+  if (a > 7.5) return sign | 31;
+  int best = 0;
+  double best_d = a;
+  for (int k = 1; k < 32; k++) {
+    double d = fabs(a - so_e2m3_value(k));
+    if (d < best_d || (d == best_d && (k % 2) == 0)) {
+      best = k;
+      best_d = d;
+    }
+  }
+  return sign | best;
+}
+
+/* UE8M0 scale value 2^(c - 127), c = 0..254. */
+float so_ue8m0_value(int code) {
+  if (code < 0 || code > 254) return NAN;
+  return (float)ldexp(1.0, code - 127);
+}
+
+/* round_UE8M0 (R19): the smallest power of two >= v, saturating to
+ * [2^-127, 2^127] (the format has no zero).  The paper only says the MXFP4
+ * algorithm is "identical" with a UE8M0 scale; rounding the scale
+ * up keeps x_max / s <= vmax (no clamping of the block maximum), is the
+ * hardware conversion cvt.rp.satfinite.ue8m0x2.f32, and reproduces the
+ * MXFP4 offset histogram of P:308 (two offsets, mostly 0). */
+int so_ue8m0_encode(float v) {
+  double a = (double)v;
+  for (int c = 0; c <= 254; c++)
+    if (ldexp(1.0, c - 127) >= a) return c;
+  return 254;
+}
+
+static double fmt_value(int vfmt, int code) {
+  return vfmt == 0 ? so_e2m1_value(code) : so_e2m3_value(code);
+}
+static int fmt_encode(int vfmt, float t) {
+  return vfmt == 0 ? so_e2m1_encode(t) : so_e2m3_encode(t);
+}
+static float fmt_inv_vmax(int vfmt) {
+  /* RN(1 / vmax) in binary32, the Alg. 1 line 2 form (R8) */
+  return vfmt == 0 ? 1.0f / 6.0f : 1.0f / 7.5f;
+}
+
+/* One candidate of a `bs`-element block: quantize, dequantize, loss.  The
+ * loss of each 16-element half is the R12 chain pair (a over even, b over
+ * odd indices of the half, then a + b); a 32-element block adds its two
+ * halves' losses, low half first (R20). */
+static float fmt_candidate_loss(int vfmt, int bs, const float* y, float s, float rho,
+                                uint8_t* code) {
+  float total = 0.0f;
+  for (int h = 0; h < bs / 16; h++) {
+    float d[16];
+    for (int i = 0; i < 16; i++) {
+      float t = y[16 * h + i] * rho; /* R7 */
+      code[16 * h + i] = (uint8_t)fmt_encode(vfmt, t);
+      float q = (float)fmt_value(vfmt, code[16 * h + i]);
+      d[i] = fmaf(-q, s, y[16 * h + i]);
+    }
+    float a = d[0] * d[0];
+    for (int i = 2; i < 16; i += 2) a = fmaf(d[i], d[i], a);
+    float b = d[1] * d[1];
+    for (int i = 3; i < 16; i += 2) b = fmaf(d[i], d[i], b);
+    total = (h == 0) ? a + b : total + (a + b);
+  }
+  return total;
+}
+
+/* Algorithm 1 for one block of a format (vfmt, sfmt, bs): the NVFP4 rules
+ * R2-R5 for UE4M3 scales; for UE8M0 every code 0..254 is a valid scale (there
+ * is no zero-scale candidate) and c0 = round_UE8M0(x_max * RN(1/vmax)). */
+int so_search_block_fmt(int vfmt, int sfmt, int bs, const float* y, int fmin, int fmax,
+                        so_block_result_fmt* out) {
+  if (fmin > 0 || fmax < 0 || (bs != 16 && bs != 32) || vfmt < 0 || vfmt > 1 || sfmt < 0 ||
+      sfmt > 1)
+    return 1;
+  float xmax = 0.0f;
+  for (int i = 0; i < bs; i++)
+    if (fabsf(y[i]) > xmax) xmax = fabsf(y[i]);
+  const float v = xmax * fmt_inv_vmax(vfmt);
+  const int c0 = sfmt == 0 ? so_e4m3_encode(v) : so_ue8m0_encode(v);
+  const int cmax = sfmt == 0 ? 126 : 254, cmin = sfmt == 0 ? 1 : 0;
+  int have = 0, cstar = -1, n_eval = 0;
+  float best = INFINITY, base = NAN;
+  uint8_t code[32], best_code[32] = {0};
+  for (int f = fmin; f <= fmax; f++) {
+    int c = c0 + f;
+    float s, rho;
+    if (sfmt == 0 && f == 0 && c0 == 0) {
+      s = 0.0f; /* R3 */
+      rho = 0.0f;
+    } else if (c < cmin || c > cmax) {
+      continue;
+    } else {
+      s = sfmt == 0 ? so_e4m3_value(c) : so_ue8m0_value(c);
+      rho = 1.0f / s;
+    }
+    float loss = fmt_candidate_loss(vfmt, bs, y, s, rho, code);
+    n_eval++;
+    if (f == 0) base = loss;
+    if (!have || loss < best) { /* R4 */
+      have = 1;
+      best = loss;
+      cstar = c;
+      memcpy(best_code, code, (size_t)bs);
+    }
+  }
+  out->c0 = c0;
+  out->cstar = cstar;
+  out->fstar = cstar - c0;
+  out->n_evaluated = n_eval;
+  out->err_best = best;
+  out->err_base = base;
+  memcpy(out->code, best_code, (size_t)bs);
+  return 0;
+}
+
+/* Whole tensor in a format.  Codes: E2M1 packed two per byte (low nibble =
+ * even element, R15) -> [rows][cols/2]; E2M3 one 6-bit code per byte (sign
+ * bit 5) -> [rows][cols].  Scales [rows][cols/bs].  gmode: 0 NONE, 1 TENSOR,
+ * 2 GIVEN, 3 ROW, as so_quantize, with G = RN(vmax * 448 / A) for UE4M3
+ * scales; UE8M0 scales take gmode 0 only (their range needs no global scale). */
+int so_quantize_fmt(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int fmax,
+                    int gmode, const uint32_t* amax_bits_in, int vfmt, int sfmt, int bs,
+                    uint8_t* codes, uint8_t* scales, int8_t* offsets, float* err,
+                    double* sums, int64_t* n_eval, float* G_out, int threads) {
+  if (rows < 0 || cols < 0 || (bs != 16 && bs != 32) || cols % bs != 0 || fmin > 0 ||
+      fmax < 0 || vfmt < 0 || vfmt > 1 || sfmt < 0 || sfmt > 1)
+    return 1;
+  if (gmode < 0 || gmode > 3 || (gmode == 2 && !amax_bits_in) || (sfmt == 1 && gmode != 0))
+    return 1;
+  const int lim = sfmt == 0 ? 126 : 254;
+  if (fmin < -lim) fmin = -lim;
+  if (fmax > lim) fmax = lim;
+  const float numer = vfmt == 0 ? 2688.0f : 3360.0f; /* vmax * 448 */
+  const int64_t nbr = cols / bs, nb = rows * nbr;
+  float* Gr = (float*)malloc(sizeof(float) * (rows > 0 ? rows : 1));
+  float* e = (float*)malloc(sizeof(float) * 2 * (nb > 0 ? nb : 1));
+  int32_t* ne = (int32_t*)malloc(sizeof(int32_t) * (nb > 0 ? nb : 1));
+  if (!Gr || !e || !ne) {
+    free(Gr);
+    free(e);
+    free(ne);
+    return 1;
+  }
+  int st = 0;
+  for (int64_t r = 0; r < rows && !st; r++) Gr[r] = 1.0f;
+  if (gmode == 3) {
+    for (int64_t r = 0; r < rows && !st; r++) {
+      uint32_t ab = 0;
+      st = so_tensor_amax(x + r * cols, cols, &ab);
+      float A;
+      memcpy(&A, &ab, 4);
+      if (!st && A > 0.0f) {
+        Gr[r] = numer / A;
+        if (!isfinite(Gr[r])) st = 5;
+      }
+    }
+    if (!st && G_out)
+      for (int64_t r = 0; r < rows; r++) G_out[r] = Gr[r];
+  } else if (gmode == 1 || gmode == 2) {
+    uint32_t ab = 0;
+    if (gmode == 1)
+      st = so_tensor_amax(x, rows * cols, &ab);
+    else
+      ab = *amax_bits_in;
+    float A;
+    memcpy(&A, &ab, 4);
+    if (!st && !(A >= 0.0f && isfinite(A))) st = 4;
+    float G = 1.0f;
+    if (!st && A > 0.0f) {
+      G = numer / A;
+      if (!isfinite(G)) st = 5;
+    }
+    for (int64_t r = 0; r < rows; r++) Gr[r] = G;
+    if (!st && G_out) *G_out = G;
+  } else if (G_out) {
+    *G_out = 1.0f;
+  }
+  if (st) {
+    free(Gr);
+    free(e);
+    free(ne);
+    return st;
+  }
+#ifdef _OPENMP
+  if (threads <= 0) threads = omp_get_num_procs();
+#pragma omp parallel for schedule(dynamic, 16) num_threads(threads)
+#endif
+  for (int64_t r = 0; r < rows; r++) {
+    for (int64_t bj = 0; bj < nbr; bj++) {
+      const int64_t blk = r * nbr + bj;
+      float y[32];
+      for (int i = 0; i < bs; i++) {
+        float xv = bf16_to_float(x[r * cols + bj * bs + i]);
+        y[i] = (gmode == 0) ? xv : xv * Gr[r];
+      }
+      so_block_result_fmt res;
+      so_search_block_fmt(vfmt, sfmt, bs, y, fmin, fmax, &res);
+      if (vfmt == 0) {
+        for (int j = 0; j < bs / 2; j++)
+          codes[r * (cols / 2) + bj * (bs / 2) + j] =
+              (uint8_t)(res.code[2 * j] | (res.code[2 * j + 1] << 4));
+      } else {
+        for (int j = 0; j < bs; j++) codes[r * cols + bj * bs + j] = res.code[j];
+      }
+      scales[blk] = (uint8_t)res.cstar;
+      if (offsets) offsets[blk] = (int8_t)res.fstar;
+      e[2 * blk] = res.err_best;
+      e[2 * blk + 1] = res.err_base;
+      ne[blk] = res.n_evaluated;
+    }
+  }
+  double sb = 0.0, s0 = 0.0;
+  int64_t total = 0;
+  for (int64_t b = 0; b < nb; b++) {
+    sb += (double)e[2 * b];
+    s0 += (double)e[2 * b + 1];
+    total += ne[b];
+  }
+  if (err) memcpy(err, e, sizeof(float) * 2 * nb);
+  if (sums) {
+    sums[0] = sb;
+    sums[1] = s0;
+  }
+  if (n_eval) *n_eval = total;
+  free(Gr);
+  free(e);
+  free(ne);
+  return 0;
+}

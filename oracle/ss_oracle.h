@@ -69,6 +69,25 @@ int so_quantize(const uint16_t* x_bf16, int64_t rows, int64_t cols, int fmin,
                 uint8_t* codes, uint8_t* scales, int8_t* offsets, float* err,
                 double* sums, int64_t* n_eval, float* G_out, int threads);
 
+/* Other block formats: value format vfmt 0 E2M1 / 1 E2M3,
+ * scale format sfmt 0 UE4M3 / 1 UE8M0 (R19), block size bs 16 / 32 (loss of
+ * a 32-block = low half + high half, each half as R12; R20). */
+double so_e2m3_value(int code);            /* code 0..63 (sign bit 5) -> value      */
+int    so_e2m3_encode(float t);            /* RNE, saturating at 7.5, sign kept     */
+float  so_ue8m0_value(int code);           /* 2^(code-127), code 0..254             */
+int    so_ue8m0_encode(float v);           /* smallest power of two >= v, sat. (R19)*/
+typedef struct {
+  int32_t c0, cstar, fstar, n_evaluated;
+  float err_best, err_base;
+  uint8_t code[32];                        /* value codes of the winner, one per byte */
+} so_block_result_fmt;
+int so_search_block_fmt(int vfmt, int sfmt, int bs, const float* y, int fmin, int fmax,
+                        so_block_result_fmt* out);
+int so_quantize_fmt(const uint16_t* x_bf16, int64_t rows, int64_t cols, int fmin, int fmax,
+                    int gmode, const uint32_t* amax_bits_in, int vfmt, int sfmt, int bs,
+                    uint8_t* codes, uint8_t* scales, int8_t* offsets, float* err,
+                    double* sums, int64_t* n_eval, float* G_out, int threads);
+
 /* Dequantization: xhat = RNE_bf16(RN((q * s) / G)). */
 int so_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows,
                   int64_t cols, float G, uint16_t* out_bf16);
