@@ -90,8 +90,25 @@ enum {
                              /* columns to 4 with zero bytes.  Size: ss_scale_bytes()         */
 };
 
-/* Bytes of the scale buffer of a [rows][cols] tensor in `scale_layout`. */
+/* Block formats (readings R19, R20).
+ * Codes: E2M1 values two per byte (low nibble = even element), E2M3 values
+ * one 6-bit code per byte (sign bit 5).  Scales: UE4M3 codes 0..126, or UE8M0
+ * codes 0..254 = 2^(c-127) rounded UP from x_max / vmax (R19; no global scale:
+ * UE8M0 formats take SS_GLOBAL_NONE only).  32-element blocks need
+ * cols % 32 == 0; their loss is the low half's R12 loss + the high half's. */
+enum {
+  SS_FMT_NVFP4 = 0,          /* E2M1 values, UE4M3 scales, 16-blocks (the north star)         */
+  SS_FMT_MXFP4 = 1,          /* E2M1 values, UE8M0 scales, 32-blocks                          */
+  SS_FMT_MXFP6_E2M3 = 2,     /* E2M3 values, UE8M0 scales, 32-blocks                          */
+  SS_FMT_NVFP6_E2M3 = 3      /* E2M3 values, UE4M3 scales, 16-blocks (the value-format sweep) */
+};
+
+/* Bytes of the scale buffer of a [rows][cols] tensor in `scale_layout`
+ * (NVFP4 blocks). */
 SS_API int64_t ss_scale_bytes(int64_t rows, int64_t cols, int scale_layout);
+/* Same for any format, and the bytes of its code buffer.  -1 on bad input. */
+SS_API int64_t ss_scale_bytes_fmt(int64_t rows, int64_t cols, int scale_layout, int format);
+SS_API int64_t ss_code_bytes(int64_t rows, int64_t cols, int format);
 
 /* Human-readable name of a status code (static string). */
 SS_API const char* ss_status_string(int status);
@@ -161,6 +178,7 @@ typedef struct {
                                 /* SS_GLOBAL_ROW: required, [rows] f32                     */
   void* stream;
   int scale_layout;             /* SS_SCALE_* (0 = linear)                                  */
+  int format;                   /* SS_FMT_* (0 = NVFP4)                                      */
 } ss_quant_args;
 
 SS_API ss_status ss_quantize_nvfp4_ex(const ss_quant_args* args);
@@ -189,6 +207,11 @@ typedef struct {
  */
 SS_API ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min,
                                     int f_max, int global_scale_mode, void* stream);
+
+/* The same for any block format (SS_FMT_*); windows are clamped to +-126
+ * (UE4M3) or +-254 (UE8M0) code steps. */
+SS_API ss_status ss_quantize_batched_fmt(const ss_tensor_io* tensors, int count, int f_min,
+                                  int f_max, int global_scale_mode, int format, void* stream);
 
 /*
  * Dequantization (step a8): xhat = RNE_bf16(RN((q * s) / G)).
@@ -245,6 +268,7 @@ typedef struct {
   int scale_layout;             /* SS_SCALE_*                                               */
   void* out_bf16;               /* [rows][cols] bf16, 16-B aligned                          */
   void* stream;
+  int format;                   /* SS_FMT_* (0 = NVFP4)                                      */
 } ss_dequant_args;
 
 SS_API ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* args);

@@ -26,5 +26,6 @@ from .oracle import (  # noqa: F401
     ue8m0_value,
     ue8m0_encode,
     quantize_fmt,
+    dequantize_fmt,
     OracleError,
 )

@@ -91,6 +91,9 @@ def lib():
             L.so_quantize_fmt.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P,
                                           P, P, ctypes.c_int]
+            L.so_dequantize_fmt.restype = ctypes.c_int
+            L.so_dequantize_fmt.argtypes = [P, P, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            P, ctypes.c_int, P]
             L.so_dequantize.restype = ctypes.c_int
             L.so_dequantize.argtypes = [P, P, i64, i64, ctypes.c_float, P]
             _LIB = L
@@ -271,3 +274,15 @@ def quantize_fmt(x, rows: int, cols: int, fmin: int, fmax: int, fmt="mxfp4", gmo
                                  _ptr(neval), _ptr(G), int(threads)))
     return QuantResult(codes, scales, offs, err, sums, int(neval[0]),
                        G.copy() if gm == 3 else float(G[0]))
+
+
+def dequantize_fmt(codes, scales, rows: int, cols: int, fmt="mxfp4", G=1.0) -> np.ndarray:
+    """bf16 bit patterns of xhat for a format; G scalar or per-row array."""
+    vf, sf, bs = FORMATS[fmt] if isinstance(fmt, str) else fmt
+    codes = np.ascontiguousarray(codes, np.uint8)
+    scales = np.ascontiguousarray(scales, np.uint8)
+    g = np.atleast_1d(np.asarray(G, np.float32)).copy()
+    out = np.empty((rows, cols), np.uint16)
+    _check(lib().so_dequantize_fmt(_ptr(codes), _ptr(scales), rows, cols, vf, sf, bs, _ptr(g),
+                                   int(g.size > 1), _ptr(out)))
+    return out

@@ -608,3 +608,29 @@ int so_quantize_fmt(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int
   free(ne);
   return 0;
 }
+
+/* Dequantization in a format: xhat = RNE_bf16(RN((q * s) / G_r)) with the
+ * code layout of so_quantize_fmt; G has one entry, or `rows` when per_row. */
+int so_dequantize_fmt(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols,
+                      int vfmt, int sfmt, int bs, const float* G, int per_row, uint16_t* out) {
+  if (rows < 0 || cols < 0 || (bs != 16 && bs != 32) || cols % bs != 0) return 1;
+  const int64_t nbr = cols / bs;
+  for (int64_t r = 0; r < rows; r++) {
+    const float g = per_row ? G[r] : G[0];
+    if (!(g > 0.0f)) return 1;
+    for (int64_t k = 0; k < cols; k++) {
+      int code;
+      if (vfmt == 0) {
+        uint8_t byte = codes[r * (cols / 2) + k / 2];
+        code = (k % 2 == 0) ? (byte & 15) : (byte >> 4);
+      } else {
+        code = codes[r * cols + k] & 63;
+      }
+      const int sc = scales[r * nbr + k / bs];
+      const float s = sfmt == 0 ? so_e4m3_value(sc) : so_ue8m0_value(sc);
+      const float q = (float)(vfmt == 0 ? so_e2m1_value(code) : so_e2m3_value(code));
+      out[r * cols + k] = float_to_bf16_rne((q * s) / g);
+    }
+  }
+  return 0;
+}

@@ -88,6 +88,9 @@ int so_quantize_fmt(const uint16_t* x_bf16, int64_t rows, int64_t cols, int fmin
                     uint8_t* codes, uint8_t* scales, int8_t* offsets, float* err,
                     double* sums, int64_t* n_eval, float* G_out, int threads);
 
+int so_dequantize_fmt(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols,
+                      int vfmt, int sfmt, int bs, const float* G, int per_row, uint16_t* out_bf16);
+
 /* Dequantization: xhat = RNE_bf16(RN((q * s) / G)). */
 int so_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows,
                   int64_t cols, float G, uint16_t* out_bf16);

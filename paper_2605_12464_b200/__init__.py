@@ -10,6 +10,7 @@ from ._binding import (  # noqa: F401
     FLAG_RANGE,
     GMODES,
     SCALE_LAYOUTS,
+    FORMATS,
     LIB_PATH,
     QuantOut,
     SSError,
@@ -30,5 +31,5 @@ from ._binding import (  # noqa: F401
 
 __all__ = [
     "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host", "quantize_host_batched",
-    "device_status", "scale_bytes", "SCALE_LAYOUTS", "status_string", "SSError", "QuantOut", "GMODES",
+    "device_status", "scale_bytes", "SCALE_LAYOUTS", "FORMATS", "status_string", "SSError", "QuantOut", "GMODES",
 ]

@@ -21,6 +21,9 @@ SS_OK, SS_ERR_INVALID_ARG, SS_ERR_ALIGNMENT, SS_ERR_CUDA = 0, 1, 2, 3
 SS_ERR_NONFINITE, SS_ERR_RANGE, SS_ERR_UNSUPPORTED_DEVICE = 4, 5, 6
 GMODES = {"none": 0, "tensor": 1, "device_amax": 2, "row": 3}
 SCALE_LAYOUTS = {"linear": 0, "swizzled": 1}
+# block formats (ss.h SS_FMT_*): name -> (id, block size, value bytes per element)
+FORMATS = {"nvfp4": (0, 16, 0.5), "mxfp4": (1, 32, 0.5), "mxfp6_e2m3": (2, 32, 1.0),
+           "nvfp6_e2m3": (3, 16, 1.0)}
 FLAG_NONFINITE, FLAG_RANGE = 1, 2
 
 _lock = threading.Lock()
@@ -78,6 +81,7 @@ class QuantArgs(ctypes.Structure):
         ("d_global_scale", ctypes.c_void_p),
         ("stream", ctypes.c_void_p),
         ("scale_layout", ctypes.c_int),
+        ("format", ctypes.c_int),
     ]
 
 
@@ -92,6 +96,7 @@ class DequantArgs(ctypes.Structure):
         ("scale_layout", ctypes.c_int),
         ("out_bf16", ctypes.c_void_p),
         ("stream", ctypes.c_void_p),
+        ("format", ctypes.c_int),
     ]
 
 
@@ -123,6 +128,12 @@ def lib():
             L.ss_dequantize_nvfp4_ex.argtypes = [ctypes.POINTER(DequantArgs)]
             L.ss_scale_bytes.restype = i64
             L.ss_scale_bytes.argtypes = [i64, i64, I]
+            L.ss_scale_bytes_fmt.restype = i64
+            L.ss_scale_bytes_fmt.argtypes = [i64, i64, I, I]
+            L.ss_code_bytes.restype = i64
+            L.ss_code_bytes.argtypes = [i64, i64, I]
+            L.ss_quantize_batched_fmt.restype = I
+            L.ss_quantize_batched_fmt.argtypes = [ctypes.POINTER(TensorIO), I, I, I, I, I, P]
             L.ss_dequantize_nvfp4.restype = I
             L.ss_dequantize_nvfp4.argtypes = [P, P, i64, i64, P, P, P]
             L.ss_quantize_nvfp4_host.restype = I
@@ -189,7 +200,7 @@ def tensor_amax(x, out=None, accumulate: bool = False, stream=None):
 def quantize(x, radius=None, fmin=None, fmax=None, gmode: str = "tensor", amax=None,
              want_err: bool = True, want_offsets: bool = True, want_sums: bool = True,
              want_g: bool = True, out: Optional[QuantOut] = None, scale_layout: str = "linear",
-             stream=None) -> QuantOut:
+             fmt: str = "nvfp4", stream=None) -> QuantOut:
     """ScaleSearch NVFP4 quantization of a [rows][cols] bf16 CUDA tensor (ss_quantize_nvfp4_ex)."""
     import torch
     assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous() and x.dim() == 2
@@ -199,10 +210,10 @@ def quantize(x, radius=None, fmin=None, fmax=None, gmode: str = "tensor", amax=N
     if gm == 2 and amax is None:
         raise ValueError("gmode='device_amax' needs amax (device int32/uint32 tensor)")
     if out is None:
-        out = alloc_out(x, want_err, want_offsets, want_sums, want_g, scale_layout, gmode)
+        out = alloc_out(x, want_err, want_offsets, want_sums, want_g, scale_layout, gmode, fmt)
     a = QuantArgs(_ptr(x), rows, cols, lo, hi, gm, _ptr(amax), _ptr(out.codes), _ptr(out.scales),
                   _ptr(out.err), _ptr(out.offsets), _ptr(out.sums), _ptr(out.G), _stream_ptr(stream),
-                  SCALE_LAYOUTS[scale_layout])
+                  SCALE_LAYOUTS[scale_layout], FORMATS[fmt][0])
     _check(lib().ss_quantize_nvfp4_ex(ctypes.byref(a)), "ss_quantize_nvfp4_ex")
     return out
 
@@ -222,26 +233,28 @@ def tensor_amax_batched(xs, out=None, accumulate: bool = False, stream=None):
     return out
 
 
-def scale_bytes(rows: int, cols: int, scale_layout: str = "linear") -> int:
-    return int(lib().ss_scale_bytes(rows, cols, SCALE_LAYOUTS[scale_layout]))
+def scale_bytes(rows: int, cols: int, scale_layout: str = "linear", fmt: str = "nvfp4") -> int:
+    return int(lib().ss_scale_bytes_fmt(rows, cols, SCALE_LAYOUTS[scale_layout], FORMATS[fmt][0]))
 
 
 def alloc_out(x, want_err=True, want_offsets=True, want_sums=True, want_g=True,
-              scale_layout: str = "linear", gmode: str = "tensor") -> QuantOut:
-    """Output buffers for ``x``: scales are [rows][cols/16] (linear) or the flat
-    swizzled tile buffer (ss_scale_bytes); G is [1], or [rows] for gmode 'row'."""
+              scale_layout: str = "linear", gmode: str = "tensor", fmt: str = "nvfp4") -> QuantOut:
+    """Output buffers for ``x`` in block format ``fmt``: codes [rows][cols/2]
+    (E2M1) or [rows][cols] (E2M3); scales [rows][cols/bs] (linear) or the flat
+    swizzled tile buffer; per-block errors/offsets; G [1] or [rows] (gmode 'row')."""
     import torch
     rows, cols = x.shape
-    nb = rows * cols // 16
+    _, bs, vbytes = FORMATS[fmt]
+    nsb = rows * cols // bs
     dev = x.device
-    scales = (torch.empty(rows, cols // 16, dtype=torch.uint8, device=dev)
+    scales = (torch.empty(rows, cols // bs, dtype=torch.uint8, device=dev)
               if scale_layout == "linear" else
-              torch.empty(scale_bytes(rows, cols, scale_layout), dtype=torch.uint8, device=dev))
+              torch.empty(scale_bytes(rows, cols, scale_layout, fmt), dtype=torch.uint8, device=dev))
     return QuantOut(
-        torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev),
+        torch.empty(rows, int(cols * vbytes), dtype=torch.uint8, device=dev),
         scales,
-        torch.empty(nb, 2, dtype=torch.float32, device=dev) if want_err else None,
-        torch.empty(nb, dtype=torch.int8, device=dev) if want_offsets else None,
+        torch.empty(nsb, 2, dtype=torch.float32, device=dev) if want_err else None,
+        torch.empty(nsb, dtype=torch.int8, device=dev) if want_offsets else None,
         torch.empty(2, dtype=torch.float64, device=dev) if want_sums else None,
         torch.empty(rows if gmode == "row" else 1, dtype=torch.float32, device=dev)
         if (want_g or gmode == "row") else None,
@@ -249,7 +262,7 @@ def alloc_out(x, want_err=True, want_offsets=True, want_sums=True, want_g=True,
 
 
 def quantize_batched(xs, outs, radius=None, fmin=None, fmax=None, gmode: str = "tensor",
-                     amax=None, scale_layout: str = "linear", stream=None):
+                     amax=None, scale_layout: str = "linear", fmt: str = "nvfp4", stream=None):
     """All tensors of ``xs`` into ``outs`` (QuantOut each) in one call
     (ss_quantize_nvfp4_batched).  ``amax``: device int32 [len(xs)] for
     gmode='device_amax' (e.g. after the NCCL max all-reduce)."""
@@ -267,8 +280,12 @@ def quantize_batched(xs, outs, radius=None, fmin=None, fmax=None, gmode: str = "
         arr[i] = TensorIO(_ptr(x), rows, cols, amax.data_ptr() + 4 * i if gm == 2 else None,
                           _ptr(o.codes), _ptr(o.scales), _ptr(o.err), _ptr(o.offsets), _ptr(o.sums),
                           _ptr(o.G), SCALE_LAYOUTS[scale_layout])
-    _check(lib().ss_quantize_nvfp4_batched(arr, n, lo, hi, gm, _stream_ptr(stream)),
-           "ss_quantize_nvfp4_batched")
+    if fmt == "nvfp4":
+        _check(lib().ss_quantize_nvfp4_batched(arr, n, lo, hi, gm, _stream_ptr(stream)),
+               "ss_quantize_nvfp4_batched")
+    else:
+        _check(lib().ss_quantize_batched_fmt(arr, n, lo, hi, gm, FORMATS[fmt][0], _stream_ptr(stream)),
+               "ss_quantize_batched_fmt")
     return outs
 
 
@@ -280,7 +297,7 @@ def quantize_simple(x, radius: int, gmode: str, codes, scales, err=None, stream=
 
 
 def dequantize(codes, scales, rows: int, cols: int, G=None, out=None, stream=None,
-               scale_layout: str = "linear"):
+               scale_layout: str = "linear", fmt: str = "nvfp4"):
     """bf16 [rows][cols] reconstruction (ss_dequantize_nvfp4_ex); G is a device
     f32 [1], a per-row [rows] (gmode 'row'), or None (G = 1)."""
     import torch
@@ -288,7 +305,7 @@ def dequantize(codes, scales, rows: int, cols: int, G=None, out=None, stream=Non
         out = torch.empty(rows, cols, dtype=torch.bfloat16, device=codes.device)
     per_row = G is not None and G.numel() == rows and rows > 1
     a = DequantArgs(_ptr(codes), _ptr(scales), rows, cols, _ptr(G), int(per_row),
-                    SCALE_LAYOUTS[scale_layout], _ptr(out), _stream_ptr(stream))
+                    SCALE_LAYOUTS[scale_layout], _ptr(out), _stream_ptr(stream), FORMATS[fmt][0])
     _check(lib().ss_dequantize_nvfp4_ex(ctypes.byref(a)), "ss_dequantize_nvfp4_ex")
     return out
 

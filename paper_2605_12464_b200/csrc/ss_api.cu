@@ -105,6 +105,19 @@ ss_status get_ws(int dev, void* stream, Workspace** out) {
   return SS_OK;
 }
 
+struct FmtInfo {
+  int vf, sf, bs;
+};
+bool fmt_info(int format, FmtInfo* f) {
+  switch (format) {
+    case SS_FMT_NVFP4: *f = {0, 0, 16}; return true;
+    case SS_FMT_MXFP4: *f = {0, 1, 32}; return true;
+    case SS_FMT_MXFP6_E2M3: *f = {1, 1, 32}; return true;
+    case SS_FMT_NVFP6_E2M3: *f = {1, 0, 16}; return true;
+    default: return false;
+  }
+}
+
 inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 ss_status launch_status() {
@@ -159,12 +172,18 @@ ss_status amax_launch(const void* const* in, const int64_t* n, uint32_t* out, in
 // ---- quantize kernel variants --------------------------------------------------
 typedef void (*QuantKernel)(QuantBatch);
 
-template <int NEG, int POS>
+template <int NEG, int POS, int FMT = ss::kFmtNVFP4>
 QuantKernel qk(bool ri) {
-  return ri ? ss::quant_kernel<NEG, POS, true> : ss::quant_kernel<NEG, POS, false>;
+  return ri ? ss::quant_kernel<NEG, POS, true, FMT> : ss::quant_kernel<NEG, POS, false, FMT>;
 }
 
-QuantKernel pick_kernel(int fmin, int fmax, bool ri) {
+QuantKernel pick_kernel(int fmin, int fmax, bool ri, int format) {
+  switch (format) {  // other formats: the runtime-window kernel
+    case SS_FMT_MXFP4: return qk<-1, -1, ss::kFmtMXFP4>(ri);
+    case SS_FMT_MXFP6_E2M3: return qk<-1, -1, ss::kFmtMXFP6E2M3>(ri);
+    case SS_FMT_NVFP6_E2M3: return qk<-1, -1, ss::kFmtNVFP6E2M3>(ri);
+    default: break;
+  }
   if (fmin == -fmax) {
     switch (fmax) {
 #define SS_SYM(R) case R: return qk<R, R>(ri);
@@ -212,8 +231,8 @@ int sums_grid(int sms) {
   return sms * occ;
 }
 
-ss_status validate_io(const ss_tensor_io& t, int gmode) {
-  if (t.rows < 0 || t.cols < 0 || (t.cols % 16) != 0) return SS_ERR_INVALID_ARG;
+ss_status validate_io(const ss_tensor_io& t, int gmode, const FmtInfo& f) {
+  if (t.rows < 0 || t.cols < 0 || (t.cols % f.bs) != 0) return SS_ERR_INVALID_ARG;
   const int64_t nb = t.rows * t.cols / 16;
   if (nb > 0 && (!t.in_bf16 || !t.out_codes || !t.out_scales)) return SS_ERR_INVALID_ARG;
   if (gmode == SS_GLOBAL_DEVICE_AMAX && !t.d_amax_bits) return SS_ERR_INVALID_ARG;
@@ -227,14 +246,14 @@ ss_status validate_io(const ss_tensor_io& t, int gmode) {
   return SS_OK;
 }
 
-int64_t scale_bytes(int64_t rows, int64_t cols, int layout) {
-  const int64_t nbr = cols / 16;
+int64_t scale_bytes(int64_t rows, int64_t cols, int layout, int bs = 16) {
+  const int64_t nbr = cols / bs;
   if (layout == SS_SCALE_SWIZZLED) return ((rows + 127) / 128) * ((nbr + 3) / 4) * 512;
   return rows * nbr;
 }
 
-void row_geometry(int64_t cols, uint32_t* nbr, uint32_t* magic, uint32_t* nkt) {
-  *nbr = (uint32_t)std::max<int64_t>(1, cols / 16);
+void row_geometry(int64_t cols, uint32_t* nbr, uint32_t* magic, uint32_t* nkt, int bs = 16) {
+  *nbr = (uint32_t)std::max<int64_t>(1, cols / bs);
   *magic = (uint32_t)(0xFFFFFFFFu / *nbr);
   *nkt = (*nbr + 3) / 4;
 }
@@ -253,13 +272,14 @@ int rows_grid(int sms) {
 }
 
 // Per-row global scales of every tensor into its d_global_scale (SS_GLOBAL_ROW).
-ss_status rowscale_launch(const ss_tensor_io* io, int count, uint32_t* flags, cudaStream_t st,
-                          int sms) {
+ss_status rowscale_launch(const ss_tensor_io* io, int count, uint32_t* flags, float numer,
+                          cudaStream_t st, int sms) {
   int i = 0;
   while (i < count) {
     ss::RowBatch b;
     std::memset(&b, 0, sizeof(b));
     b.flags = flags;
+    b.g_numer = numer;
     int64_t tasks = 0;
     for (; i < count && b.n < ss::kMaxTensors; i++) {
       if (io[i].rows * io[i].cols == 0) continue;
@@ -286,17 +306,22 @@ ss_status rowscale_launch(const ss_tensor_io* io, int count, uint32_t* flags, cu
 
 // The one quantization path behind every entry point.
 ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
-                        void* stream) {
+                        void* stream, int format = SS_FMT_NVFP4) {
+  FmtInfo fi;
+  if (!fmt_info(format, &fi)) return SS_ERR_INVALID_ARG;
   if (count < 0 || (count > 0 && !io)) return SS_ERR_INVALID_ARG;
   if (f_min > 0 || f_max < 0) return SS_ERR_INVALID_ARG;
   if (gmode < SS_GLOBAL_NONE || gmode > SS_GLOBAL_ROW) return SS_ERR_INVALID_ARG;
+  if (fi.sf == 1 && gmode != SS_GLOBAL_NONE) return SS_ERR_INVALID_ARG;  // UE8M0: no global scale
   for (int i = 0; i < count; i++)
-    if (ss_status s = validate_io(io[i], gmode)) return s;
+    if (ss_status s = validate_io(io[i], gmode, fi)) return s;
   int dev;
   DeviceInfo info;
   if (ss_status s = device_check(&dev, &info)) return s;
   if (count == 0) return SS_OK;
-  const int fmin = std::max(f_min, -126), fmax = std::min(f_max, 126);
+  const int lim = fi.sf ? 254 : 126;
+  const int fmin = std::max(f_min, -lim), fmax = std::min(f_max, lim);
+  const float numer = ss::global_numer(fi.vf);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
 
   std::lock_guard<std::mutex> lk(g_mu);
@@ -347,21 +372,21 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   } else if (gmode == SS_GLOBAL_DEVICE_AMAX) {
     for (int i = 0; i < count; i++) amax[i] = io[i].d_amax_bits;
   } else if (gmode == SS_GLOBAL_ROW) {
-    if (ss_status s = rowscale_launch(io, count, ws->flags, cs, info.sms)) return s;
+    if (ss_status s = rowscale_launch(io, count, ws->flags, numer, cs, info.sms)) return s;
   }
   // swizzled scales: zero the padding of partial 128x4 tiles first
   for (int i = 0; i < count; i++) {
     const ss_tensor_io& t = io[i];
     if (t.scale_layout == SS_SCALE_SWIZZLED && t.rows * t.cols > 0 &&
-        (t.rows % 128 != 0 || (t.cols / 16) % 4 != 0) &&
-        cudaMemsetAsync(t.out_scales, 0, (size_t)scale_bytes(t.rows, t.cols, t.scale_layout), cs) !=
+        (t.rows % 128 != 0 || (t.cols / fi.bs) % 4 != 0) &&
+        cudaMemsetAsync(t.out_scales, 0, (size_t)scale_bytes(t.rows, t.cols, t.scale_layout, fi.bs), cs) !=
             cudaSuccess)
       return SS_ERR_CUDA;
   }
 
   bool ri = gmode == SS_GLOBAL_ROW;
   for (int i = 0; i < count; i++) ri |= io[i].scale_layout == SS_SCALE_SWIZZLED;
-  QuantKernel k = pick_kernel(fmin, fmax, ri);
+  QuantKernel k = pick_kernel(fmin, fmax, ri, format);
   const int64_t slots = (int64_t)info.sms * occupancy(k);
   int i = 0;
   while (i < count) {
@@ -370,6 +395,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.fmin = fmin;
     b.fmax = fmax;
     b.gmode = gmode == SS_GLOBAL_NONE ? 0 : (gmode == SS_GLOBAL_ROW ? 2 : 1);
+    b.g_numer = numer;
     b.part1 = ws->part1;
     b.part2 = ws->part2;
     b.tick = ws->tick;
@@ -397,7 +423,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       q.amax = amax[i];
       q.g_row = gmode == SS_GLOBAL_ROW ? t.d_global_scale : nullptr;
       if (gmode == SS_GLOBAL_ROW) q.g_out = nullptr;
-      row_geometry(t.cols, &q.nbr, &q.nbr_magic, &q.nkt);
+      row_geometry(t.cols, &q.nbr, &q.nbr_magic, &q.nkt, fi.bs);
       q.swz = t.scale_layout == SS_SCALE_SWIZZLED;
       q.nb = nb;
       q.task0 = tk;
@@ -491,7 +517,7 @@ const char* ss_status_string(int s) {
   }
 }
 
-int ss_version(void) { return 300; }
+int ss_version(void) { return 400; }
 
 int64_t ss_scale_bytes(int64_t rows, int64_t cols, int scale_layout) {
   if (rows < 0 || cols < 0 || cols % 16 != 0) return -1;
@@ -540,7 +566,25 @@ ss_status ss_quantize_nvfp4(const void* in_bf16, int64_t rows, int64_t cols, int
 ss_status ss_quantize_nvfp4_ex(const ss_quant_args* a) {
   if (!a) return SS_ERR_INVALID_ARG;
   ss_tensor_io t = io_from_args(a);
-  return quantize_core(&t, 1, a->f_min, a->f_max, a->global_scale_mode, a->stream);
+  return quantize_core(&t, 1, a->f_min, a->f_max, a->global_scale_mode, a->stream, a->format);
+}
+
+ss_status ss_quantize_batched_fmt(const ss_tensor_io* tensors, int count, int f_min, int f_max,
+                                  int global_scale_mode, int format, void* stream) {
+  return quantize_core(tensors, count, f_min, f_max, global_scale_mode, stream, format);
+}
+
+int64_t ss_scale_bytes_fmt(int64_t rows, int64_t cols, int scale_layout, int format) {
+  FmtInfo f;
+  if (!fmt_info(format, &f) || rows < 0 || cols < 0 || cols % f.bs != 0) return -1;
+  if (scale_layout != SS_SCALE_LINEAR && scale_layout != SS_SCALE_SWIZZLED) return -1;
+  return scale_bytes(rows, cols, scale_layout, f.bs);
+}
+
+int64_t ss_code_bytes(int64_t rows, int64_t cols, int format) {
+  FmtInfo f;
+  if (!fmt_info(format, &f) || rows < 0 || cols < 0 || cols % f.bs != 0) return -1;
+  return f.vf ? rows * cols : rows * cols / 2;
 }
 
 ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min, int f_max,
@@ -550,7 +594,9 @@ ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int 
 
 ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {
   if (!a) return SS_ERR_INVALID_ARG;
-  if (a->rows < 0 || a->cols < 0 || a->cols % 16 != 0) return SS_ERR_INVALID_ARG;
+  FmtInfo fi;
+  if (!fmt_info(a->format, &fi)) return SS_ERR_INVALID_ARG;
+  if (a->rows < 0 || a->cols < 0 || a->cols % fi.bs != 0) return SS_ERR_INVALID_ARG;
   if (a->scale_layout != SS_SCALE_LINEAR && a->scale_layout != SS_SCALE_SWIZZLED)
     return SS_ERR_INVALID_ARG;
   const int64_t nb = a->rows * a->cols / 16;
@@ -563,17 +609,23 @@ ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {
   if (ss_status s = device_check(&dev, &info)) return s;
   if (nb == 0) return SS_OK;
   ss::DequantParams p;
-  p.codes = reinterpret_cast<const uint2*>(a->codes);
+  p.codes = a->codes;
   p.scales = a->scales;
   p.nb = nb;
   p.g = a->d_global_scale;
   p.g_per_row = a->g_per_row;
-  row_geometry(a->cols, &p.nbr, &p.nbr_magic, &p.nkt);
+  row_geometry(a->cols, &p.nbr, &p.nbr_magic, &p.nkt, fi.bs);
   p.swz = a->scale_layout == SS_SCALE_SWIZZLED;
   p.out = reinterpret_cast<uint4*>(a->out_bf16);
   int64_t want = (nb + 255) / 256;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)info.sms * 8));
-  ss::dequant_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(a->stream)>>>(p);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(a->stream);
+  switch (a->format) {
+    case SS_FMT_MXFP4: ss::dequant_kernel<ss::kFmtMXFP4><<<grid, 256, 0, cs>>>(p); break;
+    case SS_FMT_MXFP6_E2M3: ss::dequant_kernel<ss::kFmtMXFP6E2M3><<<grid, 256, 0, cs>>>(p); break;
+    case SS_FMT_NVFP6_E2M3: ss::dequant_kernel<ss::kFmtNVFP6E2M3><<<grid, 256, 0, cs>>>(p); break;
+    default: ss::dequant_kernel<ss::kFmtNVFP4><<<grid, 256, 0, cs>>>(p); break;
+  }
   return launch_status();
 }
 

@@ -35,9 +35,6 @@
 #ifndef SS_BPL
 #define SS_BPL 2         // NVFP4 blocks per lane per warp task
 #endif
-#ifndef SS_ILP
-#define SS_ILP 1         // blocks whose candidate loops are interleaved per lane (divides SS_BPL)
-#endif
 #ifndef SS_CILP
 #define SS_CILP 2        // candidates whose loss loops are interleaved (fixed windows)
 #endif
@@ -50,8 +47,6 @@ namespace ss {
 constexpr int kWarps = 8;                     // warps per CTA
 constexpr int kThreads = 32 * kWarps;
 constexpr int kBPL = SS_BPL;                  // NVFP4 blocks per lane per task
-constexpr int kILP = SS_ILP;                  // of which interleaved in registers
-static_assert(kBPL % kILP == 0, "SS_ILP must divide SS_BPL");
 constexpr int kTaskBlocks = 32 * kBPL;        // NVFP4 blocks per warp task
 constexpr int kTaskBytes = kTaskBlocks * 32;  // bf16 input bytes per task
 constexpr int kStages = kBPL >= 4 ? 2 : 4 / kBPL;  // per-warp smem buffers (tasks in flight)
@@ -63,6 +58,19 @@ constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk
 
 constexpr uint32_t kOneSixthBits = 0x3E2AAAABu;  // RN(1/6) (Alg. 1 line 2; R8)
 constexpr float kGlobalNumer = 2688.0f;          // 6 * 448: largest NVFP4 magnitude (R9)
+
+// Block formats: value format VF
+// (0 E2M1, 1 E2M3), scale format SF (0 UE4M3, 1 UE8M0, R19), block BS (16/32).
+enum : int { kFmtNVFP4 = 0, kFmtMXFP4 = 1, kFmtMXFP6E2M3 = 2, kFmtNVFP6E2M3 = 3 };
+template <int FMT>
+struct Fmt {
+  static constexpr int VF = (FMT == kFmtMXFP6E2M3 || FMT == kFmtNVFP6E2M3) ? 1 : 0;
+  static constexpr int SF = (FMT == kFmtMXFP4 || FMT == kFmtMXFP6E2M3) ? 1 : 0;
+  static constexpr int BS = SF ? 32 : 16;
+  static constexpr uint32_t kInvVmaxBits = VF ? 0x3E088889u : kOneSixthBits;  // RN(1/7.5), RN(1/6)
+  static constexpr int kMaxCode = SF ? 254 : 126;
+};
+__host__ __device__ constexpr float global_numer(int vf) { return vf ? 3360.0f : kGlobalNumer; }
 
 enum : uint32_t { kFlagNonFinite = 1u, kFlagRange = 2u };
 
@@ -117,6 +125,30 @@ __device__ __forceinline__ uint32_t e2m1_round_f16x2(float lo, float hi) {
       : "=r"(h) : "f"(lo), "f"(hi));
   return h;
 }
+// E2M3 codes of (lo, hi) -> f16x2 (q_lo, q_hi) (MXFP6 values).
+__device__ __forceinline__ uint32_t e2m3_round_f16x2(float lo, float hi) {
+  uint32_t h;
+  asm("{\n\t.reg .b16 q;\n\t"
+      "cvt.rn.satfinite.e2m3x2.f32 q, %2, %1;\n\t"
+      "cvt.rn.f16x2.e2m3x2 %0, q;\n\t}"
+      : "=r"(h) : "f"(lo), "f"(hi));
+  return h;
+}
+// Two E2M3 codes of (lo, hi), one per byte (lo in the low byte).
+__device__ __forceinline__ uint32_t e2m3_pack2(float lo, float hi) {
+  uint16_t q;
+  asm("cvt.rn.satfinite.e2m3x2.f32 %0, %2, %1;" : "=h"(q) : "f"(lo), "f"(hi));
+  return q;
+}
+// UE8M0 code of v >= 0: the smallest power of two >= v, saturating (R19).
+__device__ __forceinline__ uint32_t ue8m0_code(float v) {
+  uint16_t h;
+  asm("cvt.rp.satfinite.ue8m0x2.f32 %0, %1, %2;" : "=h"(h) : "f"(0.0f), "f"(v));
+  return h & 0xFFu;
+}
+// 2^(c - 127) for a UE8M0 code c (c = 0 is the subnormal 2^-127).
+__device__ __forceinline__ uint32_t ue8m0_bits(uint32_t c) { return c ? c << 23 : 0x00400000u; }
+
 // 8 E2M1 nibbles of 8 floats packed into one word, element 0 in the low nibble.
 __device__ __forceinline__ uint32_t e2m1_pack8(float v0, float v1, float v2, float v3,
                                                float v4, float v5, float v6, float v7) {
@@ -183,8 +215,20 @@ __device__ __forceinline__ void cp_async_wait() {
 // Entry = {rho, rho, (-s as f16) | code << 16, 0} with rho = RN(1/s) (R7);
 // code 0 has rho = 0 and -s = -0.
 // ---------------------------------------------------------------------------
-template <int Pad>
+// UE8M0 (SF = 1): one half of 255 + 2*Pad entries, code = clamp(k, 0, 254),
+// entry = {rho, rho, code << 16, bits(-s)} (every code is a scale, R19).
+template <int Pad, int SF>
 __device__ __forceinline__ void build_cand_table(uint4* tab) {
+  if constexpr (SF == 1) {
+    constexpr int TabW = 255 + 2 * Pad;
+    for (int i = threadIdx.x; i < TabW; i += blockDim.x) {
+      const int k = i - Pad;
+      const uint32_t code = (uint32_t)(k < 0 ? 0 : (k > 254 ? 254 : k));
+      const uint32_t rho = ue8m0_bits(254u - code);  // 2^(127 - c), exact
+      tab[i] = make_uint4(rho, rho, code << 16, ue8m0_bits(code) ^ 0x80000000u);
+    }
+    return;
+  }
   constexpr int TabW = 127 + 2 * Pad;
   for (int i = threadIdx.x; i < 2 * TabW; i += blockDim.x) {
     const int half = i / TabW;
@@ -205,14 +249,15 @@ __device__ __forceinline__ void build_cand_table(uint4* tab) {
 }
 
 // Global scale from the amax bit pattern (R9); flags non-finite / overflow.
-__device__ __forceinline__ float global_scale(uint32_t ab, uint32_t* flags, bool report) {
+__device__ __forceinline__ float global_scale(uint32_t ab, uint32_t* flags, bool report,
+                                              float numer = kGlobalNumer) {
   if (ab >= 0x7F800000u) {  // NaN / Inf in the input (R14)
     if (report) atomicOr(flags, kFlagNonFinite);
     return 1.0f;
   }
   const float A = __uint_as_float(ab);
   if (A == 0.0f) return 1.0f;
-  const float G = __fdiv_rn(kGlobalNumer, A);
+  const float G = __fdiv_rn(numer, A);
   if (!isfinite(G)) {
     if (report) atomicOr(flags, kFlagRange);
     return 1.0f;
@@ -262,6 +307,7 @@ struct QuantBatch {
   int n;                    // tensors in this launch
   int fmin, fmax;           // window (runtime loop variant only)
   int gmode;                // 0: G = 1; 1: G from t[i].amax; 2: per-row G from t[i].g_row
+  float g_numer;            // vmax * 448 (2688 for E2M1, 3360 for E2M3 values)
   int64_t ntasks;           // total tasks of the batch
   int64_t nsegs;            // total error-sum segments of the batch
   double2* part1;           // per task {sum best, sum base}   (when any sums wanted)
@@ -470,6 +516,45 @@ __device__ __forceinline__ void cand_loss_n(const uint64_t (&y2)[8], const float
   }
 }
 
+// Loss of one candidate for the 16 values of this lane in format FMT: the
+// NVFP4 sequence, E2M3 rounding for VF = 1, and for UE8M0 scales (s outside
+// f16) the residual as FFMA2 with q widened to f32.  A 32-element block adds
+// the two lanes' half losses, low half first (R20; FADD commutes bit-exactly).
+template <int FMT>
+__device__ __forceinline__ float block_loss(const uint64_t (&y2)[8], const float (&y)[16],
+                                            const uint4 e) {
+  using F = Fmt<FMT>;
+  float l;
+  if constexpr (FMT == kFmtNVFP4) {
+    l = cand_loss(y2, y, e);
+  } else {
+    const uint64_t rr = pack2u(e.x, e.y);
+    const uint16_t negs = (uint16_t)(e.z & 0xFFFFu);
+    const uint64_t ns2 = pack2u(e.w, e.w);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      float t0, t1;
+      unpack2(fmul2(y2[k], rr), t0, t1);
+      const uint32_t q = F::VF ? e2m3_round_f16x2(t0, t1) : e2m1_round_f16x2(t0, t1);
+      uint64_t d;
+      if constexpr (F::SF == 0) {
+        d = pack2(fhfma((uint16_t)(q & 0xFFFFu), negs, y[2 * k]),
+                  fhfma((uint16_t)(q >> 16), negs, y[2 * k + 1]));
+      } else {
+        const uint64_t qf = pack2(f16_to_f32((uint16_t)(q & 0xFFFFu)), f16_to_f32((uint16_t)(q >> 16)));
+        d = ffma2(qf, ns2, y2[k]);
+      }
+      acc = ffma2(d, d, acc);
+    }
+    float a, b;
+    unpack2(acc, a, b);
+    l = __fadd_rn(a, b);
+  }
+  if constexpr (Fmt<FMT>::BS == 32) l = __fadd_rn(l, __shfl_xor_sync(0xFFFFFFFFu, l, 1));
+  return l;
+}
+
 // Scan position i of a fixed window [-NEG, POS] (R4 order, see below):
 // i = 0 -> f = 0; 1..NEG -> f = -i; NEG+1.. -> f = i - NEG.
 template <int NEG>
@@ -482,42 +567,40 @@ __device__ __forceinline__ constexpr int scan_offset(int i) {
 // the smaller code), then f = 1, 2, ... with strict "<" (ties keep the
 // smaller code).  Clamped duplicates carry the same code, so they never
 // change the result.
-// Runtime-window updates: the same candidate offset f for the kILP blocks of
-// a lane (each with its own c0, table base, best and selection).
-#define SS_TAKE_LE_ILP(F)                                    \
-  _Pragma("unroll") for (int h = 0; h < kILP; h++) {         \
-    const uint4 e_ = base[h][F];                             \
-    const float l_ = cand_loss(y2[h], y[h], e_);             \
-    const bool t_ = l_ <= best[h];                           \
-    best[h] = t_ ? l_ : best[h];                             \
-    bsel[h] = t_ ? e_.z : bsel[h];                           \
-  }
-#define SS_TAKE_LT_ILP(F)                                    \
-  _Pragma("unroll") for (int h = 0; h < kILP; h++) {         \
-    const uint4 e_ = base[h][F];                             \
-    const float l_ = cand_loss(y2[h], y[h], e_);             \
-    const bool t_ = l_ < best[h];                            \
-    best[h] = t_ ? l_ : best[h];                             \
-    bsel[h] = t_ ? e_.z : bsel[h];                           \
+// Runtime-window updates (scan order of R4, see above).
+#define SS_TAKE(F, CMP)                                      \
+  {                                                          \
+    const uint4 e_ = base[F];                                \
+    const float l_ = block_loss<FMT>(y2, y, e_);             \
+    const bool t_ = l_ CMP best;                             \
+    best = t_ ? l_ : best;                                   \
+    bsel = t_ ? e_.z : bsel;                                 \
   }
 
 // NEG/POS >= 0: compile-time window [-NEG, POS]; NEG < 0: runtime [fmin, fmax].
 // RI: the batch needs each block's row (per-row G or the swizzled scale
-// layout); without it those per-block steps are compiled out.
-template <int NEG, int POS, bool RI>
+// layout); without it those per-block steps are compiled out.  FMT: block
+// format (Fmt<>); fixed windows (NEG >= 0) exist for NVFP4 only.  Units:
+// `b`/`j` index 16-element HALF-blocks (one per lane); a 32-element block is
+// the lane pair (2i, 2i + 1), whose even lane writes its scale, offset and
+// errors.
+template <int NEG, int POS, bool RI, int FMT>
 __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
-  constexpr int Pad = NEG < 0 ? 126 : (NEG > POS ? NEG : POS);
-  constexpr int TabW = 127 + 2 * Pad;
-  __shared__ __align__(16) uint4 tab[2 * TabW];
+  using F = Fmt<FMT>;
+  static_assert(FMT == kFmtNVFP4 || NEG < 0, "fixed windows are compiled for NVFP4 only");
+  constexpr int Pad = NEG < 0 ? F::kMaxCode : (NEG > POS ? NEG : POS);
+  constexpr int TabW = F::SF ? 255 + 2 * Pad : 127 + 2 * Pad;
+  constexpr int kHalves = F::BS / 16;  // lanes per scale block
+  __shared__ __align__(16) uint4 tab[F::SF ? TabW : 2 * TabW];
   __shared__ __align__(128) uint4 buf[kWarps][kStages][kTaskBytes / 16];
 
-  build_cand_table<Pad>(tab);
+  build_cand_table<Pad, F::SF>(tab);
   __syncthreads();
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWarps + w;
 
-  const float k6 = __uint_as_float(kOneSixthBits);
+  const float kinv = __uint_as_float(F::kInvVmaxBits);  // RN(1 / vmax) (R8)
   // Stage s of this warp holds one task.  Lane l copies its own blocks
   // l, l+32, ... (2 x 16-B LDGSTS each) and later reads back only what it
   // copied, so no cross-lane sync is needed; one commit group per stage
@@ -539,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   };
   auto gscale = [&](int ti, bool report) -> float {
     if (p.gmode != 1) return 1.0f;  // 0: G = 1; 2: per-row G, read per block
-    return global_scale(__ldg(p.t[ti].amax), p.flags, report);
+    return global_scale(__ldg(p.t[ti].amax), p.flags, report, p.g_numer);
   };
   // Dynamic scheduling: counter c hands out tasks c, c + kCounters, ... ; warp
   // gw draws from counter gw % kCounters, so warps the arbiter favours simply
@@ -592,133 +675,123 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
 
     cp_async_wait<kStages - 1>();  // this lane's copies of stage s have landed
-    uint2* codes = T.codes + b0;
-    uint8_t* scales = T.scales + b0;
-    int8_t* offsets = T.offsets ? T.offsets + b0 : nullptr;
-    float2* err = T.err ? T.err + b0 : nullptr;
+    int8_t* offsets = T.offsets ? T.offsets + b0 / kHalves : nullptr;
+    float2* err = T.err ? T.err + b0 / kHalves : nullptr;
     double sb = 0.0, sc = 0.0;
     const uint64_t GG = pack2(G, G);
 
 #pragma unroll 1
-    for (int u0 = 0; u0 < kBPL; u0 += kILP) {
-      float y[kILP][16];
-      uint64_t y2[kILP][8];
-      int c0[kILP];
-      const uint4* base[kILP];
-      uint32_t row[kILP];
-#pragma unroll
-      for (int h = 0; h < kILP; h++) {
-        const int j = (u0 + h) * 32 + lane;
-        // row of the block: per-row global scale and swizzled scale layout
-        row[h] = 0;
-        uint64_t Gb = GG;
-        if (RI && (T.g_row || T.swz)) {  // warp-uniform
-          const uint32_t b = (uint32_t)(b0 + min(j, nblk - 1));
-          row[h] = div_rows(b, T.nbr, T.nbr_magic);
-          if (T.g_row) {
-            const float gr = __ldg(T.g_row + row[h]);
-            Gb = pack2(gr, gr);
-          }
+    for (int u = 0; u < kBPL; u++) {
+      const int j = u * 32 + lane;          // half-block within the task
+      const bool active = j < nblk;
+      const bool writer = kHalves == 1 || (lane & 1) == 0;  // owns the scale block
+      // scale-block index within the tensor; its row (per-row G, swizzled layout)
+      const uint32_t sbk = (uint32_t)(b0 + min(j, nblk - 1)) / kHalves;
+      uint32_t row = 0;
+      uint64_t Gb = GG;
+      if (RI && (T.g_row || T.swz)) {  // warp-uniform
+        row = div_rows(sbk, T.nbr, T.nbr_magic);
+        if (T.g_row) {
+          const float gr = __ldg(T.g_row + row);
+          Gb = pack2(gr, gr);
         }
-        // a1 + a3: bf16 -> f32 is exact; y = RN(x * G)
-        const uint4 v0 = buf[w][s][2 * j], v1 = buf[w][s][2 * j + 1];
-        const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          y2[h][k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), Gb);
-          unpack2(y2[h][k], y[h][2 * k], y[h][2 * k + 1]);
-        }
-        // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
-        float m = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[h][i]));
-        c0[h] = (int)e4m3_code(__fmul_rn(m, k6));
-        base[h] = tab + (c0[h] ? TabW : 0) + Pad + c0[h];
       }
+      // a1 + a3: bf16 -> f32 is exact; y = RN(x * G)
+      const uint4 v0 = buf[w][s][2 * j], v1 = buf[w][s][2 * j + 1];
+      const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      float y[16];
+      uint64_t y2[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        y2[k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), Gb);
+        unpack2(y2[k], y[2 * k], y[2 * k + 1]);
+      }
+      // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
+      float m = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[i]));
+      if constexpr (kHalves == 2) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 1));
+      const float v = __fmul_rn(m, kinv);
+      const int c0 = F::SF ? (int)ue8m0_code(v) : (int)e4m3_code(v);
+      const uint4* base = F::SF ? tab + Pad + c0 : tab + (c0 ? TabW : 0) + Pad + c0;
 
       // a5 + a6: candidate search (Alg. 1 lines 5-10)
-      float best[kILP], loss0[kILP];
-      uint32_t bsel[kILP];
+      float best, loss0;
+      uint32_t bsel;
       if constexpr (NEG >= 0) {
         // scan positions 0 .. NEG+POS in chunks of CI interleaved candidates;
         // the selection updates are applied in scan order afterwards
         constexpr int NC = 1 + NEG + POS;
         constexpr int CI = SS_CILP < NC ? SS_CILP : NC;
 #pragma unroll
-        for (int h = 0; h < kILP; h++) {
+        for (int i0 = 0; i0 < NC; i0 += CI) {
+          uint4 e[CI];
+          float l[CI];
 #pragma unroll
-          for (int i0 = 0; i0 < NC; i0 += CI) {
-            uint4 e[CI];
-            float l[CI];
+          for (int c = 0; c < CI; c++) e[c] = base[scan_offset<NEG>(i0 + c < NC ? i0 + c : NC - 1)];
+          cand_loss_n<CI>(y2, y, e, l);
 #pragma unroll
-            for (int c = 0; c < CI; c++)
-              e[c] = base[h][scan_offset<NEG>(i0 + c < NC ? i0 + c : NC - 1)];
-            cand_loss_n<CI>(y2[h], y[h], e, l);
-#pragma unroll
-            for (int c = 0; c < CI; c++) {
-              const int i = i0 + c;
-              if (i >= NC) break;
-              if (i == 0) {
-                best[h] = l[c];
-                loss0[h] = l[c];  // err_base: the max-abs scale (f = 0)
-                bsel[h] = e[c].z;
-              } else {
-                const bool t_ = i <= NEG ? l[c] <= best[h] : l[c] < best[h];
-                best[h] = t_ ? l[c] : best[h];
-                bsel[h] = t_ ? e[c].z : bsel[h];
-              }
+          for (int c = 0; c < CI; c++) {
+            const int i = i0 + c;
+            if (i >= NC) break;
+            if (i == 0) {
+              best = l[c];
+              loss0 = l[c];  // err_base: the max-abs scale (f = 0)
+              bsel = e[c].z;
+            } else {
+              const bool t_ = i <= NEG ? l[c] <= best : l[c] < best;
+              best = t_ ? l[c] : best;
+              bsel = t_ ? e[c].z : bsel;
             }
           }
         }
       } else {
-#pragma unroll
-        for (int h = 0; h < kILP; h++) {
-          best[h] = cand_loss(y2[h], y[h], base[h][0]);
-          loss0[h] = best[h];  // err_base: the max-abs scale (f = 0)
-          bsel[h] = base[h][0].z;
-        }
+        best = block_loss<FMT>(y2, y, base[0]);
+        loss0 = best;  // err_base: the max-abs scale (f = 0)
+        bsel = base[0].z;
         // runtime window; skip offsets that are clamped duplicates for every lane
-        int cmin = c0[0], cmax = c0[0];
-#pragma unroll
-        for (int h = 1; h < kILP; h++) {
-          cmin = min(cmin, c0[h]);
-          cmax = max(cmax, c0[h]);
-        }
-        const int lo = __reduce_min_sync(0xFFFFFFFFu, (cmax ? 1 : 0) - cmax);
-        const int hi = __reduce_max_sync(0xFFFFFFFFu, 126 - cmin);
+        const int lo = __reduce_min_sync(0xFFFFFFFFu, F::SF ? -c0 : (c0 ? 1 : 0) - c0);
+        const int hi = __reduce_max_sync(0xFFFFFFFFu, F::kMaxCode - c0);
         const int fneg = max(p.fmin, lo), fpos = min(p.fmax, hi);
 #pragma unroll 1
-        for (int f = -1; f >= fneg; f--) SS_TAKE_LE_ILP(f)
+        for (int f = -1; f >= fneg; f--) SS_TAKE(f, <=)
 #pragma unroll 1
-        for (int f = 1; f <= fpos; f++) SS_TAKE_LT_ILP(f)
+        for (int f = 1; f <= fpos; f++) SS_TAKE(f, <)
       }
 
-      // a7: emit the winner: nibbles of t = y * rho*, scale byte, offset, errors
+      // a7: emit the winner: codes of t = y * rho*, scale byte, offset, errors
+      const uint32_t code = bsel >> 16;
+      const float rs = __uint_as_float(
+          (F::SF ? tab[Pad + code] : tab[(code ? TabW : 0) + Pad + code]).x);
+      const uint64_t rr = pack2(rs, rs);
+      float t[16];
 #pragma unroll
-      for (int h = 0; h < kILP; h++) {
-        const int j = (u0 + h) * 32 + lane;
-        const bool active = j < nblk;
-        const uint32_t code = bsel[h] >> 16;
-        const float rs = __uint_as_float(tab[(code ? TabW : 0) + Pad + code].x);
-        const uint64_t rr = pack2(rs, rs);
-        float t[16];
+      for (int k = 0; k < 8; k++) unpack2(fmul2(y2[k], rr), t[2 * k], t[2 * k + 1]);
+      if (active) {
+        const int64_t hb = b0 + j;  // half-block index within the tensor
+        if constexpr (F::VF == 0) {
+          uint2 cw;
+          cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+          cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
+          __stcs(T.codes + hb, cw);
+        } else {  // E2M3: one code per byte
+          uint32_t cw[4];
 #pragma unroll
-        for (int k = 0; k < 8; k++) unpack2(fmul2(y2[h][k], rr), t[2 * k], t[2 * k + 1]);
-        uint2 cw;
-        cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
-        cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
-        if (active) {
-          __stcs(codes + j, cw);
+          for (int k = 0; k < 4; k++)
+            cw[k] = e2m3_pack2(t[4 * k], t[4 * k + 1]) | (e2m3_pack2(t[4 * k + 2], t[4 * k + 3]) << 16);
+          __stcs(reinterpret_cast<uint4*>(T.codes) + hb, make_uint4(cw[0], cw[1], cw[2], cw[3]));
+        }
+        if (writer) {
           if (!RI || !T.swz) {
-            scales[j] = (uint8_t)code;
+            T.scales[sbk] = (uint8_t)code;
           } else {
-            const uint32_t b = (uint32_t)(b0 + j);
-            T.scales[swizzled_scale_offset(row[h], b - row[h] * T.nbr, T.nkt)] = (uint8_t)code;
+            T.scales[swizzled_scale_offset(row, sbk - row * T.nbr, T.nkt)] = (uint8_t)code;
           }
-          if (offsets) offsets[j] = (int8_t)((int)code - c0[h]);
-          if (err) __stcs(err + j, make_float2(best[h], loss0[h]));
-          sb += (double)best[h];
-          sc += (double)loss0[h];
+          const int jb = j / kHalves;  // scale block within the task
+          if (offsets) offsets[jb] = (int8_t)((int)code - c0);
+          if (err) __stcs(err + jb, make_float2(best, loss0));
+          sb += (double)best;
+          sc += (double)loss0;
         }
       }
     }
@@ -776,6 +849,7 @@ struct RowBatch {
   int n;
   int64_t ntasks;
   uint32_t* flags;
+  float g_numer;
   RTensor t[kMaxTensors];
 };
 
@@ -800,7 +874,7 @@ __global__ void __launch_bounds__(kThreads) rowscale_kernel(const __grid_constan
     }
     uint32_t mx = max(m & 0xFFFFu, m >> 16);
     for (int o = lpr >> 1; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    if (sub == 0 && r < T.rows) T.g_row[r] = global_scale(mx << 16, p.flags, true);
+    if (sub == 0 && r < T.rows) T.g_row[r] = global_scale(mx << 16, p.flags, true, p.g_numer);
   }
 }
 
@@ -808,48 +882,69 @@ __global__ void __launch_bounds__(kThreads) rowscale_kernel(const __grid_constan
 // Dequantize kernel: xhat = RNE_bf16(RN((q * s) / G)).
 // ---------------------------------------------------------------------------
 struct DequantParams {
-  const uint2* codes;
+  const uint8_t* codes;     // E2M1: 8 B per 16 elements; E2M3: 16 B per 16 elements
   const uint8_t* scales;
-  int64_t nb;
+  int64_t nb;               // 16-element half-blocks
   const float* g;           // nullable: G = 1; per tensor [1] or per row [rows]
   int g_per_row;
-  uint32_t nbr, nbr_magic, nkt;
+  uint32_t nbr, nbr_magic, nkt;  // scale blocks per row
   int swz;                  // scale layout (0 linear, 1 swizzled)
   uint4* out;
 };
 
+// xhat = RNE_bf16(RN((q * s) / G)) per element, any format (FMT).
+template <int FMT>
 __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DequantParams p) {
+  using F = Fmt<FMT>;
+  constexpr int kHalves = F::BS / 16;
   const float G0 = (p.g && !p.g_per_row) ? *p.g : 1.0f;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < p.nb;
        b += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 cw = __ldcs(p.codes + b);
+    const uint32_t sbk = (uint32_t)(b / kHalves);
     float G = G0;
     uint8_t sc;
     if (p.g_per_row || p.swz) {
-      const uint32_t r = div_rows((uint32_t)b, p.nbr, p.nbr_magic);
+      const uint32_t r = div_rows(sbk, p.nbr, p.nbr_magic);
       if (p.g_per_row) G = p.g[r];
-      sc = p.swz ? p.scales[swizzled_scale_offset(r, (uint32_t)b - r * p.nbr, p.nkt)] : p.scales[b];
+      sc = p.swz ? p.scales[swizzled_scale_offset(r, sbk - r * p.nbr, p.nkt)] : p.scales[sbk];
     } else {
-      sc = p.scales[b];
+      sc = p.scales[sbk];
     }
-    const float s = f16_to_f32(e4m3_to_f16(sc));
-    uint32_t o[8];
-    const uint32_t words[2] = {cw.x, cw.y};
+    const float s = F::SF ? __uint_as_float(ue8m0_bits(sc)) : f16_to_f32(e4m3_to_f16(sc));
+    float q[16];
+    if constexpr (F::VF == 0) {
+      const uint2 cw = __ldcs(reinterpret_cast<const uint2*>(p.codes) + b);
+      const uint32_t words[2] = {cw.x, cw.y};
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        uint32_t q;
+      for (int k = 0; k < 8; k++) {
+        uint32_t h;
         asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t"
             "mov.b32 {b0, b1, b2, b3}, %1;\n\t"
             "cvt.rn.f16x2.e2m1x2 %0, b0;\n\t}"
-            : "=r"(q) : "r"(words[h] >> (8 * k)));
-        const float x0 = __fdiv_rn(__fmul_rn(f16_to_f32((uint16_t)(q & 0xFFFFu)), s), G);
-        const float x1 = __fdiv_rn(__fmul_rn(f16_to_f32((uint16_t)(q >> 16)), s), G);
-        uint32_t r;
-        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x1), "f"(x0));
-        o[h * 4 + k] = r;
+            : "=r"(h) : "r"(words[k >> 2] >> (8 * (k & 3))));
+        q[2 * k] = f16_to_f32((uint16_t)(h & 0xFFFFu));
+        q[2 * k + 1] = f16_to_f32((uint16_t)(h >> 16));
       }
+    } else {
+      const uint4 cw = __ldcs(reinterpret_cast<const uint4*>(p.codes) + b);
+      const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        uint32_t h;
+        asm("{\n\t.reg .b16 c;\n\tcvt.u16.u32 c, %1;\n\tcvt.rn.f16x2.e2m3x2 %0, c;\n\t}"
+            : "=r"(h) : "r"(words[k >> 1] >> (16 * (k & 1))));
+        q[2 * k] = f16_to_f32((uint16_t)(h & 0xFFFFu));
+        q[2 * k + 1] = f16_to_f32((uint16_t)(h >> 16));
+      }
+    }
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const float x0 = __fdiv_rn(__fmul_rn(q[2 * k], s), G);
+      const float x1 = __fdiv_rn(__fmul_rn(q[2 * k + 1], s), G);
+      uint32_t r;
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x1), "f"(x0));
+      o[k] = r;
     }
     __stcs(p.out + 2 * b, make_uint4(o[0], o[1], o[2], o[3]));
     __stcs(p.out + 2 * b + 1, make_uint4(o[4], o[5], o[6], o[7]));

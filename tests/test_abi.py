@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_status_strings(L):
-    assert L.ss_version() == 300
+    assert L.ss_version() == 400
     for s in range(7):
         assert L.ss_status_string(s)
     assert L.ss_status_string(6).decode().startswith("unsupported device")
