@@ -39,13 +39,18 @@ def med(ts):
     return ts[len(ts) // 2]
 
 
-def measure(torch, ss, groups, fmin, fmax, reps=5):
+def measure(torch, ss, groups, fmin, fmax, reps=5, fmt="nvfp4"):
     """groups: list of tensor lists (rotated between runs).  Returns timings and stats."""
-    outs = [[ss.alloc_out(x) for x in g] for g in groups]
+    outs = [[ss.alloc_out(x, fmt=fmt) for x in g] for g in groups]
     amax = [torch.zeros(len(g), dtype=torch.int32, device=g[0].device) for g in groups]
+    mx = fmt.startswith("mx")              # UE8M0 scales: no global scale (R19)
 
     def q_only(i):
-        ss.quantize_batched(groups[i], outs[i], fmin=fmin, fmax=fmax, gmode="device_amax", amax=amax[i])
+        if mx:
+            ss.quantize_batched(groups[i], outs[i], fmin=fmin, fmax=fmax, gmode="none", fmt=fmt)
+        else:
+            ss.quantize_batched(groups[i], outs[i], fmin=fmin, fmax=fmax, gmode="device_amax",
+                                amax=amax[i], fmt=fmt)
 
     def e2e(i):
         ss.tensor_amax_batched(groups[i], out=amax[i])
@@ -76,12 +81,17 @@ def measure(torch, ss, groups, fmin, fmax, reps=5):
         c0 = oo.scales.reshape(-1).to(torch.int32) - oo.offsets.to(torch.int32)
         # valid candidates of a block: f in [fmin, fmax] with 1 <= c0 + f <= 126,
         # plus the zero-scale candidate when c0 == 0 (R2, R3)
-        hi = torch.clamp(126 - c0, max=fmax)
-        lo = torch.clamp(1 - c0, min=fmin)
-        valid = torch.clamp(hi - lo + 1, min=0) + (c0 == 0).to(torch.int32)
+        if mx:     # every UE8M0 code 0..254 is a scale
+            hi = torch.clamp(254 - c0, max=fmax)
+            lo = torch.clamp(-c0, min=fmin)
+            valid = torch.clamp(hi - lo + 1, min=0)
+        else:
+            hi = torch.clamp(126 - c0, max=fmax)
+            lo = torch.clamp(1 - c0, min=fmin)
+            valid = torch.clamp(hi - lo + 1, min=0) + (c0 == 0).to(torch.int32)
         tot_valid += int(valid.sum())
         tot_blocks += c0.numel()
-        G2 = float(oo.G.item()) ** 2
+        G2 = 1.0 if mx else float(oo.G.item()) ** 2
         s = oo.sums.cpu().tolist()
         s_best += s[0] / G2
         s_base += s[1] / G2
@@ -92,14 +102,20 @@ def measure(torch, ss, groups, fmin, fmax, reps=5):
     return res, n, tot_valid / max(tot_blocks, 1), s_best, s_base, {str(k - 126): v for k, v in enumerate(h) if v}
 
 
-def report(cfg, fmin, fmax, res, n, ceff, s_best, s_base, hist, hbm, mhz, extra=None):
+# bytes per element written+read by the quantize kernel: bf16 in + codes +
+# scales + float2 errors per scale block
+FMT_BYTES = {"nvfp4": 2 + 0.5 + 1 / 16 + 8 / 16, "mxfp4": 2 + 0.5 + 1 / 32 + 8 / 32,
+             "mxfp6_e2m3": 2 + 1 + 1 / 32 + 8 / 32, "nvfp6_e2m3": 2 + 1 + 1 / 16 + 8 / 16}
+
+
+def report(cfg, fmin, fmax, res, n, ceff, s_best, s_base, hist, hbm, mhz, extra=None, fmt="nvfp4"):
     alu_peak = 148 * 128 * mhz * 1e6
     tq = res["quant"] * 1e-3
     te = res["amax_quant"] * 1e-3
     ops = (4.0 * ceff + 2.0) * n
-    bytes_q = 3.0625 * n
+    bytes_q = FMT_BYTES[fmt] * n
     t_roof = max(bytes_q / (hbm * 1e9), ops / alu_peak)
-    line = {"config": cfg, "window": [fmin, fmax], "elements": n, "c_eff": ceff,
+    line = {"config": cfg, "format": fmt, "window": [fmin, fmax], "elements": n, "c_eff": ceff,
             "quant_ms": res["quant"], "amax_quant_ms": res["amax_quant"],
             "quant_bf16_gbs": 2 * n / tq / 1e9, "e2e_bf16_gbs": 2 * n / te / 1e9,
             "bound": "alu" if ops / alu_peak > bytes_q / (hbm * 1e9) else "hbm",
@@ -120,7 +136,7 @@ def main():
     import ssgen
     import paper_2605_12464_b200 as ss
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--configs", default="c1,c2,c3,c4,c5,formats")
     ap.add_argument("--c5-gib", default="1,8")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -166,6 +182,15 @@ def main():
                                     *measure(torch, ss, [xs], -r, r, reps=3), hbm, mhz))
             del xs
             torch.cuda.empty_cache()
+    if "formats" in cfgs:   # other block formats on C5 (1 GiB Gaussian)
+        xs = gen(ssgen.workload("c5_gauss_1gib"))
+        for fmt, radii in (("mxfp4", [0, 1, 2]), ("mxfp6_e2m3", [0, 1, 2]),
+                           ("nvfp6_e2m3", [0, 1, 2, 8]), ("nvfp4", [0, 8])):
+            for r in radii:
+                lines.append(report("c5_gauss_1gib", -r, r, *measure(torch, ss, [xs], -r, r, reps=3, fmt=fmt),
+                                    hbm, mhz, fmt=fmt))
+        del xs
+        torch.cuda.empty_cache()
     if a.out:
         with open(a.out, "w") as f:
             for ln in lines:
