@@ -341,3 +341,30 @@ def test_cuda_graph_capture_and_replay(ss, oracle_lib):
     for x, o in zip(xs, outs):
         ref = oracle_lib.quantize(x, *x.shape, -8, 8, "tensor")
         _cmp(o, ref, *x.shape)
+
+
+def test_bench_launch_configuration_c2_sampled(ss, oracle_lib):
+    # bench.py's step exactly: all 252 Qwen3-8B matrices through the row-shard
+    # driver (world 1: one batched amax + batched quantize launches of 128
+    # tensors), then sampled rows of several tensors against the oracle.
+    from paper_2605_12464_b200.dist import CudaOps, RowShardQuantizer, ShardPlan
+    specs = ssgen.workload("c2_qwen3_8b_weights")
+    xs = [ssgen.generate(s.kind, s.rows, s.cols, seed=ssgen.workloads.BASE_SEED, tid=s.tid,
+                         device="cuda") for s in specs]
+    ops = CudaOps(-8, 8, want_err=True, want_sums=True)
+    outs = [ops.alloc_out(x) for x in xs]
+    q = RowShardQuantizer(ShardPlan([(s.rows, s.cols) for s in specs], 0, 1), ops, device="cuda")
+    assert q.step(xs, outs) == 2 + 2 * 2      # amax x2, quant x2, sums x2
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(11)
+    for k in (0, 4, 127, 128, 200, 251):      # both launches, several shapes
+        spec, x, o = specs[k], xs[k].cpu(), outs[k]
+        amax = oracle_lib.tensor_amax(x)
+        rows = np.unique(np.concatenate([[0, spec.rows - 1], rng.integers(0, spec.rows, 8)]))
+        sub = x[torch.from_numpy(rows)].contiguous()
+        ref = oracle_lib.quantize(sub, len(rows), spec.cols, -8, 8, "given", amax_bits=amax)
+        r_t = torch.from_numpy(rows).cuda()
+        assert np.array_equal(o.codes[r_t].cpu().numpy(), ref.codes)
+        assert np.array_equal(o.scales[r_t].cpu().numpy(), ref.scales)
+        assert o.G.item() == np.float32(ref.G)
+    del xs, outs
