@@ -52,6 +52,7 @@ constexpr int kTaskBytes = kTaskBlocks * 32;  // bf16 input bytes per task
 constexpr int kStages = kBPL >= 4 ? 2 : 4 / kBPL;  // per-warp smem buffers (tasks in flight)
 constexpr int kSegTasks = 4096;               // tasks per CTA of the error-sum kernel
 constexpr int kCounters = 256;                // task counters of the dynamic scheduler
+constexpr int kPruneFrom = 3;                 // exact pruning for offsets f <= -kPruneFrom
 constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
 constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
 constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk (32 KiB)
@@ -555,18 +556,49 @@ __device__ __forceinline__ float block_loss(const uint64_t (&y2)[8], const float
   return l;
 }
 
-// Scan position i of a fixed window [-NEG, POS] (R4 order, see below):
-// i = 0 -> f = 0; 1..NEG -> f = -i; NEG+1.. -> f = i - NEG.
-template <int NEG>
-__device__ __forceinline__ constexpr int scan_offset(int i) {
-  return i == 0 ? 0 : (i <= NEG ? -i : i - NEG);
+// Exact lower bound of a candidate's computed loss: RN(d^2) of the block's
+// max-magnitude element (|y| = m), computed with the same instructions as its
+// term of the loss.  Each FMA step adds a non-negative value and RN is
+// monotone, so the computed loss >= RN(d_j^2) for every element j; a
+// candidate whose bound exceeds the incumbent can never be selected, and
+// skipping it changes no output bit.
+template <int FMT>
+__device__ __forceinline__ float cand_lb(float m, const uint4 e) {
+  using F = Fmt<FMT>;
+  const float t = __fmul_rn(m, __uint_as_float(e.x));
+  const uint32_t q = F::VF ? e2m3_round_f16x2(t, t) : e2m1_round_f16x2(t, t);
+  float d;
+  if constexpr (F::SF == 0) {
+    d = fhfma((uint16_t)(q & 0xFFFFu), (uint16_t)(e.z & 0xFFFFu), m);
+  } else {
+    d = __fmaf_rn(f16_to_f32((uint16_t)(q & 0xFFFFu)), __uint_as_float(e.w), m);
+  }
+  return __fmul_rn(d, d);
 }
 
 // Candidate order (equivalent to Alg. 1's ascending strict-< scan, R4): f = 0
-// first (it is also err_base), then f = -1, -2, ... with "<=" (ties move to
-// the smaller code), then f = 1, 2, ... with strict "<" (ties keep the
-// smaller code).  Clamped duplicates carry the same code, so they never
-// change the result.
+// first (it is also err_base), then f = 1, 2, ... with strict "<" (ties keep
+// the smaller code), then f = -1, -2, ... with "<=" (a tie moves to the
+// smaller code; smaller codes always come later in this order).  Clamped
+// duplicates carry the same code, so they never change the result.  The
+// negative side runs last because the incumbent is then final or nearly so:
+// a warp skips a negative candidate when no lane's cand_lb reaches it.
+// Negative-side update with exact pruning (cand_lb, warp vote).
+#ifndef SS_NO_PRUNE
+#define SS_TAKE_NEG(F)                                                   \
+  {                                                                      \
+    const uint4 e_ = base[F];                                            \
+    if (__any_sync(0xFFFFFFFFu, cand_lb<FMT>(m, e_) <= best)) {          \
+      const float l_ = block_loss<FMT>(y2, y, e_);                       \
+      const bool t_ = l_ <= best;                                        \
+      best = t_ ? l_ : best;                                             \
+      bsel = t_ ? e_.z : bsel;                                           \
+    }                                                                    \
+  }
+#else
+#define SS_TAKE_NEG(F) SS_TAKE(F, <=)
+#endif
+
 // Runtime-window updates (scan order of R4, see above).
 #define SS_TAKE(F, CMP)                                      \
   {                                                          \
@@ -719,16 +751,16 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       float best, loss0;
       uint32_t bsel;
       if constexpr (NEG >= 0) {
-        // scan positions 0 .. NEG+POS in chunks of CI interleaved candidates;
-        // the selection updates are applied in scan order afterwards
-        constexpr int NC = 1 + NEG + POS;
+        // f = 0, 1, ..., POS in chunks of CI interleaved candidates (the
+        // selection updates applied in scan order), then the negative side
+        constexpr int NC = 1 + POS;
         constexpr int CI = SS_CILP < NC ? SS_CILP : NC;
 #pragma unroll
         for (int i0 = 0; i0 < NC; i0 += CI) {
           uint4 e[CI];
           float l[CI];
 #pragma unroll
-          for (int c = 0; c < CI; c++) e[c] = base[scan_offset<NEG>(i0 + c < NC ? i0 + c : NC - 1)];
+          for (int c = 0; c < CI; c++) e[c] = base[i0 + c < NC ? i0 + c : NC - 1];
           cand_loss_n<CI>(y2, y, e, l);
 #pragma unroll
           for (int c = 0; c < CI; c++) {
@@ -739,10 +771,18 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
               loss0 = l[c];  // err_base: the max-abs scale (f = 0)
               bsel = e[c].z;
             } else {
-              const bool t_ = i <= NEG ? l[c] <= best : l[c] < best;
+              const bool t_ = l[c] < best;
               best = t_ ? l[c] : best;
               bsel = t_ ? e[c].z : bsel;
             }
+          }
+        }
+#pragma unroll
+        for (int f = 1; f <= NEG; f++) {
+          if (f < kPruneFrom) {  // near offsets almost never prune for a whole warp
+            SS_TAKE(-f, <=)
+          } else {
+            SS_TAKE_NEG(-f)
           }
         }
       } else {
@@ -754,9 +794,15 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         const int hi = __reduce_max_sync(0xFFFFFFFFu, F::kMaxCode - c0);
         const int fneg = max(p.fmin, lo), fpos = min(p.fmax, hi);
 #pragma unroll 1
-        for (int f = -1; f >= fneg; f--) SS_TAKE(f, <=)
-#pragma unroll 1
         for (int f = 1; f <= fpos; f++) SS_TAKE(f, <)
+#pragma unroll 1
+        for (int f = -1; f >= fneg; f--) {
+          if (f > -kPruneFrom) {
+            SS_TAKE(f, <=)
+          } else {
+            SS_TAKE_NEG(f)
+          }
+        }
       }
 
       // a7: emit the winner: codes of t = y * rho*, scale byte, offset, errors
