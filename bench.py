@@ -360,6 +360,20 @@ def run_ours(a, rank, world, local_rank):
             "hbm_frac": hbm_achieved / pk["hbm_gbs"]}
     if clk and clk.get("sm_mhz"):
         roof["frac_at_run_clock"] = achieved / (148 * FP32_LANES_PER_SM * clk["sm_mhz"] * 1e6 / 1e12)
+    # The kernel skips, exactly, candidates whose lower bound exceeds the incumbent
+    # (DESIGN.md §4.2): `achieved` counts the method's work (every valid candidate),
+    # `executed_*` the evaluations the kernel actually runs (profiles/quant_evals.json).
+    ef = os.path.join(ROOT, "profiles", "quant_evals.json")
+    try:
+        with open(ef) as f:
+            ev = json.load(f)["evaluated_per_block"].get("%d:%d" % (a.fmin, a.fmax))
+    except Exception:
+        ev = None
+    if ev:
+        ex_ops = 4.0 * ev + 2.0
+        roof["executed_c_per_block"] = ev
+        roof["executed_achieved"] = n_local * ex_ops / (quant_ms * 1e-3) / 1e12
+        roof["executed_frac"] = roof["executed_achieved"] / peak
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,

@@ -38,6 +38,10 @@ struct Workspace {
 };
 
 std::mutex g_mu;
+#ifdef SS_COUNT_EVALS
+unsigned long long* g_evals = nullptr;  // tools-only counting build
+#endif
+
 std::map<std::pair<int, void*>, Workspace> g_ws;
 
 struct DeviceInfo {
@@ -400,6 +404,10 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.part2 = ws->part2;
     b.tick = ws->tick;
     b.ctr = ws->ctr;
+#ifdef SS_COUNT_EVALS
+    if (!g_evals && cudaMalloc(&g_evals, 8) == cudaSuccess) cudaMemset(g_evals, 0, 8);
+    b.evals = g_evals;
+#endif
     b.flags = ws->flags;
     bool sums = false;
     int64_t tk = 0, gr = 0;
@@ -847,5 +855,18 @@ ss_status ss_quantize_nvfp4_host_batched(const ss_host_tensor_io* t, int count, 
   cudaError_t e3 = cudaStreamSynchronize(R.s_d2h);
   return (e1 || e2 || e3) ? SS_ERR_CUDA : SS_OK;
 }
+
+#ifdef SS_COUNT_EVALS
+/* Tools-only (libss_count.so): block-candidate evaluations executed since the
+ * last call (synchronizes the device). */
+SS_API unsigned long long ss_debug_take_evals(void) {
+  unsigned long long h = 0;
+  if (!g_evals) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(&h, g_evals, 8, cudaMemcpyDeviceToHost);
+  cudaMemset(g_evals, 0, 8);
+  return h;
+}
+#endif
 
 }  // extern "C"

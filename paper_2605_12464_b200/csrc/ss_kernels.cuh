@@ -316,6 +316,7 @@ struct QuantBatch {
   uint32_t* tick;           // per tensor, zero and self re-arming
   uint32_t* ctr;            // [kCounters + 1] task counters + done count, zero and self re-arming
   uint32_t* flags;
+  unsigned long long* evals;  // SS_COUNT_EVALS builds: block-candidate evaluations executed
   QTensor t[kMaxTensors];
 };
 
@@ -583,12 +584,20 @@ __device__ __forceinline__ float cand_lb(float m, const uint4 e) {
 // duplicates carry the same code, so they never change the result.  The
 // negative side runs last because the incumbent is then final or nearly so:
 // a warp skips a negative candidate when no lane's cand_lb reaches it.
+// SS_COUNT_EVALS (tools only): count the candidate evaluations a warp executes.
+#ifdef SS_COUNT_EVALS
+#define SS_COUNT(n) (n_evals += (n))
+#else
+#define SS_COUNT(n) ((void)0)
+#endif
+
 // Negative-side update with exact pruning (cand_lb, warp vote).
 #ifndef SS_NO_PRUNE
 #define SS_TAKE_NEG(F)                                                   \
   {                                                                      \
     const uint4 e_ = base[F];                                            \
     if (__any_sync(0xFFFFFFFFu, cand_lb<FMT>(m, e_) <= best)) {          \
+      SS_COUNT(1);                                                       \
       const float l_ = block_loss<FMT>(y2, y, e_);                       \
       const bool t_ = l_ <= best;                                        \
       best = t_ ? l_ : best;                                             \
@@ -602,6 +611,7 @@ __device__ __forceinline__ float cand_lb(float m, const uint4 e) {
 // Runtime-window updates (scan order of R4, see above).
 #define SS_TAKE(F, CMP)                                      \
   {                                                          \
+    SS_COUNT(1);                                             \
     const uint4 e_ = base[F];                                \
     const float l_ = block_loss<FMT>(y2, y, e_);             \
     const bool t_ = l_ CMP best;                             \
@@ -692,6 +702,9 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     cp_async_commit();
   }
   int s = 0;
+#ifdef SS_COUNT_EVALS
+  unsigned long long n_evals = 0;  // per warp (all lanes count the same)
+#endif
   // global scale of the current task's tensor, recomputed when the tensor changes
   int cur_ti = -1;
   float G = 1.0f;
@@ -762,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 #pragma unroll
           for (int c = 0; c < CI; c++) e[c] = base[i0 + c < NC ? i0 + c : NC - 1];
           cand_loss_n<CI>(y2, y, e, l);
+          SS_COUNT(NC - i0 < CI ? NC - i0 : CI);
 #pragma unroll
           for (int c = 0; c < CI; c++) {
             const int i = i0 + c;
@@ -787,6 +801,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         }
       } else {
         best = block_loss<FMT>(y2, y, base[0]);
+        SS_COUNT(1);
         loss0 = best;  // err_base: the max-abs scale (f = 0)
         bsel = base[0].z;
         // runtime window; skip offsets that are clamped duplicates for every lane
@@ -865,6 +880,9 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 
     s = s + 1 == kStages ? 0 : s + 1;
   }
+#ifdef SS_COUNT_EVALS
+  if (lane == 0 && p.evals) atomicAdd(p.evals, n_evals * 32ull / (unsigned long long)kHalves);
+#endif
   // the last warp of the grid to finish re-arms the counters for the next launch
   if (lane == 0) {
     __threadfence();

@@ -24,6 +24,7 @@ sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
     "noprune": ["SS_NO_PRUNE=1"],
+    "count": ["SS_COUNT_EVALS=1"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
 
@@ -69,12 +70,22 @@ def run_one(variant, layers, windows, reps):
     t_amax = timed(lambda: ss.tensor_amax_batched(xs, out=amax))
     print(json.dumps({"variant": variant, "kernel": "amax", "ms": t_amax, "elements": n,
                       "hbm_gbs": 2 * n / t_amax / 1e6}), flush=True)
+    counting = variant == "count"
+    if counting:
+        import ctypes
+        L = ss.lib()
+        L.ss_debug_take_evals.restype = ctypes.c_ulonglong
     for fmin, fmax in windows:
         t = timed(lambda: ss.quantize_batched(xs, outs, fmin=fmin, fmax=fmax, gmode="device_amax",
                                               amax=amax))
-        print(json.dumps({"variant": variant, "kernel": "quant", "window": [fmin, fmax], "ms": t,
-                          "elements": n, "gelem_s": n / t / 1e6, "bf16_gbs": 2 * n / t / 1e6,
-                          "bytes_gbs": 3.0625 * n / t / 1e6}), flush=True)
+        line = {"variant": variant, "kernel": "quant", "window": [fmin, fmax], "ms": t,
+                "elements": n, "gelem_s": n / t / 1e6, "bf16_gbs": 2 * n / t / 1e6,
+                "bytes_gbs": 3.0625 * n / t / 1e6}
+        if counting:   # executed block-candidate evaluations per block (one pass)
+            L.ss_debug_take_evals()
+            ss.quantize_batched(xs, outs, fmin=fmin, fmax=fmax, gmode="device_amax", amax=amax)
+            line["evaluated_per_block"] = L.ss_debug_take_evals() / (n / 16)
+        print(json.dumps(line), flush=True)
 
 
 def main():
