@@ -563,10 +563,15 @@ __device__ __forceinline__ float block_loss(const uint64_t (&y2)[8], const float
 // monotone, so the computed loss >= RN(d_j^2) for every element j; a
 // candidate whose bound exceeds the incumbent can never be selected, and
 // skipping it changes no output bit.
+//
+// `sat` reports t = m * rho >= vmax: the max element then rounds to vmax for
+// this and every smaller scale, and d = m - vmax * s >= 0 grows as s shrinks,
+// so the bound only increases along the negative side from here on.
 template <int FMT>
-__device__ __forceinline__ float cand_lb(float m, const uint4 e) {
+__device__ __forceinline__ float cand_lb(float m, const uint4 e, bool& sat) {
   using F = Fmt<FMT>;
   const float t = __fmul_rn(m, __uint_as_float(e.x));
+  sat = t >= (F::VF ? 7.5f : 6.0f);
   const uint32_t q = F::VF ? e2m3_round_f16x2(t, t) : e2m1_round_f16x2(t, t);
   float d;
   if constexpr (F::SF == 0) {
@@ -593,10 +598,15 @@ __device__ __forceinline__ float cand_lb(float m, const uint4 e) {
 
 // Negative-side update with exact pruning (cand_lb, warp vote).
 #ifndef SS_NO_PRUNE
+// Used inside the negative-side loop: `break`s once every lane is pruned AND
+// saturated (no further negative offset can win, cand_lb).
 #define SS_TAKE_NEG(F)                                                   \
   {                                                                      \
     const uint4 e_ = base[F];                                            \
-    if (__any_sync(0xFFFFFFFFu, cand_lb<FMT>(m, e_) <= best)) {          \
+    bool sat_;                                                           \
+    const bool prune_ = cand_lb<FMT>(m, e_, sat_) > best;                \
+    if (__all_sync(0xFFFFFFFFu, prune_ && sat_)) break;                  \
+    if (!__all_sync(0xFFFFFFFFu, prune_)) {                              \
       SS_COUNT(1);                                                       \
       const float l_ = block_loss<FMT>(y2, y, e_);                       \
       const bool t_ = l_ <= best;                                        \

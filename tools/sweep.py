@@ -6,7 +6,9 @@ ALU / HBM roofline fractions, valid-candidate count, and the MSE cut.
     python tools/sweep.py [--configs c1,c2,c3,c4,c5] [--out gpurun_out/sweep.jsonl]
 
 Timing: CUDA events on the launching stream around `reps` back-to-back calls
-(2 warm-ups first).
+(2 warm-ups first).  With SS_LIB_VARIANT=count (libss_count.so) each line also
+carries the candidate evaluations the kernel executed per block (exact pruning
+skips the rest) and the ALU fraction of that executed work.
 C1 (33.5 MB) is rotated over 40 copies (> L2) between runs; the others
 exceed L2.  The driver's bench line is bench.py; this is the table behind
 DESIGN.md §11.
@@ -59,6 +61,14 @@ def measure(torch, ss, groups, fmin, fmax, reps=5, fmt="nvfp4"):
     for i in range(len(groups)):
         ss.tensor_amax_batched(groups[i], out=amax[i])
     res = {}
+    if os.environ.get("SS_LIB_VARIANT") == "count":   # executed evaluations, one pass
+        import ctypes
+        L = ss.lib()
+        L.ss_debug_take_evals.restype = ctypes.c_ulonglong
+        L.ss_debug_take_evals()
+        q_only(0)
+        nb = sum(x.numel() for x in groups[0]) // 16
+        res["evaluated_per_block"] = L.ss_debug_take_evals() / nb * (2 if mx else 1)
     for name, fn in (("quant", q_only), ("amax_quant", e2e)):
         for w in range(2):
             fn(w % len(groups))
@@ -125,6 +135,10 @@ def report(cfg, fmin, fmax, res, n, ceff, s_best, s_base, hist, hbm, mhz, extra=
             "mse_base": s_base / n, "mse_best": s_best / n}
     if hist is not None and len(hist) <= 40:
         line["fstar_hist"] = hist
+    if "evaluated_per_block" in res:
+        ev = res["evaluated_per_block"]
+        line["executed_c_per_block"] = ev
+        line["executed_alu_frac"] = (4.0 * ev + 2.0) * n / alu_peak / tq
     if extra:
         line.update(extra)
     print(json.dumps(line), flush=True)
