@@ -74,19 +74,30 @@ class ShardPlan:
 class RowShardQuantizer:
     """Quantize a list of tensors whose rows are sharded over ``world`` ranks."""
 
-    def __init__(self, plan: ShardPlan, ops, group=None, device=None):
+    def __init__(self, plan: ShardPlan, ops, group=None, device=None, pipeline_groups: int = 1):
         self.plan, self.ops, self.group = plan, ops, group
         self.amax_buf = ops.new_amax(len(plan.shapes), device)
+        self.pipeline_groups = pipeline_groups
+        self._side = None
 
     def step(self, shards: List[torch.Tensor], outs: List, hooks=None) -> int:
         """One pass over every tensor; returns the number of kernels launched.
 
-        Shard amaxes (one batched launch) -> [the one exchange step: ONE max
-        all-reduce of all the amaxes, 4 B per tensor] -> batched quantize.
-        ``hooks`` (optional) has ``before()`` / ``after()`` called around the
-        quantize launches (bench.py records CUDA events there).
+        N > 1: shard amaxes (one batched launch) -> the one exchange step (ONE
+        max all-reduce of all the amaxes, 4 B per tensor) -> batched quantize.
+        N = 1 with pipeline_groups > 1: the tensors are cut into groups; the
+        amax of every group is launched on a side stream up front and group k's
+        quantize waits only for group k's amax, so the HBM-bound amax pass runs
+        under the ALU-bound quantize (same results).  Measured on C2: 2 % less
+        time per step, but the co-running amax slows the quantize kernel by
+        ~10 %, so the default keeps the two passes sequential.  ``hooks`` (optional) has ``before()`` /
+        ``after()`` called around each quantize call (bench.py records CUDA
+        events there).
         """
         import torch.distributed as dist
+        if self.plan.world == 1 and self.pipeline_groups > 1 and torch.cuda.is_available() \
+                and len(shards) > 1 and shards[0].is_cuda:
+            return self._pipelined(shards, outs, hooks)
         n = self.ops.amax_all(shards, self.amax_buf)
         if self.plan.world > 1:
             dist.all_reduce(self.amax_buf, op=dist.ReduceOp.MAX, group=self.group)
@@ -95,4 +106,27 @@ class RowShardQuantizer:
         n += self.ops.quantize_all(shards, self.amax_buf, outs)
         if hooks is not None:
             hooks.after()
+        return n
+
+    def _pipelined(self, shards, outs, hooks) -> int:
+        main = torch.cuda.current_stream()
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=shards[0].device)
+        side = self._side
+        T = len(shards)
+        per = -(-T // min(self.pipeline_groups, T))
+        bounds = [(k, min(T, k + per)) for k in range(0, T, per)]
+        side.wait_stream(main)          # amax slots are free once the previous step is done
+        events, n = [], 0
+        with torch.cuda.stream(side):
+            for lo, hi in bounds:
+                n += self.ops.amax_all(shards[lo:hi], self.amax_buf[lo:hi])
+                events.append(side.record_event())
+        for (lo, hi), ev in zip(bounds, events):
+            main.wait_event(ev)
+            if hooks is not None:
+                hooks.before()
+            n += self.ops.quantize_all(shards[lo:hi], self.amax_buf[lo:hi], outs[lo:hi])
+            if hooks is not None:
+                hooks.after()
         return n

@@ -355,6 +355,16 @@ def test_bench_launch_configuration_c2_sampled(ss, oracle_lib):
     outs = [ops.alloc_out(x) for x in xs]
     q = RowShardQuantizer(ShardPlan([(s.rows, s.cols) for s in specs], 0, 1), ops, device="cuda")
     assert q.step(xs, outs) == 2 + 2 * 2      # amax x2, quant x2, sums x2
+    # the pipelined variant (8 groups on two streams) gives the same outputs
+    codes0 = [outs[k].codes.clone() for k in (0, 127, 251)]
+    qp = RowShardQuantizer(ShardPlan([(s.rows, s.cols) for s in specs], 0, 1), ops, device="cuda",
+                           pipeline_groups=8)
+    for o in outs:
+        o.codes.zero_()
+    assert qp.step(xs, outs) == 8 * 3
+    torch.cuda.synchronize()
+    for c, k in zip(codes0, (0, 127, 251)):
+        assert torch.equal(c, outs[k].codes)
     torch.cuda.synchronize()
     rng = np.random.default_rng(11)
     for k in (0, 4, 127, 128, 200, 251):      # both launches, several shapes
