@@ -30,7 +30,7 @@
 #include <stdint.h>
 
 #ifndef SS_MIN_BLOCKS
-#define SS_MIN_BLOCKS 5
+#define SS_MIN_BLOCKS 4
 #endif
 #ifndef SS_BPL
 #define SS_BPL 2         // NVFP4 blocks per lane per warp task
