@@ -95,12 +95,16 @@ enum {
  * one 6-bit code per byte (sign bit 5).  Scales: UE4M3 codes 0..126, or UE8M0
  * codes 0..254 = 2^(c-127) rounded UP from x_max / vmax (R19; no global scale:
  * UE8M0 formats take SS_GLOBAL_NONE only).  32-element blocks need
- * cols % 32 == 0; their loss is the low half's R12 loss + the high half's. */
+ * cols % block == 0; their loss is the tree sum of the 16-element parts' R12 losses. */
 enum {
   SS_FMT_NVFP4 = 0,          /* E2M1 values, UE4M3 scales, 16-blocks (the north star)         */
   SS_FMT_MXFP4 = 1,          /* E2M1 values, UE8M0 scales, 32-blocks                          */
   SS_FMT_MXFP6_E2M3 = 2,     /* E2M3 values, UE8M0 scales, 32-blocks                          */
-  SS_FMT_NVFP6_E2M3 = 3      /* E2M3 values, UE4M3 scales, 16-blocks (the value-format sweep) */
+  SS_FMT_NVFP6_E2M3 = 3,     /* E2M3 values, UE4M3 scales, 16-blocks (the value-format sweep) */
+  SS_FMT_NVFP4_B32 = 4,      /* NVFP4 values and scales on 32-, 64-, 128-, 256-element       */
+  SS_FMT_NVFP4_B64 = 5,      /* blocks: the block-size study (fig:block_size);    */
+  SS_FMT_NVFP4_B128 = 6,     /* a block's loss is the pairwise tree sum of its 16-element    */
+  SS_FMT_NVFP4_B256 = 7      /* parts' R12 losses (R20)                                       */
 };
 
 /* Bytes of the scale buffer of a [rows][cols] tensor in `scale_layout`

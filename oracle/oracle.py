@@ -234,6 +234,9 @@ FORMATS = {
     "mxfp4": (0, 1, 32),        # E2M1 values, UE8M0 scales, 32-blocks
     "mxfp6_e2m3": (1, 1, 32),   # E2M3 values, UE8M0 scales, 32-blocks
     "nvfp6_e2m3": (1, 0, 16),   # E2M3 values, UE4M3 scales, 16-blocks (value sweep)
+    # block-size study (fig:block_size): NVFP4 values and scales
+    "nvfp4_b32": (0, 0, 32), "nvfp4_b64": (0, 0, 64), "nvfp4_b128": (0, 0, 128),
+    "nvfp4_b256": (0, 0, 256),
 }
 
 

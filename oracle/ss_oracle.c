@@ -421,14 +421,17 @@ static float fmt_inv_vmax(int vfmt) {
   return vfmt == 0 ? 1.0f / 6.0f : 1.0f / 7.5f;
 }
 
-/* One candidate of a `bs`-element block: quantize, dequantize, loss.  The
- * loss of each 16-element half is the R12 chain pair (a over even, b over
- * odd indices of the half, then a + b); a 32-element block adds its two
- * halves' losses, low half first (R20). */
+/* One candidate of a `bs`-element block (bs = 16 * 2^k): quantize,
+ * dequantize, loss.  The loss of each 16-element part is the R12 chain pair
+ * (a over even, b over odd indices of the part, then a + b); the parts'
+ * losses are added as a balanced pairwise tree: level 1 adds parts (0,1),
+ * (2,3), ..., level 2 adds those sums pairwise, and so on (R20: for 32
+ * elements simply low + high). */
 static float fmt_candidate_loss(int vfmt, int bs, const float* y, float s, float rho,
                                 uint8_t* code) {
-  float total = 0.0f;
-  for (int h = 0; h < bs / 16; h++) {
+  float part[16];
+  const int np = bs / 16;
+  for (int h = 0; h < np; h++) {
     float d[16];
     for (int i = 0; i < 16; i++) {
       float t = y[16 * h + i] * rho; /* R7 */
@@ -440,17 +443,21 @@ static float fmt_candidate_loss(int vfmt, int bs, const float* y, float s, float
     for (int i = 2; i < 16; i += 2) a = fmaf(d[i], d[i], a);
     float b = d[1] * d[1];
     for (int i = 3; i < 16; i += 2) b = fmaf(d[i], d[i], b);
-    total = (h == 0) ? a + b : total + (a + b);
+    part[h] = a + b;
   }
-  return total;
+  for (int w = 1; w < np; w *= 2) /* pairwise tree */
+    for (int h = 0; h < np; h += 2 * w) part[h] = part[h] + part[h + w];
+  return part[0];
 }
+
+static int bs_ok(int bs) { return bs == 16 || bs == 32 || bs == 64 || bs == 128 || bs == 256; }
 
 /* Algorithm 1 for one block of a format (vfmt, sfmt, bs): the NVFP4 rules
  * R2-R5 for UE4M3 scales; for UE8M0 every code 0..254 is a valid scale (there
  * is no zero-scale candidate) and c0 = round_UE8M0(x_max * RN(1/vmax)). */
 int so_search_block_fmt(int vfmt, int sfmt, int bs, const float* y, int fmin, int fmax,
                         so_block_result_fmt* out) {
-  if (fmin > 0 || fmax < 0 || (bs != 16 && bs != 32) || vfmt < 0 || vfmt > 1 || sfmt < 0 ||
+  if (fmin > 0 || fmax < 0 || !bs_ok(bs) || vfmt < 0 || vfmt > 1 || sfmt < 0 ||
       sfmt > 1)
     return 1;
   float xmax = 0.0f;
@@ -461,7 +468,7 @@ int so_search_block_fmt(int vfmt, int sfmt, int bs, const float* y, int fmin, in
   const int cmax = sfmt == 0 ? 126 : 254, cmin = sfmt == 0 ? 1 : 0;
   int have = 0, cstar = -1, n_eval = 0;
   float best = INFINITY, base = NAN;
-  uint8_t code[32], best_code[32] = {0};
+  uint8_t code[256], best_code[256] = {0};
   for (int f = fmin; f <= fmax; f++) {
     int c = c0 + f;
     float s, rho;
@@ -503,7 +510,7 @@ int so_quantize_fmt(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int
                     int gmode, const uint32_t* amax_bits_in, int vfmt, int sfmt, int bs,
                     uint8_t* codes, uint8_t* scales, int8_t* offsets, float* err,
                     double* sums, int64_t* n_eval, float* G_out, int threads) {
-  if (rows < 0 || cols < 0 || (bs != 16 && bs != 32) || cols % bs != 0 || fmin > 0 ||
+  if (rows < 0 || cols < 0 || !bs_ok(bs) || cols % bs != 0 || fmin > 0 ||
       fmax < 0 || vfmt < 0 || vfmt > 1 || sfmt < 0 || sfmt > 1)
     return 1;
   if (gmode < 0 || gmode > 3 || (gmode == 2 && !amax_bits_in) || (sfmt == 1 && gmode != 0))
@@ -569,7 +576,7 @@ int so_quantize_fmt(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int
   for (int64_t r = 0; r < rows; r++) {
     for (int64_t bj = 0; bj < nbr; bj++) {
       const int64_t blk = r * nbr + bj;
-      float y[32];
+      float y[256];
       for (int i = 0; i < bs; i++) {
         float xv = bf16_to_float(x[r * cols + bj * bs + i]);
         y[i] = (gmode == 0) ? xv : xv * Gr[r];
@@ -613,7 +620,7 @@ int so_quantize_fmt(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int
  * code layout of so_quantize_fmt; G has one entry, or `rows` when per_row. */
 int so_dequantize_fmt(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols,
                       int vfmt, int sfmt, int bs, const float* G, int per_row, uint16_t* out) {
-  if (rows < 0 || cols < 0 || (bs != 16 && bs != 32) || cols % bs != 0) return 1;
+  if (rows < 0 || cols < 0 || !bs_ok(bs) || cols % bs != 0) return 1;
   const int64_t nbr = cols / bs;
   for (int64_t r = 0; r < rows; r++) {
     const float g = per_row ? G[r] : G[0];

@@ -70,8 +70,8 @@ int so_quantize(const uint16_t* x_bf16, int64_t rows, int64_t cols, int fmin,
                 double* sums, int64_t* n_eval, float* G_out, int threads);
 
 /* Other block formats: value format vfmt 0 E2M1 / 1 E2M3,
- * scale format sfmt 0 UE4M3 / 1 UE8M0 (R19), block size bs 16 / 32 (loss of
- * a 32-block = low half + high half, each half as R12; R20). */
+ * scale format sfmt 0 UE4M3 / 1 UE8M0 (R19), block size bs 16..256 (16 * 2^k;
+ * loss = pairwise tree sum of the 16-element parts' R12 losses; R20). */
 double so_e2m3_value(int code);            /* code 0..63 (sign bit 5) -> value      */
 int    so_e2m3_encode(float t);            /* RNE, saturating at 7.5, sign kept     */
 float  so_ue8m0_value(int code);           /* 2^(code-127), code 0..254             */
@@ -79,7 +79,7 @@ int    so_ue8m0_encode(float v);           /* smallest power of two >= v, sat. (
 typedef struct {
   int32_t c0, cstar, fstar, n_evaluated;
   float err_best, err_base;
-  uint8_t code[32];                        /* value codes of the winner, one per byte */
+  uint8_t code[256];                       /* value codes of the winner, one per byte */
 } so_block_result_fmt;
 int so_search_block_fmt(int vfmt, int sfmt, int bs, const float* y, int fmin, int fmax,
                         so_block_result_fmt* out);

@@ -23,7 +23,8 @@ GMODES = {"none": 0, "tensor": 1, "device_amax": 2, "row": 3}
 SCALE_LAYOUTS = {"linear": 0, "swizzled": 1}
 # block formats (ss.h SS_FMT_*): name -> (id, block size, value bytes per element)
 FORMATS = {"nvfp4": (0, 16, 0.5), "mxfp4": (1, 32, 0.5), "mxfp6_e2m3": (2, 32, 1.0),
-           "nvfp6_e2m3": (3, 16, 1.0)}
+           "nvfp6_e2m3": (3, 16, 1.0), "nvfp4_b32": (4, 32, 0.5), "nvfp4_b64": (5, 64, 0.5),
+           "nvfp4_b128": (6, 128, 0.5), "nvfp4_b256": (7, 256, 0.5)}
 FLAG_NONFINITE, FLAG_RANGE = 1, 2
 
 _lock = threading.Lock()

@@ -118,6 +118,10 @@ bool fmt_info(int format, FmtInfo* f) {
     case SS_FMT_MXFP4: *f = {0, 1, 32}; return true;
     case SS_FMT_MXFP6_E2M3: *f = {1, 1, 32}; return true;
     case SS_FMT_NVFP6_E2M3: *f = {1, 0, 16}; return true;
+    case SS_FMT_NVFP4_B32: *f = {0, 0, 32}; return true;
+    case SS_FMT_NVFP4_B64: *f = {0, 0, 64}; return true;
+    case SS_FMT_NVFP4_B128: *f = {0, 0, 128}; return true;
+    case SS_FMT_NVFP4_B256: *f = {0, 0, 256}; return true;
     default: return false;
   }
 }
@@ -186,6 +190,10 @@ QuantKernel pick_kernel(int fmin, int fmax, bool ri, int format) {
     case SS_FMT_MXFP4: return qk<-1, -1, ss::kFmtMXFP4>(ri);
     case SS_FMT_MXFP6_E2M3: return qk<-1, -1, ss::kFmtMXFP6E2M3>(ri);
     case SS_FMT_NVFP6_E2M3: return qk<-1, -1, ss::kFmtNVFP6E2M3>(ri);
+    case SS_FMT_NVFP4_B32: return qk<-1, -1, ss::kFmtNVFP4B32>(ri);
+    case SS_FMT_NVFP4_B64: return qk<-1, -1, ss::kFmtNVFP4B64>(ri);
+    case SS_FMT_NVFP4_B128: return qk<-1, -1, ss::kFmtNVFP4B128>(ri);
+    case SS_FMT_NVFP4_B256: return qk<-1, -1, ss::kFmtNVFP4B256>(ri);
     default: break;
   }
   if (fmin == -fmax) {
@@ -632,6 +640,10 @@ ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {
     case SS_FMT_MXFP4: ss::dequant_kernel<ss::kFmtMXFP4><<<grid, 256, 0, cs>>>(p); break;
     case SS_FMT_MXFP6_E2M3: ss::dequant_kernel<ss::kFmtMXFP6E2M3><<<grid, 256, 0, cs>>>(p); break;
     case SS_FMT_NVFP6_E2M3: ss::dequant_kernel<ss::kFmtNVFP6E2M3><<<grid, 256, 0, cs>>>(p); break;
+    case SS_FMT_NVFP4_B32: ss::dequant_kernel<ss::kFmtNVFP4B32><<<grid, 256, 0, cs>>>(p); break;
+    case SS_FMT_NVFP4_B64: ss::dequant_kernel<ss::kFmtNVFP4B64><<<grid, 256, 0, cs>>>(p); break;
+    case SS_FMT_NVFP4_B128: ss::dequant_kernel<ss::kFmtNVFP4B128><<<grid, 256, 0, cs>>>(p); break;
+    case SS_FMT_NVFP4_B256: ss::dequant_kernel<ss::kFmtNVFP4B256><<<grid, 256, 0, cs>>>(p); break;
     default: ss::dequant_kernel<ss::kFmtNVFP4><<<grid, 256, 0, cs>>>(p); break;
   }
   return launch_status();

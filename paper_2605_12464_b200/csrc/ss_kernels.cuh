@@ -62,12 +62,17 @@ constexpr float kGlobalNumer = 2688.0f;          // 6 * 448: largest NVFP4 magni
 
 // Block formats: value format VF
 // (0 E2M1, 1 E2M3), scale format SF (0 UE4M3, 1 UE8M0, R19), block BS (16/32).
-enum : int { kFmtNVFP4 = 0, kFmtMXFP4 = 1, kFmtMXFP6E2M3 = 2, kFmtNVFP6E2M3 = 3 };
+// Formats 4-7: NVFP4 values and scales on 32..256-element blocks (the
+// block-size study of fig:block_size).
+enum : int {
+  kFmtNVFP4 = 0, kFmtMXFP4 = 1, kFmtMXFP6E2M3 = 2, kFmtNVFP6E2M3 = 3,
+  kFmtNVFP4B32 = 4, kFmtNVFP4B64 = 5, kFmtNVFP4B128 = 6, kFmtNVFP4B256 = 7
+};
 template <int FMT>
 struct Fmt {
   static constexpr int VF = (FMT == kFmtMXFP6E2M3 || FMT == kFmtNVFP6E2M3) ? 1 : 0;
   static constexpr int SF = (FMT == kFmtMXFP4 || FMT == kFmtMXFP6E2M3) ? 1 : 0;
-  static constexpr int BS = SF ? 32 : 16;
+  static constexpr int BS = FMT >= kFmtNVFP4B32 ? (32 << (FMT - kFmtNVFP4B32)) : (SF ? 32 : 16);
   static constexpr uint32_t kInvVmaxBits = VF ? 0x3E088889u : kOneSixthBits;  // RN(1/7.5), RN(1/6)
   static constexpr int kMaxCode = SF ? 254 : 126;
 };
@@ -520,14 +525,16 @@ __device__ __forceinline__ void cand_loss_n(const uint64_t (&y2)[8], const float
 
 // Loss of one candidate for the 16 values of this lane in format FMT: the
 // NVFP4 sequence, E2M3 rounding for VF = 1, and for UE8M0 scales (s outside
-// f16) the residual as FFMA2 with q widened to f32.  A 32-element block adds
-// the two lanes' half losses, low half first (R20; FADD commutes bit-exactly).
+// f16) the residual as FFMA2 with q widened to f32.  A block of BS = 16 * 2^k
+// elements spans 2^k lanes; their part losses are summed by an xor butterfly,
+// which every lane evaluates as the same pairwise tree (R20; FADD commutes
+// bit-exactly).
 template <int FMT>
 __device__ __forceinline__ float block_loss(const uint64_t (&y2)[8], const float (&y)[16],
                                             const uint4 e) {
   using F = Fmt<FMT>;
   float l;
-  if constexpr (FMT == kFmtNVFP4) {
+  if constexpr (F::VF == 0 && F::SF == 0) {
     l = cand_loss(y2, y, e);
   } else {
     const uint64_t rr = pack2u(e.x, e.y);
@@ -553,7 +560,8 @@ __device__ __forceinline__ float block_loss(const uint64_t (&y2)[8], const float
     unpack2(acc, a, b);
     l = __fadd_rn(a, b);
   }
-  if constexpr (Fmt<FMT>::BS == 32) l = __fadd_rn(l, __shfl_xor_sync(0xFFFFFFFFu, l, 1));
+#pragma unroll
+  for (int o = 1; o < Fmt<FMT>::BS / 16; o <<= 1) l = __fadd_rn(l, __shfl_xor_sync(0xFFFFFFFFu, l, o));
   return l;
 }
 
@@ -739,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     for (int u = 0; u < kBPL; u++) {
       const int j = u * 32 + lane;          // half-block within the task
       const bool active = j < nblk;
-      const bool writer = kHalves == 1 || (lane & 1) == 0;  // owns the scale block
+      const bool writer = (lane & (kHalves - 1)) == 0;  // owns the scale block
       // scale-block index within the tensor; its row (per-row G, swizzled layout)
       const uint32_t sbk = (uint32_t)(b0 + min(j, nblk - 1)) / kHalves;
       uint32_t row = 0;
@@ -765,7 +773,8 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       float m = 0.0f;
 #pragma unroll
       for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[i]));
-      if constexpr (kHalves == 2) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 1));
+#pragma unroll
+      for (int o = 1; o < kHalves; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
       const float v = __fmul_rn(m, kinv);
       const int c0 = F::SF ? (int)ue8m0_code(v) : (int)e4m3_code(v);
       const uint4* base = F::SF ? tab + Pad + c0 : tab + (c0 ? TabW : 0) + Pad + c0;

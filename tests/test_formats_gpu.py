@@ -104,3 +104,30 @@ def test_mx_rejects_global_scale(ss):
     with pytest.raises(ss.SSError):
         ss.quantize(torch.zeros(4, 48, dtype=torch.bfloat16, device="cuda"), radius=1, gmode="none",
                     fmt="mxfp4")                     # cols % 32 != 0
+
+
+BLOCK_FMTS = ["nvfp4_b32", "nvfp4_b64", "nvfp4_b128", "nvfp4_b256"]
+
+
+@pytest.mark.parametrize("fmt", BLOCK_FMTS)
+@pytest.mark.parametrize("shape", [(37, 256), (65, 512), (9, 4096)])
+def test_block_size_parity(ss, oracle_lib, fmt, shape):
+    x = ssgen.generate("gaussian", *shape, seed=34, tid=shape[0] + shape[1])
+    for gmode in ("none", "tensor", "row"):
+        for w in [(0, 0), (-2, 2), (-126, 126)]:
+            g = ss.quantize(x.cuda(), fmin=w[0], fmax=w[1], gmode=gmode, fmt=fmt)
+            torch.cuda.synchronize()
+            _cmp(g, oracle_lib.quantize_fmt(x, *shape, w[0], w[1], fmt, gmode), G=gmode != "none")
+
+
+def test_block_size_swizzled(ss, oracle_lib):
+    rows, cols = 300, 512
+    x = ssgen.generate("student_t", rows, cols, seed=35, tid=1)
+    g = ss.quantize(x.cuda(), radius=8, gmode="tensor", fmt="nvfp4_b64", scale_layout="swizzled")
+    torch.cuda.synchronize()
+    ref = oracle_lib.quantize_fmt(x, rows, cols, -8, 8, "nvfp4_b64", "tensor")
+    assert np.array_equal(g.scales.cpu().numpy(), blocked(ref.scales))
+    d = ss.dequantize(g.codes, g.scales, rows, cols, g.G, scale_layout="swizzled", fmt="nvfp4_b64")
+    torch.cuda.synchronize()
+    rd = oracle_lib.dequantize_fmt(ref.codes, ref.scales, rows, cols, "nvfp4_b64", ref.G)
+    assert np.array_equal(d.cpu().view(torch.int16).numpy().view(np.uint16), rd)

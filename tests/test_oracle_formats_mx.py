@@ -135,3 +135,51 @@ def test_mxfp4_offsets_two_modes(oracle_lib):
     cut = 100 * (1 - r.sums[0] / r.sums[1])
     print("MXFP4 Gaussian MSE cut %.2f%% (paper: 8%%, P:303; unpinned, R19)" % cut)
     assert 0 < cut < 30
+
+
+def _tree_loss_brute(o, y, bs):
+    """Independent exhaustive search for an NVFP4-valued block of bs elements:
+    every UE4M3 code 1..126 (and the zero scale when c0 == 0 is irrelevant for
+    nonzero blocks), parts of 16 summed as a pairwise tree (R20)."""
+    best = None
+    for c in range(1, 127):
+        s = np.float32(o.e4m3_value(c))
+        rho = np.float32(1.0) / s
+        codes = o.e2m1_encode((y * rho).astype(np.float32))
+        q = np.array([o.e2m1_value(int(k)) for k in codes], np.float32)
+        parts = []
+        for h in range(bs // 16):
+            d = [fma32(-q[16 * h + i], s, y[16 * h + i]) for i in range(16)]
+            a = np.float32(d[0] * d[0])
+            for i in range(2, 16, 2):
+                a = fma32(d[i], d[i], a)
+            b = np.float32(d[1] * d[1])
+            for i in range(3, 16, 2):
+                b = fma32(d[i], d[i], b)
+            parts.append(np.float32(a + b))
+        while len(parts) > 1:
+            parts = [np.float32(parts[i] + parts[i + 1]) for i in range(0, len(parts), 2)]
+        if best is None or parts[0] < best[0]:
+            best = (parts[0], c)
+    return best
+
+
+def test_block_size_64_brute_force(oracle_lib):
+    rng = np.random.default_rng(7)
+    for trial in range(3):
+        y = (rng.standard_normal(64) * 10.0 ** rng.uniform(-2, 2)).astype(np.float32)
+        x = y.astype(ml_dtypes.bfloat16).view(np.uint16)
+        yb = x.view(ml_dtypes.bfloat16).astype(np.float32)
+        r = oracle_lib.quantize_fmt(x, 1, 64, -126, 126, "nvfp4_b64", "none")
+        loss, c = _tree_loss_brute(oracle_lib, yb, 64)
+        assert r.scales[0, 0] == c and np.float32(r.err[0, 0]) == loss
+
+
+def test_block_size_gap_shrinks(oracle_lib):
+    # fig:block_size (P:306-307): the search's MSE gain shrinks as blocks grow
+    x = ssgen.generate("gaussian", 64, 4096, seed=8, tid=8)
+    cuts = []
+    for fmt in ("nvfp4", "nvfp4_b32", "nvfp4_b64", "nvfp4_b128", "nvfp4_b256"):
+        r = oracle_lib.quantize_fmt(x, 64, 4096, -126, 126, fmt, "none")
+        cuts.append(100 * (1 - r.sums[0] / r.sums[1]))
+    assert all(a > b for a, b in zip(cuts, cuts[1:])), cuts
