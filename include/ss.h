@@ -24,17 +24,26 @@
  *
  * Layouts (R15): codes [rows][cols/2] u8, element 2j in the low nibble of byte
  * j, sign in bit 3 of each nibble (negative values that round to 0 keep the
- * sign, R11); scales [rows][cols/16] u8 E4M3 codes, linear row-major.
+ * sign, R11); scales [rows][cols/16] u8 E4M3 codes, linear row-major, or the
+ * tensor-core swizzled layout (SS_SCALE_SWIZZLED, R15b).  Per-row global
+ * scales (SS_GLOBAL_ROW, R9b) and other block formats (SS_FMT_*, R19, R20)
+ * are opt-in through the _ex / _batched / _fmt entry points.
+ *
+ * Implementation note: candidates that provably cannot win are skipped
+ * (exact branch and bound); outputs are unaffected.
  *
  * Conventions for every entry point:
  *  - All array arguments are DEVICE pointers owned by the caller unless the
  *    name starts with h_ (host).  The library never keeps a pointer after the
- *    call returns; its only allocations are a small per-(device, stream)
- *    workspace (amax slot, status flags, per-CTA partial sums), created on
- *    first use and reused.
+ *    call returns; its only allocations are a per-(device, stream) workspace
+ *    (status flags, scheduler counters, amax slots, error-sum partials) and,
+ *    for the host-buffer entry points, a ring of device staging slots, all
+ *    created on first use, grown monotonically and reused.  Growing one
+ *    synchronizes its stream once; a CUDA graph may capture a call whose
+ *    workspace is already warm (tests/test_parity_gpu.py).
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Every call only enqueues work on `stream` and returns; none synchronizes
- *    except ss_get_device_status and ss_quantize_nvfp4_host.
+ *    except ss_get_device_status and the two _host entry points.
  *  - Argument errors are detected synchronously and returned without
  *    launching anything.  A failed launch returns SS_ERR_CUDA.
  *  - Non-finite input (NaN/Inf) cannot be reported synchronously: the amax
@@ -166,18 +175,20 @@ SS_API ss_status ss_quantize_nvfp4(const void* in_bf16, int64_t rows, int64_t co
 /* Full argument set.  Unused nullable outputs cost nothing. */
 typedef struct {
   const void* in_bf16;          /* [rows][cols] bf16, 16-B aligned                         */
-  int64_t rows, cols;           /* rows >= 0, cols % 16 == 0                                */
+  int64_t rows, cols;           /* rows >= 0, cols % (block size of `format`) == 0         */
   int f_min, f_max;             /* inclusive window, f_min <= 0 <= f_max (R6); clamped to   */
-                                /* [-126, 126]; e.g. the paper's production [-2, 6] */
+                                /* [-126, 126] (UE4M3) / [-254, 254] (UE8M0); e.g. the      */
+                                /* paper's production [-2, 6]                        */
   int global_scale_mode;        /* SS_GLOBAL_*                                              */
   const uint32_t* d_amax_bits;  /* SS_GLOBAL_DEVICE_AMAX: device u32 FP32 bits of the amax  */
-  uint8_t* out_codes;           /* [rows][cols/2] u8, 8-B aligned                           */
-  uint8_t* out_scales;          /* [rows][cols/16] u8                                       */
-  float* out_err;               /* nullable: [nb][2] f32 {err_best, err_base}, 8-B aligned  */
+  uint8_t* out_codes;           /* ss_code_bytes(): [rows][cols/2] u8 for E2M1, 8-B aligned */
+  uint8_t* out_scales;          /* ss_scale_bytes_fmt(): [rows][cols/bs] u8 or swizzled     */
+  float* out_err;               /* nullable: [nb][2] f32 {err_best, err_base}, 8-B aligned; */
+                                /* nb = rows * cols / block size                            */
   int8_t* out_offset;           /* nullable: [nb] f* = c* - c0 (R5)                          */
   double* d_err_sums;           /* nullable: device f64[2] = {sum err_best, sum err_base},  */
-                                /* overwritten; fixed-order two-level reduction of per-32-  */
-                                /* block partials: deterministic for any grid               */
+                                /* overwritten; fixed-order reduction of per-warp-task      */
+                                /* partials (sums_kernel): deterministic for any grid       */
   float* d_global_scale;        /* nullable: device f32 receives G (for dequantization);    */
                                 /* SS_GLOBAL_ROW: required, [rows] f32                     */
   void* stream;
