@@ -1,0 +1,53 @@
+// ss_common.cuh — tuning macros, launch constants and block-format traits.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef SS_MIN_BLOCKS
+#define SS_MIN_BLOCKS 4
+#endif
+#ifndef SS_BPL
+#define SS_BPL 2         // NVFP4 blocks per lane per warp task
+#endif
+#ifndef SS_CILP
+#define SS_CILP 2        // candidates whose loss loops are interleaved (fixed windows)
+#endif
+namespace ss {
+
+constexpr int kWarps = 8;                     // warps per CTA
+constexpr int kThreads = 32 * kWarps;
+constexpr int kBPL = SS_BPL;                  // 16-element blocks per lane per task
+constexpr int kTaskBlocks = 32 * kBPL;        // NVFP4 blocks per warp task
+constexpr int kTaskBytes = kTaskBlocks * 32;  // bf16 input bytes per task
+constexpr int kStages = kBPL >= 4 ? 2 : 4 / kBPL;  // per-warp smem buffers (tasks in flight)
+constexpr int kSegTasks = 4096;               // tasks per CTA of the error-sum kernel
+constexpr int kCounters = 256;                // task counters of the dynamic scheduler
+constexpr int kPruneFrom = 3;                 // exact pruning for offsets f <= -kPruneFrom
+constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
+constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
+constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk (32 KiB)
+
+constexpr uint32_t kOneSixthBits = 0x3E2AAAABu;  // RN(1/6) (Alg. 1 line 2; R8)
+constexpr float kGlobalNumer = 2688.0f;          // 6 * 448: largest NVFP4 magnitude (R9)
+
+// Block formats: value format VF
+// (0 E2M1, 1 E2M3), scale format SF (0 UE4M3, 1 UE8M0, R19), block BS (16..256).
+// Formats 4-7: NVFP4 values and scales on 32..256-element blocks (the
+// block-size study of fig:block_size).
+enum : int {
+  kFmtNVFP4 = 0, kFmtMXFP4 = 1, kFmtMXFP6E2M3 = 2, kFmtNVFP6E2M3 = 3,
+  kFmtNVFP4B32 = 4, kFmtNVFP4B64 = 5, kFmtNVFP4B128 = 6, kFmtNVFP4B256 = 7
+};
+template <int FMT>
+struct Fmt {
+  static constexpr int VF = (FMT == kFmtMXFP6E2M3 || FMT == kFmtNVFP6E2M3) ? 1 : 0;
+  static constexpr int SF = (FMT == kFmtMXFP4 || FMT == kFmtMXFP6E2M3) ? 1 : 0;
+  static constexpr int BS = FMT >= kFmtNVFP4B32 ? (32 << (FMT - kFmtNVFP4B32)) : (SF ? 32 : 16);
+  static constexpr uint32_t kInvVmaxBits = VF ? 0x3E088889u : kOneSixthBits;  // RN(1/7.5), RN(1/6)
+  static constexpr int kMaxCode = SF ? 254 : 126;
+};
+__host__ __device__ constexpr float global_numer(int vf) { return vf ? 3360.0f : kGlobalNumer; }
+
+enum : uint32_t { kFlagNonFinite = 1u, kFlagRange = 2u };
+
+}  // namespace ss

@@ -1,0 +1,281 @@
+// ss_quant_kernel.cuh — the search-quantize kernel (Algorithm 1 per block, a1 and a3-a7).
+#pragma once
+#include "ss_search.cuh"
+
+namespace ss {
+
+// RI: the batch needs each block's row (per-row G or the swizzled scale
+// layout); without it those per-block steps are compiled out.  FMT: block
+// format (Fmt<>); fixed windows (NEG >= 0) exist for NVFP4 only.  Units:
+// `b`/`j` index 16-element HALF-blocks (one per lane); a 32-element block is
+// the lane pair (2i, 2i + 1), whose even lane writes its scale, offset and
+// errors.
+template <int NEG, int POS, bool RI, int FMT>
+__global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
+  using F = Fmt<FMT>;
+  static_assert(FMT == kFmtNVFP4 || NEG < 0, "fixed windows are compiled for NVFP4 only");
+  constexpr int Pad = NEG < 0 ? F::kMaxCode : (NEG > POS ? NEG : POS);
+  constexpr int TabW = F::SF ? 255 + 2 * Pad : 127 + 2 * Pad;
+  constexpr int kHalves = F::BS / 16;  // lanes per scale block
+  __shared__ __align__(16) uint4 tab[F::SF ? TabW : 2 * TabW];
+  __shared__ __align__(128) uint4 buf[kWarps][kStages][kTaskBytes / 16];
+
+  build_cand_table<Pad, F::SF>(tab);
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarps + w;
+
+  const float kinv = __uint_as_float(F::kInvVmaxBits);  // RN(1 / vmax) (R8)
+  // Stage s of this warp holds one task.  Lane l copies its own blocks
+  // l, l+32, ... (2 x 16-B LDGSTS each) and later reads back only what it
+  // copied, so no cross-lane sync is needed; one commit group per stage
+  // (empty groups past the end keep the group count uniform).
+  // Task indices are 32-bit: a batch holds < 2^31 tasks (2^41 elements).
+  auto issue = [&](int tk, int ti, int s) {
+    const QTensor& T = p.t[ti];
+    const int b0 = (tk - (int)T.task0) * kTaskBlocks;
+    const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
+    const uint8_t* src = T.in + (int64_t)b0 * 32;
+#pragma unroll
+    for (int u = 0; u < kBPL; u++) {
+      const int j = u * 32 + lane;
+      if (j < nblk) {
+        cp_async16(&buf[w][s][2 * j], src + j * 32);
+        cp_async16(&buf[w][s][2 * j + 1], src + j * 32 + 16);
+      }
+    }
+  };
+  auto gscale = [&](int ti, bool report) -> float {
+    if (p.gmode != 1) return 1.0f;  // 0: G = 1; 2: per-row G, read per block
+    return global_scale(__ldg(p.t[ti].amax), p.flags, report, p.g_numer);
+  };
+  // Dynamic scheduling: counter c hands out tasks c, c + kCounters, ... ; warp
+  // gw draws from counter gw % kCounters, so warps the arbiter favours simply
+  // take more tasks and every warp finishes at about the same time.  Each
+  // warp's tasks increase, so the tensor lookup only moves forward.
+  const int cidx = gw % kCounters;
+  bool exhausted = false;
+  const int ntasks = (int)p.ntasks;
+  auto grab = [&]() -> int {
+    if (exhausted) return -1;
+    uint32_t idx = 0;
+    if (lane == 0) idx = atomicAdd(p.ctr + cidx, 1u);
+    idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
+    const int64_t t = cidx + (int64_t)idx * kCounters;
+    if (t >= ntasks) {
+      exhausted = true;
+      return -1;
+    }
+    return t;
+  };
+
+  // prologue: kStages tasks in flight
+  int q_task[kStages];
+  int q_ti[kStages];
+  int tj = 0;
+#pragma unroll
+  for (int k = 0; k < kStages; k++) {
+    const int t = grab();
+    if (t >= 0) {
+      tj = locate_task(p, t, tj);
+      issue(t, tj, k);
+    }
+    q_task[k] = t;
+    q_ti[k] = tj;
+    cp_async_commit();
+  }
+  int s = 0;
+#ifdef SS_COUNT_EVALS
+  unsigned long long n_evals = 0;  // per warp (all lanes count the same)
+#endif
+  // global scale of the current task's tensor, recomputed when the tensor changes
+  int cur_ti = -1;
+  float G = 1.0f;
+  while (q_task[0] >= 0) {
+    const int task = q_task[0];
+    const int ti = q_ti[0];
+    const QTensor& T = p.t[ti];
+    if (ti != cur_ti) {  // warp-uniform
+      cur_ti = ti;
+      G = gscale(ti, task == (int)T.task0 && lane == 0);
+    }
+    const int b0 = (task - (int)T.task0) * kTaskBlocks;   // first block of the task
+    const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
+
+    cp_async_wait<kStages - 1>();  // this lane's copies of stage s have landed
+    int8_t* offsets = T.offsets ? T.offsets + b0 / kHalves : nullptr;
+    float2* err = T.err ? T.err + b0 / kHalves : nullptr;
+    double sb = 0.0, sc = 0.0;
+    const uint64_t GG = pack2(G, G);
+
+#pragma unroll 1
+    for (int u = 0; u < kBPL; u++) {
+      const int j = u * 32 + lane;          // half-block within the task
+      const bool active = j < nblk;
+      const bool writer = (lane & (kHalves - 1)) == 0;  // owns the scale block
+      // scale-block index within the tensor; its row (per-row G, swizzled layout)
+      const uint32_t sbk = (uint32_t)(b0 + min(j, nblk - 1)) / kHalves;
+      uint32_t row = 0;
+      uint64_t Gb = GG;
+      if (RI && (T.g_row || T.swz)) {  // warp-uniform
+        row = div_rows(sbk, T.nbr, T.nbr_magic);
+        if (T.g_row) {
+          const float gr = __ldg(T.g_row + row);
+          Gb = pack2(gr, gr);
+        }
+      }
+      // a1 + a3: bf16 -> f32 is exact; y = RN(x * G)
+      const uint4 v0 = buf[w][s][2 * j], v1 = buf[w][s][2 * j + 1];
+      const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      float y[16];
+      uint64_t y2[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        y2[k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), Gb);
+        unpack2(y2[k], y[2 * k], y[2 * k + 1]);
+      }
+      // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)
+      float m = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; i++) m = fmaxf(m, fabsf(y[i]));
+#pragma unroll
+      for (int o = 1; o < kHalves; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+      const float v = __fmul_rn(m, kinv);
+      const int c0 = F::SF ? (int)ue8m0_code(v) : (int)e4m3_code(v);
+      const uint4* base = F::SF ? tab + Pad + c0 : tab + (c0 ? TabW : 0) + Pad + c0;
+
+      // a5 + a6: candidate search (Alg. 1 lines 5-10)
+      float best, loss0;
+      uint32_t bsel;
+      if constexpr (NEG >= 0) {
+        // f = 0, 1, ..., POS in chunks of CI interleaved candidates (the
+        // selection updates applied in scan order), then the negative side
+        constexpr int NC = 1 + POS;
+        constexpr int CI = SS_CILP < NC ? SS_CILP : NC;
+#pragma unroll
+        for (int i0 = 0; i0 < NC; i0 += CI) {
+          uint4 e[CI];
+          float l[CI];
+#pragma unroll
+          for (int c = 0; c < CI; c++) e[c] = base[i0 + c < NC ? i0 + c : NC - 1];
+          cand_loss_n<CI>(y2, y, e, l);
+          SS_COUNT(NC - i0 < CI ? NC - i0 : CI);
+#pragma unroll
+          for (int c = 0; c < CI; c++) {
+            const int i = i0 + c;
+            if (i >= NC) break;
+            if (i == 0) {
+              best = l[c];
+              loss0 = l[c];  // err_base: the max-abs scale (f = 0)
+              bsel = e[c].z;
+            } else {
+              const bool t_ = l[c] < best;
+              best = t_ ? l[c] : best;
+              bsel = t_ ? e[c].z : bsel;
+            }
+          }
+        }
+#pragma unroll
+        for (int f = 1; f <= NEG; f++) {
+          if (f < kPruneFrom) {  // near offsets almost never prune for a whole warp
+            SS_TAKE(-f, <=)
+          } else {
+            SS_TAKE_NEG(-f)
+          }
+        }
+      } else {
+        best = block_loss<FMT>(y2, y, base[0]);
+        SS_COUNT(1);
+        loss0 = best;  // err_base: the max-abs scale (f = 0)
+        bsel = base[0].z;
+        // runtime window; skip offsets that are clamped duplicates for every lane
+        const int lo = __reduce_min_sync(0xFFFFFFFFu, F::SF ? -c0 : (c0 ? 1 : 0) - c0);
+        const int hi = __reduce_max_sync(0xFFFFFFFFu, F::kMaxCode - c0);
+        const int fneg = max(p.fmin, lo), fpos = min(p.fmax, hi);
+#pragma unroll 1
+        for (int f = 1; f <= fpos; f++) SS_TAKE(f, <)
+#pragma unroll 1
+        for (int f = -1; f >= fneg; f--) {
+          if (f > -kPruneFrom) {
+            SS_TAKE(f, <=)
+          } else {
+            SS_TAKE_NEG(f)
+          }
+        }
+      }
+
+      // a7: emit the winner: codes of t = y * rho*, scale byte, offset, errors
+      const uint32_t code = bsel >> 16;
+      const float rs = __uint_as_float(
+          (F::SF ? tab[Pad + code] : tab[(code ? TabW : 0) + Pad + code]).x);
+      const uint64_t rr = pack2(rs, rs);
+      float t[16];
+#pragma unroll
+      for (int k = 0; k < 8; k++) unpack2(fmul2(y2[k], rr), t[2 * k], t[2 * k + 1]);
+      if (active) {
+        const int64_t hb = b0 + j;  // half-block index within the tensor
+        if constexpr (F::VF == 0) {
+          uint2 cw;
+          cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+          cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
+          __stcs(T.codes + hb, cw);
+        } else {  // E2M3: one code per byte
+          uint32_t cw[4];
+#pragma unroll
+          for (int k = 0; k < 4; k++)
+            cw[k] = e2m3_pack2(t[4 * k], t[4 * k + 1]) | (e2m3_pack2(t[4 * k + 2], t[4 * k + 3]) << 16);
+          __stcs(reinterpret_cast<uint4*>(T.codes) + hb, make_uint4(cw[0], cw[1], cw[2], cw[3]));
+        }
+        if (writer) {
+          if (!RI || !T.swz) {
+            T.scales[sbk] = (uint8_t)code;
+          } else {
+            T.scales[swizzled_scale_offset(row, sbk - row * T.nbr, T.nkt)] = (uint8_t)code;
+          }
+          const int jb = j / kHalves;  // scale block within the task
+          if (offsets) offsets[jb] = (int8_t)((int)code - c0);
+          if (err) __stcs(err + jb, make_float2(best, loss0));
+          sb += (double)best;
+          sc += (double)loss0;
+        }
+      }
+    }
+    {  // refill stage s with the next task drawn (always commit: uniform group count)
+      const int t = grab();
+      if (t >= 0) {
+        tj = locate_task(p, t, tj);
+        issue(t, tj, s);
+      }
+      cp_async_commit();
+#pragma unroll
+      for (int k = 0; k + 1 < kStages; k++) {
+        q_task[k] = q_task[k + 1];
+        q_ti[k] = q_ti[k + 1];
+      }
+      q_task[kStages - 1] = t;
+      q_ti[kStages - 1] = tj;
+    }
+    if (T.sums) {  // per-task partial (fixed lane tree); reduced by sums_kernel
+      sb = warp_sum(sb);
+      sc = warp_sum(sc);
+      if (lane == 0) p.part1[task] = make_double2(sb, sc);
+    }
+    if (T.g_out && b0 == 0 && lane == 0 && p.gmode != 2) *T.g_out = G;
+
+    s = s + 1 == kStages ? 0 : s + 1;
+  }
+#ifdef SS_COUNT_EVALS
+  if (lane == 0 && p.evals) atomicAdd(p.evals, n_evals * 32ull / (unsigned long long)kHalves);
+#endif
+  // the last warp of the grid to finish re-arms the counters for the next launch
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(p.ctr + kCounters, 1u) == gridDim.x * kWarps - 1) {
+      for (int c = 0; c < kCounters; c++) p.ctr[c] = 0u;
+      p.ctr[kCounters] = 0u;
+    }
+  }
+}
+
+}  // namespace ss

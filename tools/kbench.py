@@ -23,8 +23,7 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "mb4": ["SS_MIN_BLOCKS=4"],
-    "mb6": ["SS_MIN_BLOCKS=6"],
+    "noprune": ["SS_NO_PRUNE=1"],
     "count": ["SS_COUNT_EVALS=1"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
