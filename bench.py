@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no clocks, e2e or cpu baseline")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="test only: initialise the process group and run the sharded path "
+                         "(NCCL all-reduces) even with one rank")
     a = ap.parse_args()
     if a.fmin is None and a.fmax is None:
         a.fmin, a.fmax = -min(a.radius, 126), min(a.radius, 126)
@@ -288,7 +291,8 @@ def run_ours(a, rank, world, local_rank):
     dev_idx = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev_idx)
     dev = torch.device("cuda", dev_idx)
-    if world > 1:
+    dist_on = world > 1 or a.force_dist
+    if dist_on:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -303,7 +307,7 @@ def run_ours(a, rank, world, local_rank):
                                      tid=s.tid, row_start=lo, row_end=hi, device=dev))
     ops = CudaOps(a.fmin, a.fmax, want_err=True, want_sums=True)
     outs = [ops.alloc_out(x) for x in shards]
-    q = RowShardQuantizer(plan, ops, group=None, device=dev)
+    q = RowShardQuantizer(plan, ops, group=None, device=dev, collective=dist_on)
     hooks = QuantEvents(torch)
     copies = l2_copies(2 * plan.local_numel())
     shard_sets = [shards] + [[x.clone() for x in shards] for _ in range(copies - 1)]
@@ -312,7 +316,7 @@ def run_ours(a, rank, world, local_rank):
     for i in range(a.warmup):
         q.step(shard_sets[i % copies], outs)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     clocks = ClockSampler(dev_idx) if not a.no_clocks else None
     if clocks:
@@ -320,7 +324,7 @@ def run_ours(a, rank, world, local_rank):
         time.sleep(0.3)
     hooks.active = True
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     start.record()
@@ -329,14 +333,14 @@ def run_ours(a, rank, world, local_rank):
         launches += q.step(shard_sets[i % copies], outs, hooks)
     stop.record()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     hooks.active = False
     clk = clocks.stop() if clocks else None
     ms = start.elapsed_time(stop) / a.steps
     quant_ms = hooks.total_ms() / a.steps
     t = torch.tensor([ms, quant_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, quant_ms = t.tolist()
 
@@ -349,7 +353,7 @@ def run_ours(a, rank, world, local_rank):
     live = [o for o in outs if o.sums is not None and o.codes.numel()]
     sums = torch.stack([o.sums / o.G.double() ** 2 for o in live]).sum(0) if live else \
         torch.zeros(2, dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(sums)
     s_best, s_base = sums.tolist()
     cut = 100.0 * (1.0 - s_best / s_base) if s_base > 0 else 0.0
@@ -409,7 +413,7 @@ def run_ours(a, rank, world, local_rank):
 
     # e2e through the C ABI with host buffers (pinned), copies inside the timed region
     if not a.no_e2e:
-        line["e2e"] = run_e2e(a, torch, ss, shards, specs, plan, world, dev)
+        line["e2e"] = run_e2e(a, torch, ss, shards, specs, plan, world, dev, dist_on)
 
     del outs, shard_sets
     if not a.no_cpu_baseline and rank == 0 and world == 1:
@@ -428,11 +432,11 @@ def run_ours(a, rank, world, local_rank):
                       % (n // passes, a.fmin, a.fmax, passes, dt)}
     if rank == 0:
         emit(line, a)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 
-def run_e2e(a, torch, ss, shards, specs, plan, world, dev):
+def run_e2e(a, torch, ss, shards, specs, plan, world, dev, dist_on=False):
     import torch.distributed as dist
     hx = [x.cpu().pin_memory() for x in shards]
     hc = [torch.empty(x.shape[0], x.shape[1] // 2, dtype=torch.uint8).pin_memory() for x in shards]
@@ -441,33 +445,51 @@ def run_e2e(a, torch, ss, shards, specs, plan, world, dev):
     bi = sum(x.numel() * 2 for x in hx)
     bo = sum(c.numel() + s.numel() + e.numel() * 4 for c, s, e in zip(hc, hs, he))
 
+    if dist_on:
+        # sharded: device buffers allocated once; per group of tensors
+        # H2D -> batched amax -> NCCL max of the group's amaxes -> batched
+        # quantize -> D2H, the copies on their own streams so that group k+1
+        # uploads while group k computes and group k-1 downloads
+        dx = [torch.empty_like(x, device=dev) for x in hx]
+        douts = [ss.alloc_out(x, want_offsets=False, want_sums=False) for x in dx]
+        amax = torch.zeros(len(hx), dtype=torch.int32, device=dev)
+        live = [k for k, x in enumerate(hx) if x.shape[0]]
+        per = max(1, -(-len(live) // 8))
+        groups = [live[i:i + per] for i in range(0, len(live), per)]
+        s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
     def one_step():
-        if world == 1:
+        if not dist_on:
             # the C-ABI host entry point: per tensor H2D -> amax -> quantize -> D2H,
             # pipelined across tensors on three streams
             ss.quantize_host_batched(hx, hc, hs, he, fmin=a.fmin, fmax=a.fmax, gmode="tensor")
-        else:
-            # sharded: same calls composed through the public API + one all-reduce
-            dx = [torch.empty_like(x, device=dev) for x in hx]
-            amax = torch.zeros(len(hx), dtype=torch.int32, device=dev)
-            for k, x in enumerate(hx):
-                dx[k].copy_(x, non_blocking=True)
-                if x.shape[0]:
-                    ss.tensor_amax(dx[k], out=amax[k:k + 1])
-            dist.all_reduce(amax, op=dist.ReduceOp.MAX)
-            for k, x in enumerate(dx):
-                if x.shape[0] == 0:
-                    continue
-                o = ss.quantize(x, fmin=a.fmin, fmax=a.fmax, gmode="device_amax",
-                                amax=amax[k:k + 1], want_offsets=False, want_sums=False)
-                hc[k].copy_(o.codes, non_blocking=True)
-                hs[k].copy_(o.scales, non_blocking=True)
-                he[k].copy_(o.err, non_blocking=True)
-            torch.cuda.synchronize()
+            return
+        main = torch.cuda.current_stream()
+        s_in.wait_stream(main)
+        for g in groups:
+            with torch.cuda.stream(s_in):
+                for k in g:
+                    dx[k].copy_(hx[k], non_blocking=True)
+                ev_in = s_in.record_event()
+            main.wait_event(ev_in)
+            xs = [dx[k] for k in g]
+            lo, hi = g[0], g[-1] + 1                  # groups are contiguous ranges of tensors
+            ss.tensor_amax_batched(xs, out=amax[lo:hi])
+            dist.all_reduce(amax[lo:hi], op=dist.ReduceOp.MAX)
+            ss.quantize_batched(xs, [douts[k] for k in g], fmin=a.fmin, fmax=a.fmax,
+                                gmode="device_amax", amax=amax[lo:hi])
+            ev_out = main.record_event()
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_out)
+                for k in g:
+                    hc[k].copy_(douts[k].codes, non_blocking=True)
+                    hs[k].copy_(douts[k].scales, non_blocking=True)
+                    he[k].copy_(douts[k].err, non_blocking=True)
+        torch.cuda.synchronize()
 
     one_step()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(a.e2e_steps):
@@ -475,14 +497,15 @@ def run_e2e(a, torch, ss, shards, specs, plan, world, dev):
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / a.e2e_steps
     t = torch.tensor([dt], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dt = t.item()
     n_total = sum(s.numel for s in specs)
     return {"value": 2.0 * n_total / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": bi,
             "d2h_bytes_per_step": bo, "ms_per_step": dt * 1e3,
-            "path": "ss_quantize_nvfp4_host_batched (pinned host buffers)" if world == 1 else
-                    "public API: H2D + ss_tensor_amax + NCCL max + ss_quantize_nvfp4_ex + D2H"}
+            "path": "ss_quantize_nvfp4_host_batched (pinned host buffers)" if not dist_on else
+                    "public API per tensor group: H2D + ss_tensor_amax_batched + NCCL max + "
+                    "ss_quantize_nvfp4_batched + D2H, copies overlapped on two streams"}
 
 
 def main():

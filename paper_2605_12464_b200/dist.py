@@ -74,8 +74,11 @@ class ShardPlan:
 class RowShardQuantizer:
     """Quantize a list of tensors whose rows are sharded over ``world`` ranks."""
 
-    def __init__(self, plan: ShardPlan, ops, group=None, device=None, pipeline_groups: int = 1):
+    def __init__(self, plan: ShardPlan, ops, group=None, device=None, pipeline_groups: int = 1,
+                 collective: bool | None = None):
         self.plan, self.ops, self.group = plan, ops, group
+        # the amax all-reduce runs whenever ranks > 1 (or when forced, to test it with one rank)
+        self.collective = plan.world > 1 if collective is None else collective
         self.amax_buf = ops.new_amax(len(plan.shapes), device)
         self.pipeline_groups = pipeline_groups
         self._side = None
@@ -95,11 +98,11 @@ class RowShardQuantizer:
         events there).
         """
         import torch.distributed as dist
-        if self.plan.world == 1 and self.pipeline_groups > 1 and torch.cuda.is_available() \
+        if not self.collective and self.pipeline_groups > 1 and torch.cuda.is_available() \
                 and len(shards) > 1 and shards[0].is_cuda:
             return self._pipelined(shards, outs, hooks)
         n = self.ops.amax_all(shards, self.amax_buf)
-        if self.plan.world > 1:
+        if self.collective:
             dist.all_reduce(self.amax_buf, op=dist.ReduceOp.MAX, group=self.group)
         if hooks is not None:
             hooks.before()
