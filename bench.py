@@ -399,6 +399,10 @@ def run_ours(a, rank, world, local_rank):
         roof["executed_c_per_block"] = ev
         roof["executed_achieved"] = n_local * ex_ops / (quant_ms * 1e-3) / 1e12
         roof["executed_frac"] = roof["executed_achieved"] / peak
+        # the 3-op FP32-pipe-only figure (E2M1 rounding on the
+        # conversion pipe): 3 lane-ops per element-candidate + 2
+        roof["executed_frac_3op"] = n_local * (3.0 * ev + 2.0) / (quant_ms * 1e-3) / 1e12 / peak
+    roof["frac_3op"] = n_local * (3.0 * ceff + 2.0) / (quant_ms * 1e-3) / 1e12 / peak
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
