@@ -185,11 +185,26 @@ QuantKernel qk(bool ri) {
   return ri ? ss::quant_kernel<NEG, POS, true, FMT> : ss::quant_kernel<NEG, POS, false, FMT>;
 }
 
+// Other formats: fixed symmetric windows of radius 0..2 (MX formats use two
+// offsets in practice), the runtime-window kernel otherwise.
+template <int FMT>
+QuantKernel qk_small(int fmin, int fmax, bool ri) {
+  if (fmin == -fmax) {
+    switch (fmax) {
+      case 0: return qk<0, 0, FMT>(ri);
+      case 1: return qk<1, 1, FMT>(ri);
+      case 2: return qk<2, 2, FMT>(ri);
+      default: break;
+    }
+  }
+  return qk<-1, -1, FMT>(ri);
+}
+
 QuantKernel pick_kernel(int fmin, int fmax, bool ri, int format) {
-  switch (format) {  // other formats: the runtime-window kernel
-    case SS_FMT_MXFP4: return qk<-1, -1, ss::kFmtMXFP4>(ri);
-    case SS_FMT_MXFP6_E2M3: return qk<-1, -1, ss::kFmtMXFP6E2M3>(ri);
-    case SS_FMT_NVFP6_E2M3: return qk<-1, -1, ss::kFmtNVFP6E2M3>(ri);
+  switch (format) {
+    case SS_FMT_MXFP4: return qk_small<ss::kFmtMXFP4>(fmin, fmax, ri);
+    case SS_FMT_MXFP6_E2M3: return qk_small<ss::kFmtMXFP6E2M3>(fmin, fmax, ri);
+    case SS_FMT_NVFP6_E2M3: return qk_small<ss::kFmtNVFP6E2M3>(fmin, fmax, ri);
     case SS_FMT_NVFP4_B32: return qk<-1, -1, ss::kFmtNVFP4B32>(ri);
     case SS_FMT_NVFP4_B64: return qk<-1, -1, ss::kFmtNVFP4B64>(ri);
     case SS_FMT_NVFP4_B128: return qk<-1, -1, ss::kFmtNVFP4B128>(ri);

@@ -6,14 +6,14 @@ namespace ss {
 
 // RI: the batch needs each block's row (per-row G or the swizzled scale
 // layout); without it those per-block steps are compiled out.  FMT: block
-// format (Fmt<>); fixed windows (NEG >= 0) exist for NVFP4 only.  Units:
+// format (Fmt<>); fixed windows (NEG >= 0) are compiled for NVFP4 and for
+// radius 0..2 of the other formats (ss_api.cu pick_kernel).  Units:
 // `b`/`j` index 16-element HALF-blocks (one per lane); a 32-element block is
 // the lane pair (2i, 2i + 1), whose even lane writes its scale, offset and
 // errors.
 template <int NEG, int POS, bool RI, int FMT>
 __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
   using F = Fmt<FMT>;
-  static_assert(FMT == kFmtNVFP4 || NEG < 0, "fixed windows are compiled for NVFP4 only");
   constexpr int Pad = NEG < 0 ? F::kMaxCode : (NEG > POS ? NEG : POS);
   constexpr int TabW = F::SF ? 255 + 2 * Pad : 127 + 2 * Pad;
   constexpr int kHalves = F::BS / 16;  // lanes per scale block
@@ -159,7 +159,12 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
           float l[CI];
 #pragma unroll
           for (int c = 0; c < CI; c++) e[c] = base[i0 + c < NC ? i0 + c : NC - 1];
-          cand_loss_n<CI>(y2, y, e, l);
+          if constexpr (FMT == kFmtNVFP4) {
+            cand_loss_n<CI>(y2, y, e, l);
+          } else {
+#pragma unroll
+            for (int c = 0; c < CI; c++) l[c] = block_loss<FMT>(y2, y, e[c]);
+          }
           SS_COUNT(NC - i0 < CI ? NC - i0 : CI);
 #pragma unroll
           for (int c = 0; c < CI; c++) {
