@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -180,15 +181,20 @@ ss_status amax_launch(const void* const* in, const int64_t* n, uint32_t* out, in
 // ---- quantize kernel variants --------------------------------------------------
 typedef void (*QuantKernel)(QuantBatch);
 
+// ri: 0 plain, 1 per-block row index, 2 row-fused tensors (UE4M3 formats only:
+// UE8M0 formats take no global scale)
 template <int NEG, int POS, int FMT = ss::kFmtNVFP4>
-QuantKernel qk(bool ri) {
-  return ri ? ss::quant_kernel<NEG, POS, true, FMT> : ss::quant_kernel<NEG, POS, false, FMT>;
+QuantKernel qk(int ri) {
+  if constexpr (ss::Fmt<FMT>::SF == 0) {
+    if (ri == 2) return ss::quant_kernel<NEG, POS, 2, FMT>;
+  }
+  return ri ? ss::quant_kernel<NEG, POS, 1, FMT> : ss::quant_kernel<NEG, POS, 0, FMT>;
 }
 
 // Other formats: fixed symmetric windows of radius 0..2 (MX formats use two
 // offsets in practice), the runtime-window kernel otherwise.
 template <int FMT>
-QuantKernel qk_small(int fmin, int fmax, bool ri) {
+QuantKernel qk_small(int fmin, int fmax, int ri) {
   if (fmin == -fmax) {
     switch (fmax) {
       case 0: return qk<0, 0, FMT>(ri);
@@ -200,7 +206,7 @@ QuantKernel qk_small(int fmin, int fmax, bool ri) {
   return qk<-1, -1, FMT>(ri);
 }
 
-QuantKernel pick_kernel(int fmin, int fmax, bool ri, int format) {
+QuantKernel pick_kernel(int fmin, int fmax, int ri, int format) {
   switch (format) {
     case SS_FMT_MXFP4: return qk_small<ss::kFmtMXFP4>(fmin, fmax, ri);
     case SS_FMT_MXFP6_E2M3: return qk_small<ss::kFmtMXFP6E2M3>(fmin, fmax, ri);
@@ -241,9 +247,6 @@ int occupancy(QuantKernel k) {
 }
 
 inline int64_t tasks_of(int64_t nb) { return (nb + ss::kTaskBlocks - 1) / ss::kTaskBlocks; }
-inline int64_t segs_of(int64_t nb) {
-  return (tasks_of(nb) + ss::kSegTasks - 1) / ss::kSegTasks;
-}
 
 int sums_grid(int sms) {
   static int occ = 0;
@@ -299,8 +302,8 @@ int rows_grid(int sms) {
 }
 
 // Per-row global scales of every tensor into its d_global_scale (SS_GLOBAL_ROW).
-ss_status rowscale_launch(const ss_tensor_io* io, int count, uint32_t* flags, float numer,
-                          cudaStream_t st, int sms) {
+ss_status rowscale_launch(const ss_tensor_io* io, int count, const std::vector<char>& fused,
+                          uint32_t* flags, float numer, cudaStream_t st, int sms) {
   int i = 0;
   while (i < count) {
     ss::RowBatch b;
@@ -309,7 +312,7 @@ ss_status rowscale_launch(const ss_tensor_io* io, int count, uint32_t* flags, fl
     b.g_numer = numer;
     int64_t tasks = 0;
     for (; i < count && b.n < ss::kMaxTensors; i++) {
-      if (io[i].rows * io[i].cols == 0) continue;
+      if (io[i].rows * io[i].cols == 0 || fused[i]) continue;
       ss::RTensor& t = b.t[b.n++];
       t.in = reinterpret_cast<const uint4*>(io[i].in_bf16);
       t.g_row = io[i].d_global_scale;
@@ -330,6 +333,32 @@ ss_status rowscale_launch(const ss_tensor_io* io, int count, uint32_t* flags, fl
   }
   return SS_OK;
 }
+
+// SS_GLOBAL_ROW with the row amax fused into the quantize pass: rows of
+// 64..512 half-blocks (1024..8192 elements), where a row is a few work items
+// and the rows a whole grid has in flight fit in L2 (<= 4736 warps x 16 KB),
+// so the quantize reads after the warp's own amax pass hit L2.  Shorter rows
+// would leave lanes idle, longer ones would re-read HBM: those use the
+// separate rowscale pass.  SS_ROW_FUSION=0 disables it (A/B measurement).
+bool row_fusion_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("SS_ROW_FUSION");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+inline bool row_fused(const ss_tensor_io& t, int gmode) {
+  const int64_t hpr = t.cols / 16;
+  return gmode == SS_GLOBAL_ROW && t.rows > 0 && hpr >= ss::kTaskBlocks && hpr <= 8 * ss::kTaskBlocks &&
+         row_fusion_enabled();
+}
+inline int64_t parts_of(const ss_tensor_io& t, int gmode) {
+  const int64_t nb = t.rows * t.cols / 16;
+  if (!row_fused(t, gmode)) return tasks_of(nb);
+  return t.rows * ((t.cols / 16 + ss::kTaskBlocks - 1) / ss::kTaskBlocks);
+}
+inline int64_t psegs_of(int64_t parts) { return (parts + ss::kSegTasks - 1) / ss::kSegTasks; }
 
 // The one quantization path behind every entry point.
 ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
@@ -370,8 +399,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         tk = gr = 0;
         in_batch = 0;
       }
-      tk += tasks_of(nb);
-      gr += segs_of(nb);
+      tk += parts_of(io[i], gmode);
+      gr += psegs_of(parts_of(io[i], gmode));
       in_batch++;
       any_sums |= io[i].d_err_sums != nullptr;
     }
@@ -399,7 +428,9 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   } else if (gmode == SS_GLOBAL_DEVICE_AMAX) {
     for (int i = 0; i < count; i++) amax[i] = io[i].d_amax_bits;
   } else if (gmode == SS_GLOBAL_ROW) {
-    if (ss_status s = rowscale_launch(io, count, ws->flags, numer, cs, info.sms)) return s;
+    std::vector<char> fused(count);
+    for (int i = 0; i < count; i++) fused[i] = row_fused(io[i], gmode);
+    if (ss_status s = rowscale_launch(io, count, fused, ws->flags, numer, cs, info.sms)) return s;
   }
   // swizzled scales: zero the padding of partial 128x4 tiles first
   for (int i = 0; i < count; i++) {
@@ -411,8 +442,11 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       return SS_ERR_CUDA;
   }
 
-  bool ri = gmode == SS_GLOBAL_ROW;
-  for (int i = 0; i < count; i++) ri |= io[i].scale_layout == SS_SCALE_SWIZZLED;
+  int ri = gmode == SS_GLOBAL_ROW ? 1 : 0;
+  for (int i = 0; i < count; i++) {
+    if (io[i].scale_layout == SS_SCALE_SWIZZLED) ri = std::max(ri, 1);
+    if (row_fused(io[i], gmode)) ri = 2;
+  }
   QuantKernel k = pick_kernel(fmin, fmax, ri, format);
   const int64_t slots = (int64_t)info.sms * occupancy(k);
   int i = 0;
@@ -433,16 +467,34 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
 #endif
     b.flags = ws->flags;
     bool sums = false;
-    int64_t tk = 0, gr = 0;
+    int64_t tk = 0, gr = 0, pk = 0;
     for (; i < count && b.n < ss::kMaxTensors; i++) {
       const ss_tensor_io& t = io[i];
       const int64_t nb = t.rows * t.cols / 16;
-      // the kernel indexes tasks with 32 bits: close the batch before overflow
-      if (b.n > 0 && tk + tasks_of(nb) > (int64_t)INT32_MAX - ss::kCounters) break;
       if (nb == 0) {
         if (t.d_err_sums && cudaMemsetAsync(t.d_err_sums, 0, 16, cs) != cudaSuccess) return SS_ERR_CUDA;
         continue;
       }
+      const bool rf = row_fused(t, gmode);
+      int hpr = 0, cpr = 0, upr = 0, cpu = 0;
+      int64_t units = tasks_of(nb);
+      if (rf) {
+        // units of `cpu` chunks: enough units for ~6 per warp of the grid, so
+        // the dynamic schedule balances; each unit re-reads its row from L2
+        // for the row amax
+        hpr = (int)(t.cols / 16);
+        cpr = (hpr + ss::kTaskBlocks - 1) / ss::kTaskBlocks;
+        const int64_t want = (6 * slots * ss::kWarps + t.rows - 1) / t.rows;
+        upr = (int)std::min<int64_t>(cpr, std::max<int64_t>(1, want));
+        if (const char* e = std::getenv("SS_ROW_UPR")) upr = std::max(1, std::min(cpr, std::atoi(e)));
+        cpu = (cpr + upr - 1) / upr;
+        upr = (cpr + cpu - 1) / cpu;
+        units = t.rows * upr;
+      }
+      const int64_t parts = parts_of(t, gmode);
+      // the kernel indexes units and partials with 32 bits: close the batch before overflow
+      if (b.n > 0 && (tk + units > (int64_t)INT32_MAX - ss::kCounters || pk + parts > (int64_t)INT32_MAX))
+        break;
       QTensor& q = b.t[b.n++];
       q.in = reinterpret_cast<const uint8_t*>(t.in_bf16);
       q.codes = reinterpret_cast<uint2*>(t.out_codes);
@@ -452,15 +504,22 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       q.sums = t.d_err_sums;
       q.g_out = t.d_global_scale;
       q.amax = amax[i];
-      q.g_row = gmode == SS_GLOBAL_ROW ? t.d_global_scale : nullptr;
-      if (gmode == SS_GLOBAL_ROW) q.g_out = nullptr;
+      q.g_row = (gmode == SS_GLOBAL_ROW && !rf) ? t.d_global_scale : nullptr;
+      if (gmode == SS_GLOBAL_ROW && !rf) q.g_out = nullptr;  // rowscale_kernel wrote G_r
       row_geometry(t.cols, &q.nbr, &q.nbr_magic, &q.nkt, fi.bs);
       q.swz = t.scale_layout == SS_SCALE_SWIZZLED;
       q.nb = nb;
+      q.hpr = (int16_t)hpr;
+      q.cpr = (int16_t)cpr;
+      q.upr = (int16_t)upr;
+      q.cpu = (int16_t)cpu;
       q.task0 = tk;
+      q.part0 = (int32_t)pk;
+      q.npart = (int32_t)parts;
       q.seg0 = gr;
-      tk += tasks_of(nb);
-      gr += segs_of(nb);
+      tk += units;
+      pk += parts;
+      gr += psegs_of(parts);
       sums |= t.d_err_sums != nullptr;
     }
     if (b.n == 0) break;

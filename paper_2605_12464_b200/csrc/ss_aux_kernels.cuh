@@ -96,11 +96,10 @@ __global__ void __launch_bounds__(kThreads) sums_kernel(const __grid_constant__ 
     while (ti + 1 < p.n && p.t[ti + 1].seg0 <= sg) ti++;
     const QTensor& T = p.t[ti];
     if (!T.sums) continue;  // CTA-uniform
-    const int64_t ntask = (T.nb + kTaskBlocks - 1) / kTaskBlocks;
-    const int64_t nseg = (ntask + kSegTasks - 1) / kSegTasks;
+    const int64_t nseg = (T.npart + kSegTasks - 1) / kSegTasks;
     const int64_t k = sg - T.seg0;
     const int64_t t0 = k * kSegTasks;
-    const double2 r = cta_sum(p.part1 + T.task0 + t0, min((int64_t)kSegTasks, ntask - t0), red);
+    const double2 r = cta_sum(p.part1 + T.part0 + t0, min((int64_t)kSegTasks, T.npart - t0), red);
     if (threadIdx.x == 0) {
       p.part2[sg] = r;
       __threadfence();

@@ -4,14 +4,16 @@
 
 namespace ss {
 
-// RI: the batch needs each block's row (per-row G or the swizzled scale
-// layout); without it those per-block steps are compiled out.  FMT: block
+// RI: 0 = no per-block row; 1 = the batch needs each block's row (per-row G
+// from rowscale_kernel or the swizzled scale layout); 2 = also row-fused
+// tensors (their row amax inside this kernel, T.hpr > 0).  Lower levels
+// compile the unused steps out.  FMT: block
 // format (Fmt<>); fixed windows (NEG >= 0) are compiled for NVFP4 and for
 // radius 0..2 of the other formats (ss_api.cu pick_kernel).  Units:
 // `b`/`j` index 16-element HALF-blocks (one per lane); a 32-element block is
 // the lane pair (2i, 2i + 1), whose even lane writes its scale, offset and
 // errors.
-template <int NEG, int POS, bool RI, int FMT>
+template <int NEG, int POS, int RI, int FMT>
 __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
   using F = Fmt<FMT>;
   constexpr int Pad = NEG < 0 ? F::kMaxCode : (NEG > POS ? NEG : POS);
@@ -27,20 +29,45 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   const int gw = blockIdx.x * kWarps + w;
 
   const float kinv = __uint_as_float(F::kInvVmaxBits);  // RN(1 / vmax) (R8)
-  // Stage s of this warp holds one task.  Lane l copies its own blocks
+  // A work item is up to kTaskBlocks half-blocks of one tensor, named by its
+  // error-sum partial index (global over the batch).  Plain tensor: item
+  // part0 + k covers half-blocks [64k, 64k + 64).  Row-fused tensor (T.hpr >
+  // 0): item part0 + r * cpr + c is chunk c of row r; its G_r rides along in
+  // shared memory (q_g).
+  struct Item {
+    int b0;  // < 2^31 half-blocks per tensor (validate_io)
+    int nblk;
+    uint32_t row;
+  };
+  // first item of a tensor (part0; equal to task0 unless the launch has row-fused tensors)
+  auto first_item = [&](const QTensor& T) -> int { return RI == 2 ? (int)T.part0 : (int)T.task0; };
+  auto item_of = [&](const QTensor& T, int it) -> Item {
+    const int local = it - first_item(T);
+    Item x;
+    if (RI == 2 && T.hpr) {
+      x.row = (uint32_t)(local / T.cpr);
+      const int c = local - (int)x.row * T.cpr;
+      x.b0 = (int)x.row * T.hpr + c * kTaskBlocks;
+      x.nblk = min(kTaskBlocks, T.hpr - c * kTaskBlocks);
+    } else {
+      x.row = 0;
+      x.b0 = local * kTaskBlocks;
+      x.nblk = (int)min((int64_t)kTaskBlocks, T.nb - x.b0);
+    }
+    return x;
+  };
+  // Stage s of this warp holds one item.  Lane l copies its own blocks
   // l, l+32, ... (2 x 16-B LDGSTS each) and later reads back only what it
   // copied, so no cross-lane sync is needed; one commit group per stage
   // (empty groups past the end keep the group count uniform).
-  // Task indices are 32-bit: a batch holds < 2^31 tasks (2^41 elements).
-  auto issue = [&](int tk, int ti, int s) {
+  auto issue = [&](int it, int ti, int s) {
     const QTensor& T = p.t[ti];
-    const int b0 = (tk - (int)T.task0) * kTaskBlocks;
-    const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
-    const uint8_t* src = T.in + (int64_t)b0 * 32;
+    const Item x = item_of(T, it);
+    const uint8_t* src = T.in + (int64_t)x.b0 * 32;
 #pragma unroll
     for (int u = 0; u < kBPL; u++) {
       const int j = u * 32 + lane;
-      if (j < nblk) {
+      if (j < x.nblk) {
         cp_async16(&buf[w][s][2 * j], src + j * 32);
         cp_async16(&buf[w][s][2 * j + 1], src + j * 32 + 16);
       }
@@ -50,38 +77,88 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     if (p.gmode != 1) return 1.0f;  // 0: G = 1; 2: per-row G, read per block
     return global_scale(__ldg(p.t[ti].amax), p.flags, report, p.g_numer);
   };
-  // Dynamic scheduling: counter c hands out tasks c, c + kCounters, ... ; warp
+  // Dynamic scheduling: counter c hands out units c, c + kCounters, ... ; warp
   // gw draws from counter gw % kCounters, so warps the arbiter favours simply
-  // take more tasks and every warp finishes at about the same time.  Each
-  // warp's tasks increase, so the tensor lookup only moves forward.
+  // take more units and every warp finishes at about the same time.  A unit is
+  // one item (plain tensor) or, for a row-fused tensor, `cpu` consecutive
+  // chunks of one row, whose global scale the warp first computes from the
+  // whole row (one coalesced pass; the chunks' own reads then hit L2).  Each
+  // warp's units increase, so the tensor lookup only moves forward.  Unit and
+  // item indices are 32-bit (the host splits batches before 2^31).
   const int cidx = gw % kCounters;
   bool exhausted = false;
-  const int ntasks = (int)p.ntasks;
-  auto grab = [&]() -> int {
+  const int nunits = (int)p.ntasks;
+  int tj = 0;
+  // RI == 2 kernels: the current row-fused unit (chunks [c, ce) of row `row`, scale
+  // g still to hand out) lives in shared memory, off the register budget
+  struct RowUnit {
+    int c, ce;
+    uint32_t row;
+    float g;
+  };
+  __shared__ RowUnit ru[RI == 2 ? kWarps : 1];
+  __shared__ float q_g[RI == 2 ? kWarps : 1][kStages];
+  if (RI == 2) {
+    if (lane == 0) ru[w] = RowUnit{0, 0, 0u, 1.0f};
+    __syncwarp();
+  }
+  // next item (its partial index; its tensor in tj), -1 when exhausted.  In a
+  // launch without row-fused tensors (RI < 2) part0 == task0: item == unit.
+  auto grab = [&](int s) -> int {
+    if constexpr (RI == 2) {
+      __syncwarp();
+      const RowUnit cur = ru[w];
+      if (cur.c < cur.ce) {  // next chunk of the current row
+        const QTensor& T = p.t[tj];
+        __syncwarp();
+        if (lane == 0) {
+          ru[w].c = cur.c + 1;
+          q_g[w][s] = cur.g;
+        }
+        return (int)(T.part0 + (int64_t)cur.row * T.cpr + cur.c);
+      }
+    }
     if (exhausted) return -1;
     uint32_t idx = 0;
     if (lane == 0) idx = atomicAdd(p.ctr + cidx, 1u);
     idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
-    const int64_t t = cidx + (int64_t)idx * kCounters;
-    if (t >= ntasks) {
+    const int64_t u = cidx + (int64_t)idx * kCounters;
+    if (u >= nunits) {
       exhausted = true;
       return -1;
     }
-    return t;
+    if constexpr (RI == 2) {
+      tj = locate_task(p, u, tj);
+      const QTensor& T = p.t[tj];
+      const int k = (int)(u - T.task0);
+      if (T.hpr) {  // row-fused unit: row k / upr, chunk group k % upr
+        const uint32_t row = (uint32_t)(k / T.upr);
+        const int c = (k - (int)row * T.upr) * T.cpu;
+        const float g = row_global_scale(T, row, lane, p.flags, p.g_numer);
+        if (lane == 0 && c == 0) T.g_out[row] = g;
+        __syncwarp();
+        if (lane == 0) {
+          ru[w] = RowUnit{c + 1, min(c + T.cpu, T.cpr), row, g};
+          q_g[w][s] = g;
+        }
+        return (int)(T.part0 + (int64_t)row * T.cpr + c);
+      }
+      return (int)T.part0 + k;
+    }
+    return (int)u;  // the caller locates its tensor
   };
 
-  // prologue: kStages tasks in flight
-  int q_task[kStages];
+  // prologue: kStages items in flight
+  int q_it[kStages];
   int q_ti[kStages];
-  int tj = 0;
 #pragma unroll
   for (int k = 0; k < kStages; k++) {
-    const int t = grab();
+    const int t = grab(k);
     if (t >= 0) {
-      tj = locate_task(p, t, tj);
+      if (RI != 2) tj = locate_task(p, t, tj);
       issue(t, tj, k);
     }
-    q_task[k] = t;
+    q_it[k] = t;
     q_ti[k] = tj;
     cp_async_commit();
   }
@@ -89,19 +166,24 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 #ifdef SS_COUNT_EVALS
   unsigned long long n_evals = 0;  // per warp (all lanes count the same)
 #endif
-  // global scale of the current task's tensor, recomputed when the tensor changes
+  // global scale of the current item's tensor, recomputed when the tensor changes
   int cur_ti = -1;
   float G = 1.0f;
-  while (q_task[0] >= 0) {
-    const int task = q_task[0];
+  while (q_it[0] >= 0) {
+    const int it = q_it[0];
     const int ti = q_ti[0];
     const QTensor& T = p.t[ti];
-    if (ti != cur_ti) {  // warp-uniform
+    const Item x = item_of(T, it);
+    const int b0 = x.b0;  // first half-block of the item
+    const int nblk = x.nblk;
+    if (RI == 2 && T.hpr) {  // row-fused: this item's G_r (the next plain item reloads G)
+      __syncwarp();
+      G = q_g[w][s];
+      cur_ti = -1;
+    } else if (ti != cur_ti) {  // warp-uniform
       cur_ti = ti;
-      G = gscale(ti, task == (int)T.task0 && lane == 0);
+      G = gscale(ti, it == first_item(T) && lane == 0);
     }
-    const int b0 = (task - (int)T.task0) * kTaskBlocks;   // first block of the task
-    const int nblk = (int)min((int64_t)kTaskBlocks, T.nb - b0);
 
     cp_async_wait<kStages - 1>();  // this lane's copies of stage s have landed
     int8_t* offsets = T.offsets ? T.offsets + b0 / kHalves : nullptr;
@@ -111,14 +193,14 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 
 #pragma unroll 1
     for (int u = 0; u < kBPL; u++) {
-      const int j = u * 32 + lane;          // half-block within the task
+      const int j = u * 32 + lane;          // half-block within the item
       const bool active = j < nblk;
       const bool writer = (lane & (kHalves - 1)) == 0;  // owns the scale block
       // scale-block index within the tensor; its row (per-row G, swizzled layout)
       const uint32_t sbk = (uint32_t)(b0 + min(j, nblk - 1)) / kHalves;
-      uint32_t row = 0;
+      uint32_t row = x.row;
       uint64_t Gb = GG;
-      if (RI && (T.g_row || T.swz)) {  // warp-uniform
+      if (RI && !(RI == 2 && T.hpr) && (T.g_row || T.swz)) {  // warp-uniform
         row = div_rows(sbk, T.nbr, T.nbr_magic);
         if (T.g_row) {
           const float gr = __ldg(T.g_row + row);
@@ -238,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
           } else {
             T.scales[swizzled_scale_offset(row, sbk - row * T.nbr, T.nkt)] = (uint8_t)code;
           }
-          const int jb = j / kHalves;  // scale block within the task
+          const int jb = j / kHalves;  // scale block within the item
           if (offsets) offsets[jb] = (int8_t)((int)code - c0);
           if (err) __stcs(err + jb, make_float2(best, loss0));
           sb += (double)best;
@@ -246,25 +328,25 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         }
       }
     }
-    {  // refill stage s with the next task drawn (always commit: uniform group count)
-      const int t = grab();
+    {  // refill stage s with the next item drawn (always commit: uniform group count)
+      const int t = grab(s);
       if (t >= 0) {
-        tj = locate_task(p, t, tj);
+        if (RI != 2) tj = locate_task(p, t, tj);
         issue(t, tj, s);
       }
       cp_async_commit();
 #pragma unroll
       for (int k = 0; k + 1 < kStages; k++) {
-        q_task[k] = q_task[k + 1];
+        q_it[k] = q_it[k + 1];
         q_ti[k] = q_ti[k + 1];
       }
-      q_task[kStages - 1] = t;
+      q_it[kStages - 1] = t;
       q_ti[kStages - 1] = tj;
     }
-    if (T.sums) {  // per-task partial (fixed lane tree); reduced by sums_kernel
+    if (T.sums) {  // per-item partial (fixed lane tree); reduced by sums_kernel
       sb = warp_sum(sb);
       sc = warp_sum(sc);
-      if (lane == 0) p.part1[task] = make_double2(sb, sc);
+      if (lane == 0) p.part1[it] = make_double2(sb, sc);
     }
     if (T.g_out && b0 == 0 && lane == 0 && p.gmode != 2) *T.g_out = G;
 

@@ -97,12 +97,20 @@ struct QTensor {
   const uint32_t* amax;     // gmode 1: FP32 bits of the tensor amax
   const float* g_row;       // gmode 2: per-row global scales [rows]
   int64_t nb;               // NVFP4 blocks
-  int64_t task0;            // first global task of this tensor
+  int64_t task0;            // first global scheduling unit of this tensor
   int64_t seg0;             // first global segment (error-sum kernel CTA) of this tensor
   uint32_t nbr;             // blocks per row (cols / 16)
   uint32_t nbr_magic;       // floor((2^32 - 1) / nbr): row = div_rows(block)
   uint32_t nkt;             // swizzled layout: ceil(nbr / 4) scale tiles per 128-row band
   int swz;                  // scale layout: 0 linear [rows][nbr], 1 128x4 swizzled (R15b)
+  // row-fused per-row G (gmode 2 with the row amax inside the quantize pass):
+  // hpr > 0 marks it.  A row is cpr chunks of <= kTaskBlocks half-blocks; a
+  // scheduling unit is cpu chunks of one row (upr units per row); G_r goes to
+  // g_out[row].  hpr == 0: plain tensor, units = items of kTaskBlocks.
+  // (16-bit: hpr <= 512, cpr <= 8; small fields keep the launch parameters small)
+  int16_t hpr, cpr, upr, cpu;
+  int32_t part0;            // first error-sum partial (one per work item) of this tensor
+  int32_t npart;            // error-sum partials of this tensor
 };
 
 struct QuantBatch {
@@ -141,6 +149,33 @@ __device__ __forceinline__ int locate_task(const QuantBatch& p, int64_t k, int f
   int i = from;
   while (i + 1 < p.n && p.t[i + 1].task0 <= k) i++;
   return i;
+}
+
+// Per-row global scale of row `row` of a row-fused tensor, computed by one
+// warp (identical in every lane): G_r = RN(numer / max_k |x_rk|) exactly as
+// rowscale_kernel (R9b), from one coalesced pass over the row's 16-B vectors
+// (8 loads in flight per lane).  The row stays in L2 for the quantize reads.
+__device__ __forceinline__ float row_global_scale(const QTensor& T, uint32_t row, int lane,
+                                                  uint32_t* flags, float numer) {
+  const uint4* src = reinterpret_cast<const uint4*>(T.in) + (int64_t)row * T.hpr * 2;
+  const int nv = T.hpr * 2;
+  const uint32_t M = 0x7FFF7FFFu;
+  uint32_t m = 0;
+  int v = lane;
+  for (; v + 224 < nv; v += 256) {  // 8 loads in flight per lane
+    uint4 a[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = __ldg(src + v + 32 * k);
+#pragma unroll
+    for (int k = 0; k < 8; k++)
+      m = __vmaxu2(m, __vmaxu2(__vmaxu2(a[k].x & M, a[k].y & M), __vmaxu2(a[k].z & M, a[k].w & M)));
+  }
+  for (; v < nv; v += 32) {
+    const uint4 a = __ldg(src + v);
+    m = __vmaxu2(m, __vmaxu2(__vmaxu2(a.x & M, a.y & M), __vmaxu2(a.z & M, a.w & M)));
+  }
+  const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, max(m & 0xFFFFu, m >> 16));
+  return global_scale(mx << 16, flags, lane == 0, numer);
 }
 
 // ---------------------------------------------------------------------------

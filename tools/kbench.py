@@ -39,7 +39,7 @@ def build(names):
         print("built", v, flush=True)
 
 
-def run_one(variant, layers, windows, reps):
+def run_one(variant, layers, windows, reps, layout="linear"):
     import torch
     import ssgen
     if variant != "base":
@@ -50,7 +50,7 @@ def run_one(variant, layers, windows, reps):
     xs = [ssgen.generate(s.kind, s.rows, s.cols, seed=ssgen.workloads.BASE_SEED, tid=s.tid,
                          device=dev) for s in specs]
     n = sum(x.numel() for x in xs)
-    outs = [ss.alloc_out(x, want_offsets=False) for x in xs]
+    outs = [ss.alloc_out(x, want_offsets=False, scale_layout=layout) for x in xs]
     amax = torch.zeros(len(xs), dtype=torch.int32, device=dev)
 
     def timed(fn):
@@ -77,13 +77,14 @@ def run_one(variant, layers, windows, reps):
         L.ss_debug_take_evals.restype = ctypes.c_ulonglong
     for fmin, fmax in windows:
         t = timed(lambda: ss.quantize_batched(xs, outs, fmin=fmin, fmax=fmax, gmode="device_amax",
-                                              amax=amax))
-        line = {"variant": variant, "kernel": "quant", "window": [fmin, fmax], "ms": t,
+                                              amax=amax, scale_layout=layout))
+        line = {"variant": variant, "kernel": "quant", "layout": layout, "window": [fmin, fmax], "ms": t,
                 "elements": n, "gelem_s": n / t / 1e6, "bf16_gbs": 2 * n / t / 1e6,
                 "bytes_gbs": 3.0625 * n / t / 1e6}
         if counting:   # executed block-candidate evaluations per block (one pass)
             L.ss_debug_take_evals()
-            ss.quantize_batched(xs, outs, fmin=fmin, fmax=fmax, gmode="device_amax", amax=amax)
+            ss.quantize_batched(xs, outs, fmin=fmin, fmax=fmax, gmode="device_amax", amax=amax,
+                                scale_layout=layout)
             line["evaluated_per_block"] = L.ss_debug_take_evals() / (n / 16)
         print(json.dumps(line), flush=True)
 
@@ -95,6 +96,7 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--windows", default=None, help="e.g. -8:8,0:0")
+    ap.add_argument("--layout", default="linear", choices=["linear", "swizzled"])
     a = ap.parse_args()
     names = a.variants.split(",")
     wins = WINDOWS if not a.windows else [tuple(int(v) for v in w.split(":"))
@@ -102,11 +104,12 @@ def main():
     if a.mode == "build":
         build(names)
     elif a.mode == "one":
-        run_one(names[0], a.layers, wins, a.reps)
+        run_one(names[0], a.layers, wins, a.reps, a.layout)
     else:
         for v in names:
             cmd = [sys.executable, __file__, "one", "--variants", v, "--layers", str(a.layers),
-                   "--reps", str(a.reps), "--windows", ",".join("%d:%d" % w for w in wins)]
+                   "--reps", str(a.reps), "--windows=" + ",".join("%d:%d" % w for w in wins),
+                   "--layout", a.layout]
             subprocess.run(cmd, timeout=900)
 
 
