@@ -363,7 +363,10 @@ def run_ours(a, rank, world, local_rank):
     ops_per_elem = 4.0 * ceff + 2.0
     achieved = n_local * ops_per_elem / (quant_ms * 1e-3) / 1e12        # T lane-op/s
     peak = 148 * FP32_LANES_PER_SM * pk["sm_max_mhz"] * 1e6 / 1e12
-    bytes_q = n_local * (2.0 + 0.5 + 0.0625 + 0.5)                     # in + codes + scales + err
+    # unsharded runs fuse the amax pass into the quantize launch when the window has
+    # >= 4 offsets (ss_api.cu): that kernel reads the input twice
+    fused = not dist_on and a.fmax - a.fmin >= 3
+    bytes_q = n_local * ((2.0 if fused else 0.0) + 2.0 + 0.5 + 0.0625 + 0.5)  # [amax] + in + codes + scales + err
     hbm_achieved = bytes_q / (quant_ms * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "quant_traffic.json")
@@ -371,12 +374,14 @@ def run_ours(a, rank, world, local_rank):
         try:
             with open(tf) as f:
                 tj = json.load(f)
-            traffic = tj["dram_bytes_per_elem"] * n_local / ((len(shards) + 127) // 128)
+            traffic = tj["fused" if fused else "plain"]["dram_bytes_per_elem"] * n_local / \
+                ((len(shards) + 127) // 128)
         except Exception:
             traffic = None
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
             "frac": achieved / peak, "traffic": traffic,
-            "kernel": "ss::quant_kernel<%d,%d>" % (-a.fmin, a.fmax),
+            "kernel": "ss::quant_kernel<%d,%d,0,0,%s>" % (-a.fmin, a.fmax, "true" if fused else "false"),
+            "amax_fused": fused, "bytes_per_elem": bytes_q / n_local,
             "ops_per_elem": ops_per_elem, "c_eff": ceff,
             "peak_source": "148 SMs x 128 FP32 lanes x %.0f MHz (%s)" % (pk["sm_max_mhz"], pk["source"]),
             "quant_ms_per_step": quant_ms, "quant_share_of_step": quant_ms / ms,

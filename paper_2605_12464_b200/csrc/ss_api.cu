@@ -30,6 +30,7 @@ struct Workspace {
   uint32_t* flags = nullptr;     // sticky status flags (1 word)
   uint32_t* tick = nullptr;      // [kMaxTensors] per-tensor tickets (zero, self re-arming)
   uint32_t* ctr = nullptr;       // [kCounters + 1] scheduler counters (zero, self re-arming)
+  uint32_t* done = nullptr;      // [kMaxTensors + 1] fused-amax completion counts + unit counter (zero, self re-arming)
   uint32_t* amax = nullptr;      // SS_GLOBAL_TENSOR slots
   int64_t amax_cap = 0;
   double2* part1 = nullptr;      // per-task partial sums
@@ -39,8 +40,8 @@ struct Workspace {
 };
 
 std::mutex g_mu;
-#ifdef SS_COUNT_EVALS
-unsigned long long* g_evals = nullptr;  // tools-only counting build
+#if defined(SS_COUNT_EVALS) || defined(SS_AF_TRACE)
+unsigned long long* g_evals = nullptr;  // tools-only counting / tracing builds
 #endif
 
 std::map<std::pair<int, void*>, Workspace> g_ws;
@@ -99,12 +100,13 @@ ss_status get_ws(int dev, void* stream, Workspace** out) {
   Workspace& w = g_ws[std::make_pair(dev, stream)];
   if (!w.flags) {
     void* p = nullptr;
-    const size_t bytes = sizeof(uint32_t) * (1 + ss::kMaxTensors + ss::kCounters + 1);
+    const size_t bytes = sizeof(uint32_t) * (1 + ss::kMaxTensors + ss::kCounters + 1 + ss::kMaxTensors + 1);
     if (cudaMalloc(&p, bytes) != cudaSuccess) return SS_ERR_CUDA;
     if (cudaMemset(p, 0, bytes) != cudaSuccess) return SS_ERR_CUDA;
     w.flags = reinterpret_cast<uint32_t*>(p);
     w.tick = w.flags + 1;
     w.ctr = w.tick + ss::kMaxTensors;
+    w.done = w.ctr + ss::kCounters + 1;
   }
   *out = &w;
   return SS_OK;
@@ -184,7 +186,10 @@ typedef void (*QuantKernel)(QuantBatch);
 // ri: 0 plain, 1 per-block row index, 2 row-fused tensors (UE4M3 formats only:
 // UE8M0 formats take no global scale)
 template <int NEG, int POS, int FMT = ss::kFmtNVFP4>
-QuantKernel qk(int ri) {
+QuantKernel qk(int ri, bool af = false) {
+  if constexpr (FMT == ss::kFmtNVFP4) {
+    if (af) return ss::quant_kernel<NEG, POS, 0, FMT, true>;
+  }
   if constexpr (ss::Fmt<FMT>::SF == 0) {
     if (ri == 2) return ss::quant_kernel<NEG, POS, 2, FMT>;
   }
@@ -206,7 +211,7 @@ QuantKernel qk_small(int fmin, int fmax, int ri) {
   return qk<-1, -1, FMT>(ri);
 }
 
-QuantKernel pick_kernel(int fmin, int fmax, int ri, int format) {
+QuantKernel pick_kernel(int fmin, int fmax, int ri, int format, bool af = false) {
   switch (format) {
     case SS_FMT_MXFP4: return qk_small<ss::kFmtMXFP4>(fmin, fmax, ri);
     case SS_FMT_MXFP6_E2M3: return qk_small<ss::kFmtMXFP6E2M3>(fmin, fmax, ri);
@@ -219,15 +224,15 @@ QuantKernel pick_kernel(int fmin, int fmax, int ri, int format) {
   }
   if (fmin == -fmax) {
     switch (fmax) {
-#define SS_SYM(R) case R: return qk<R, R>(ri);
+#define SS_SYM(R) case R: return qk<R, R>(ri, af);
       SS_SYM(0) SS_SYM(1) SS_SYM(2) SS_SYM(3) SS_SYM(4) SS_SYM(5) SS_SYM(6) SS_SYM(7) SS_SYM(8)
       SS_SYM(9) SS_SYM(10) SS_SYM(11) SS_SYM(12) SS_SYM(13) SS_SYM(14) SS_SYM(15) SS_SYM(16)
 #undef SS_SYM
       default: break;
     }
   }
-  if (fmin == -2 && fmax == 6) return qk<2, 6>(ri);  // the paper's production window
-  return qk<-1, -1>(ri);
+  if (fmin == -2 && fmax == 6) return qk<2, 6>(ri, af);  // the paper's production window
+  return qk<-1, -1>(ri, af);
 }
 
 int occupancy(QuantKernel k) {
@@ -348,6 +353,19 @@ bool row_fusion_enabled() {
   }
   return on == 1;
 }
+// SS_GLOBAL_TENSOR, NVFP4, plain layout: the amax pass runs inside the quantize
+// launch (quant_kernel<..., AF>).  SS_AMAX_FUSION=0 restores the separate
+// amax launch (A/B measurement).
+bool amax_fusion_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("SS_AMAX_FUSION");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+inline int64_t amax_units(int64_t nb) { return (2 * nb + ss::kAmaxUnitVecs - 1) / ss::kAmaxUnitVecs; }
+
 inline bool row_fused(const ss_tensor_io& t, int gmode) {
   const int64_t hpr = t.cols / 16;
   return gmode == SS_GLOBAL_ROW && t.rows > 0 && hpr >= ss::kTaskBlocks && hpr <= 8 * ss::kTaskBlocks &&
@@ -383,6 +401,16 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   std::lock_guard<std::mutex> lk(g_mu);
   Workspace* ws = nullptr;
   if (ss_status s = get_ws(dev, stream, &ws)) return s;
+
+  int ri = gmode == SS_GLOBAL_ROW ? 1 : 0;
+  for (int i = 0; i < count; i++) {
+    if (io[i].scale_layout == SS_SCALE_SWIZZLED) ri = std::max(ri, 1);
+    if (row_fused(io[i], gmode)) ri = 2;
+  }
+  // fused only where the search is ALU-bound (>= 4 offsets; the HBM crossover is ~3
+  // candidates): there the second read of the input is free
+  const bool af = gmode == SS_GLOBAL_TENSOR && ri == 0 && format == SS_FMT_NVFP4 && fmax - fmin >= 3 &&
+                  amax_fusion_enabled();
 
   // sizes of the largest launch (workspace grown once, before any launch)
   int64_t max_tasks = 0, max_segs = 0;
@@ -423,8 +451,11 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       ns[i] = io[i].rows * io[i].cols;
       amax[i] = ws->amax + i;
     }
-    if (ss_status s = amax_launch(ins.data(), ns.data(), ws->amax, count, false, cs, info.sms))
+    if (af) {  // the quantize launches fold their amax units into zeroed slots
+      if (cudaMemsetAsync(ws->amax, 0, 4 * (size_t)count, cs) != cudaSuccess) return SS_ERR_CUDA;
+    } else if (ss_status s = amax_launch(ins.data(), ns.data(), ws->amax, count, false, cs, info.sms)) {
       return s;
+    }
   } else if (gmode == SS_GLOBAL_DEVICE_AMAX) {
     for (int i = 0; i < count; i++) amax[i] = io[i].d_amax_bits;
   } else if (gmode == SS_GLOBAL_ROW) {
@@ -442,12 +473,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       return SS_ERR_CUDA;
   }
 
-  int ri = gmode == SS_GLOBAL_ROW ? 1 : 0;
-  for (int i = 0; i < count; i++) {
-    if (io[i].scale_layout == SS_SCALE_SWIZZLED) ri = std::max(ri, 1);
-    if (row_fused(io[i], gmode)) ri = 2;
-  }
-  QuantKernel k = pick_kernel(fmin, fmax, ri, format);
+  QuantKernel k = pick_kernel(fmin, fmax, ri, format, af);
   const int64_t slots = (int64_t)info.sms * occupancy(k);
   int i = 0;
   while (i < count) {
@@ -461,11 +487,12 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.part2 = ws->part2;
     b.tick = ws->tick;
     b.ctr = ws->ctr;
-#ifdef SS_COUNT_EVALS
-    if (!g_evals && cudaMalloc(&g_evals, 8) == cudaSuccess) cudaMemset(g_evals, 0, 8);
+#if defined(SS_COUNT_EVALS) || defined(SS_AF_TRACE)
+    if (!g_evals && cudaMalloc(&g_evals, 32) == cudaSuccess) cudaMemset(g_evals, 0, 32);
     b.evals = g_evals;
 #endif
     b.flags = ws->flags;
+    b.done = ws->done;
     bool sums = false;
     int64_t tk = 0, gr = 0, pk = 0;
     for (; i < count && b.n < ss::kMaxTensors; i++) {
@@ -492,8 +519,10 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         units = t.rows * upr;
       }
       const int64_t parts = parts_of(t, gmode);
-      // the kernel indexes units and partials with 32 bits: close the batch before overflow
-      if (b.n > 0 && (tk + units > (int64_t)INT32_MAX - ss::kCounters || pk + parts > (int64_t)INT32_MAX))
+      // the kernel indexes units, partials and amax units with 32 bits: close the batch before overflow
+      const int64_t au = af ? amax_units(nb) : 0;
+      if (b.n > 0 && (tk + units > (int64_t)INT32_MAX - ss::kCounters || pk + parts > (int64_t)INT32_MAX ||
+                      b.namax + au > (int64_t)INT32_MAX - ss::kWarps * 65536))
         break;
       QTensor& q = b.t[b.n++];
       q.in = reinterpret_cast<const uint8_t*>(t.in_bf16);
@@ -517,6 +546,9 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       q.part0 = (int32_t)pk;
       q.npart = (int32_t)parts;
       q.seg0 = gr;
+      q.a0 = b.namax;
+      q.na = (int32_t)au;
+      b.namax += (int32_t)au;
       tk += units;
       pk += parts;
       gr += psegs_of(parts);
@@ -952,6 +984,18 @@ SS_API unsigned long long ss_debug_take_evals(void) {
   cudaMemcpy(&h, g_evals, 8, cudaMemcpyDeviceToHost);
   cudaMemset(g_evals, 0, 8);
   return h;
+}
+#endif
+#ifdef SS_AF_TRACE
+/* Tools-only (libss_trace.so): fused-amax trace of the launches since the last
+ * call: {first CTA start, last amax-warp finish, summed search-warp wait,
+ * last warp finish}, globaltimer ns (synchronizes the device). */
+SS_API void ss_debug_take_aftrace(unsigned long long* out) {
+  if (!g_evals) return;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, g_evals, 32, cudaMemcpyDeviceToHost);
+  unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+  cudaMemcpy(g_evals, init, 32, cudaMemcpyHostToDevice);
 }
 #endif
 

@@ -26,6 +26,14 @@ constexpr int kPruneFrom = 3;                 // exact pruning for offsets f <= 
 constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
 constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
 constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk (32 KiB)
+#ifndef SS_AMAX_WARPS
+#define SS_AMAX_WARPS 2  // fused amax: 1 -> +0.8 %, 2 -> +4.6 %, 3 slower (C2 step, r = 8)
+#endif
+
+// fused amax (quant_kernel<..., AF>): warps per CTA that start as amax warps,
+// and the 16-B vectors of one amax unit (32 KiB)
+constexpr int kAmaxWarps = SS_AMAX_WARPS;
+constexpr int kAmaxUnitVecs = 2048;
 
 constexpr uint32_t kOneSixthBits = 0x3E2AAAABu;  // RN(1/6) (Alg. 1 line 2; R8)
 constexpr float kGlobalNumer = 2688.0f;          // 6 * 448: largest NVFP4 magnitude (R9)

@@ -12,6 +12,7 @@
 //   ss_search.cuh        candidate table, global scale, row / swizzle indexing,
 //                        batch descriptors, per-candidate loss, exact lower
 //                        bound and the selection steps
+//   ss_fused_amax.cuh    the amax warps of the fused-amax quantize kernel (a2)
 //   ss_quant_kernel.cuh  the search-quantize kernel (a1, a3-a7)
 //   ss_aux_kernels.cuh   amax (a2), error sums, per-row scale, dequantize (a8)
 //

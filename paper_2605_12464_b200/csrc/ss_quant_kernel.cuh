@@ -1,6 +1,6 @@
 // ss_quant_kernel.cuh — the search-quantize kernel (Algorithm 1 per block, a1 and a3-a7).
 #pragma once
-#include "ss_search.cuh"
+#include "ss_fused_amax.cuh"
 
 namespace ss {
 
@@ -13,8 +13,19 @@ namespace ss {
 // `b`/`j` index 16-element HALF-blocks (one per lane); a 32-element block is
 // the lane pair (2i, 2i + 1), whose even lane writes its scale, offset and
 // errors.
-template <int NEG, int POS, int RI, int FMT>
+//
+// AF (fused amax, gmode 1, RI 0): the batch's amax passes (a2) run inside
+// this launch.  The last kAmaxWarps warps of every CTA start as amax warps:
+// they draw 32-KiB amax units in tensor order from one counter, keep 8
+// coalesced 16-B loads in flight per lane, fold each unit's max into the
+// tensor's amax slot (atomicMax) and release-increment done[i]; when the
+// units run out they join the search.  A search warp waits (acquire) for
+// done[i] == na before its first item of tensor i.  The amax warps never
+// wait, so the HBM-bound amax runs ahead under the ALU-bound search and no
+// schedule can deadlock.
+template <int NEG, int POS, int RI, int FMT, bool AF = false>
 __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
+  static_assert(!AF || RI == 0, "fused amax: per-tensor G, plain layout");
   using F = Fmt<FMT>;
   constexpr int Pad = NEG < 0 ? F::kMaxCode : (NEG > POS ? NEG : POS);
   constexpr int TabW = F::SF ? 255 + 2 * Pad : 127 + 2 * Pad;
@@ -27,6 +38,23 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWarps + w;
+
+#ifdef SS_AF_TRACE
+  auto gtime = []() -> unsigned long long {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (AF && threadIdx.x == 0) atomicMin(p.evals + 0, gtime());
+#endif
+  if constexpr (AF) {
+    if (w >= kWarps - kAmaxWarps) {  // amax warp (a2), then a search warp
+      amax_warp(p, lane);
+#ifdef SS_AF_TRACE
+      if (lane == 0) atomicMax(p.evals + 1, gtime());
+#endif
+    }
+  }
 
   const float kinv = __uint_as_float(F::kInvVmaxBits);  // RN(1 / vmax) (R8)
   // A work item is up to kTaskBlocks half-blocks of one tensor, named by its
@@ -182,7 +210,18 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       cur_ti = -1;
     } else if (ti != cur_ti) {  // warp-uniform
       cur_ti = ti;
-      G = gscale(ti, it == first_item(T) && lane == 0);
+      if constexpr (AF) {  // wait until every amax unit of the tensor has been folded in
+#ifdef SS_AF_TRACE
+        const unsigned long long t0 = gtime();
+#endif
+        while (ld_acquire_gpu(p.done + ti) < (uint32_t)T.na) __nanosleep(256);
+#ifdef SS_AF_TRACE
+        if (lane == 0) atomicAdd(p.evals + 2, gtime() - t0);
+#endif
+        G = global_scale(ld_relaxed_gpu(T.amax), p.flags, it == first_item(T) && lane == 0, p.g_numer);
+      } else {
+        G = gscale(ti, it == first_item(T) && lane == 0);
+      }
     }
 
     cp_async_wait<kStages - 1>();  // this lane's copies of stage s have landed
@@ -352,6 +391,9 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 
     s = s + 1 == kStages ? 0 : s + 1;
   }
+#ifdef SS_AF_TRACE
+  if (AF && lane == 0) atomicMax(p.evals + 3, gtime());
+#endif
 #ifdef SS_COUNT_EVALS
   if (lane == 0 && p.evals) atomicAdd(p.evals, n_evals * 32ull / (unsigned long long)kHalves);
 #endif
@@ -360,6 +402,10 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     __threadfence();
     if (atomicAdd(p.ctr + kCounters, 1u) == gridDim.x * kWarps - 1) {
       for (int c = 0; c < kCounters; c++) p.ctr[c] = 0u;
+      if (AF) {
+        for (int i = 0; i < p.n; i++) p.done[i] = 0u;
+        p.done[kMaxTensors] = 0u;
+      }
       p.ctr[kCounters] = 0u;
     }
   }

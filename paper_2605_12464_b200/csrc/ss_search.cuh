@@ -111,6 +111,9 @@ struct QTensor {
   int16_t hpr, cpr, upr, cpu;
   int32_t part0;            // first error-sum partial (one per work item) of this tensor
   int32_t npart;            // error-sum partials of this tensor
+  // fused amax (AF launches, gmode 1): amax units [a0, a0 + na) of
+  // kAmaxUnitVecs 16-B vectors; their completion count goes to QuantBatch::done[i]
+  int32_t a0, na;
 };
 
 struct QuantBatch {
@@ -125,6 +128,9 @@ struct QuantBatch {
   uint32_t* tick;           // per tensor, zero and self re-arming
   uint32_t* ctr;            // [kCounters + 1] task counters + done count, zero and self re-arming
   uint32_t* flags;
+  uint32_t* done;           // AF launches: [kMaxTensors] finished amax units per tensor, then the
+                            // amax unit counter (zero, re-armed)
+  int32_t namax;            // AF launches: amax units of the batch
   unsigned long long* evals;  // SS_COUNT_EVALS builds: block-candidate evaluations executed
   QTensor t[kMaxTensors];
 };

@@ -28,8 +28,10 @@ def shard_rows(rows: int, rank: int, world: int) -> tuple:
 
 
 class CudaOps:
-    """libss.so batched calls on the current CUDA stream: one amax launch and
-    one quantize launch per 128 tensors of a step."""
+    """libss.so batched calls on the current CUDA stream.  Sharded (N > 1):
+    one amax launch and one quantize launch per 128 tensors of a step, the
+    all-reduce between them.  Unsharded: ``quantize_local`` — one fused
+    amax + quantize launch per 128 tensors (SS_GLOBAL_TENSOR)."""
 
     def __init__(self, fmin: int, fmax: int, want_err: bool = True, want_sums: bool = True,
                  want_offsets: bool = False):
@@ -47,6 +49,15 @@ class CudaOps:
 
     def alloc_out(self, x: torch.Tensor):
         return self.B.alloc_out(x, self.want_err, self.want_offsets, self.want_sums, True)
+
+    def quantize_local(self, xs, outs) -> int:
+        """Whole tensors on this device: per-tensor amax inside the quantize launch."""
+        live = [k for k, x in enumerate(xs) if x.shape[0] > 0]
+        self.B.quantize_batched([xs[k] for k in live], [outs[k] for k in live], fmin=self.fmin,
+                                fmax=self.fmax, gmode="tensor")
+        launches = (len(live) + 127) // 128
+        fused = self.fmax - self.fmin >= 3      # ss_api.cu: fusion where the search is ALU-bound
+        return launches * ((2 if self.want_sums else 1) + (0 if fused else 1))
 
     def quantize_all(self, xs, buf, outs) -> int:
         live = [k for k, x in enumerate(xs) if x.shape[0] > 0]
@@ -88,6 +99,8 @@ class RowShardQuantizer:
 
         N > 1: shard amaxes (one batched launch) -> the one exchange step (ONE
         max all-reduce of all the amaxes, 4 B per tensor) -> batched quantize.
+        N = 1 (no collective): ``ops.quantize_local`` when the ops have it —
+        the amax runs inside the quantize launch.
         N = 1 with pipeline_groups > 1: the tensors are cut into groups; the
         amax of every group is launched on a side stream up front and group k's
         quantize waits only for group k's amax, so the HBM-bound amax pass runs
@@ -98,6 +111,14 @@ class RowShardQuantizer:
         events there).
         """
         import torch.distributed as dist
+        if not self.collective and self.pipeline_groups <= 1 and hasattr(self.ops, "quantize_local"):
+            # unsharded: amax and quantize in one launch per 128 tensors
+            if hooks is not None:
+                hooks.before()
+            n = self.ops.quantize_local(shards, outs)
+            if hooks is not None:
+                hooks.after()
+            return n
         if not self.collective and self.pipeline_groups > 1 and torch.cuda.is_available() \
                 and len(shards) > 1 and shards[0].is_cuda:
             return self._pipelined(shards, outs, hooks)

@@ -354,7 +354,7 @@ def test_bench_launch_configuration_c2_sampled(ss, oracle_lib):
     ops = CudaOps(-8, 8, want_err=True, want_sums=True)
     outs = [ops.alloc_out(x) for x in xs]
     q = RowShardQuantizer(ShardPlan([(s.rows, s.cols) for s in specs], 0, 1), ops, device="cuda")
-    assert q.step(xs, outs) == 2 + 2 * 2      # amax x2, quant x2, sums x2
+    assert q.step(xs, outs) == 2 * 2          # fused amax+quant x2, sums x2
     # the pipelined variant (8 groups on two streams) gives the same outputs
     codes0 = [outs[k].codes.clone() for k in (0, 127, 251)]
     qp = RowShardQuantizer(ShardPlan([(s.rows, s.cols) for s in specs], 0, 1), ops, device="cuda",

@@ -1,0 +1,90 @@
+#!/usr/bin/env python
+"""A/B of the fused amax (quant_kernel<..., AF>) against the
+separate amax launch, on the bench workloads.
+
+    python tools/fusebench.py [--configs c1_gauss4096,c2_qwen3_8b_weights] [--windows -8:8,0:0]
+
+Per config and window, one JSON line with the median time (CUDA events, 3
+warm-ups, `--reps` timed calls; inputs rotated over copies when the workload
+fits in L2) of
+  sep    ss_tensor_amax_batched + ss_quantize_nvfp4_batched(DEVICE_AMAX)
+  fused  ss_quantize_nvfp4_batched(TENSOR)   (amax units inside the launch)
+and whether the fused outputs (codes, scales, errors, sums, G) equal the
+separate path's bit for bit.  Run with SS_AMAX_FUSION=0 to time the TENSOR
+call without fusion (the library reads it once per process).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c1_gauss4096,c2_qwen3_8b_weights,c4_llama70b_kv")
+    ap.add_argument("--windows", default="-8:8,0:0")
+    ap.add_argument("--reps", type=int, default=7)
+    a = ap.parse_args()
+    import torch
+    import ssgen
+    import paper_2605_12464_b200 as ss
+    dev = torch.device("cuda", 0)
+    wins = [tuple(int(v) for v in w.split(":")) for w in a.windows.split(",")]
+    for cfg in a.configs.split(","):
+        specs = ssgen.workload(cfg)
+        xs = [ssgen.generate(s.kind, s.rows, s.cols, seed=ssgen.workloads.BASE_SEED, tid=s.tid,
+                             device=dev) for s in specs]
+        n = sum(x.numel() for x in xs)
+        copies = max(1, min(40, (1 << 30) // (2 * n)))
+        sets = [xs] + [[x.clone() for x in xs] for _ in range(copies - 1)]
+        outs_a = [ss.alloc_out(x, want_offsets=True) for x in xs]
+        outs_b = [ss.alloc_out(x, want_offsets=True) for x in xs]
+        amax = torch.zeros(len(xs), dtype=torch.int32, device=dev)
+
+        def timed(fn):
+            for i in range(3):
+                fn(sets[i % copies])
+            ts = []
+            for i in range(a.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn(sets[i % copies])
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return sorted(ts)[len(ts) // 2]
+
+        for fmin, fmax in wins:
+            def sep(s):
+                ss.tensor_amax_batched(s, out=amax)
+                ss.quantize_batched(s, outs_a, fmin=fmin, fmax=fmax, gmode="device_amax", amax=amax)
+
+            def fused(s):
+                ss.quantize_batched(s, outs_b, fmin=fmin, fmax=fmax, gmode="tensor")
+
+            t_sep = timed(sep)
+            t_fused = timed(fused)
+            sep(xs)
+            fused(xs)
+            torch.cuda.synchronize()
+            same = all(torch.equal(getattr(oa, f), getattr(ob, f))
+                       for oa, ob in zip(outs_a, outs_b)
+                       for f in ("codes", "scales", "err", "offsets", "sums", "G")
+                       if getattr(oa, f) is not None)
+            print(json.dumps({"config": cfg, "window": [fmin, fmax], "tensors": len(xs), "elements": n,
+                              "fusion_env": os.environ.get("SS_AMAX_FUSION", "1"),
+                              "sep_ms": t_sep, "fused_ms": t_fused, "speedup": t_sep / t_fused,
+                              "sep_gbs": 2 * n / t_sep / 1e6, "fused_gbs": 2 * n / t_fused / 1e6,
+                              "bit_identical": bool(same),
+                              "status": ss.device_status()}), flush=True)
+        del xs, sets, outs_a, outs_b
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

@@ -21,7 +21,17 @@ fi
 if has ncu; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"quant_kernel|amax_kernel|sums_kernel" -c 40 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --profile --steps 2 --warmup 1 > gpurun_out/ncu_launch_$TAG.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:quant_kernel -s 3 -c 1 -o gpurun_out/quant_full_$TAG python tools/kbench.py one --variants base --layers 2 --reps 1 --windows=-8:8 > gpurun_out/ncu_full_$TAG.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:quant_kernel -s 2 -c 1 -o gpurun_out/quant_fused_$TAG python tools/aftrace.py run --variant base --gmode tensor --layers 18 --windows=-8:8 > gpurun_out/ncu_fused_$TAG.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:amax_kernel -s 3 -c 1 -o gpurun_out/amax_full_$TAG python tools/kbench.py one --variants base --layers 2 --reps 1 --windows=-8:8 > gpurun_out/ncu_amax_$TAG.log 2>&1
+  # summarise on the box (each full report with source is ~30 MB; gpurun returns <= 64 MiB)
+  for r in quant_full quant_fused amax_full; do
+    if [ -f gpurun_out/${r}_$TAG.ncu-rep ]; then
+      python tools/ncu_summary.py full gpurun_out/${r}_$TAG.ncu-rep > gpurun_out/${r}_$TAG.md 2>&1
+      ncu -i gpurun_out/${r}_$TAG.ncu-rep --page raw --csv > gpurun_out/${r}_$TAG.raw.csv 2>/dev/null
+      [ -n "$KEEP_REP" ] && [ "$r" = "$KEEP_REP" ] || rm -f gpurun_out/${r}_$TAG.ncu-rep
+    fi
+  done
+  python tools/ncu_summary.py launches gpurun_out/launches_$TAG.csv > gpurun_out/launches_$TAG.md 2>&1
 fi
 if has sweep; then
   timeout 1500 python tools/sweep.py --out gpurun_out/sweep_$TAG.jsonl > gpurun_out/sweep_$TAG.log 2>&1; echo "sweep exit $?" >> gpurun_out/sweep_$TAG.log
