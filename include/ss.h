@@ -217,8 +217,12 @@ typedef struct {
  * Batched ScaleSearch quantization: every tensor of `tensors[0..count)` (a
  * HOST array) with one window and one global-scale mode, in as few launches
  * as possible (one persistent grid per 128 tensors, so a step over many
- * small tensors has no per-tensor tail).  SS_GLOBAL_TENSOR runs one batched
- * amax launch first.  Results are bit-identical to per-tensor calls.
+ * small tensors has no per-tensor tail).  SS_GLOBAL_TENSOR computes each
+ * tensor's amax inside the quantize launch when the format is NVFP4,
+ * the scales are linear and the window has >= 4 offsets (amax warps run ahead
+ * of the search; SS_AMAX_FUSION=0 in the environment
+ * disables it), else in one batched amax launch first.  Results are
+ * bit-identical either way and to per-tensor calls.
  */
 SS_API ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min,
                                     int f_max, int global_scale_mode, void* stream);
