@@ -365,7 +365,8 @@ def run_ours(a, rank, world, local_rank):
     peak = 148 * FP32_LANES_PER_SM * pk["sm_max_mhz"] * 1e6 / 1e12
     # unsharded runs fuse the amax pass into the quantize launch when the window has
     # >= 4 offsets (ss_api.cu): that kernel reads the input twice
-    fused = not dist_on and a.fmax - a.fmin >= 3
+    from paper_2605_12464_b200.dist import amax_fused
+    fused = not dist_on and amax_fused([x.numel() for x in shards], a.fmin, a.fmax)
     bytes_q = n_local * ((2.0 if fused else 0.0) + 2.0 + 0.5 + 0.0625 + 0.5)  # [amax] + in + codes + scales + err
     hbm_achieved = bytes_q / (quant_ms * 1e-3) / 1e9
     traffic = None

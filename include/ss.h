@@ -237,6 +237,27 @@ SS_API ss_status ss_quantize_batched_fmt(const ss_tensor_io* tensors, int count,
  *   codes [rows][cols/2] u8 (8-B aligned), scales [rows][cols/16] u8,
  *   d_global_scale nullable (NULL => G = 1), out_bf16 [rows][cols] (16-B aligned).
  */
+/*
+ * FP32-input ScaleSearch NVFP4 through the one-thread block routine of
+ * include/ss_device.cuh (the search a fused producer, e.g. attention's P
+ * tile, runs in registers).  One thread per block.
+ *   in              DEVICE float [rows][cols], 16-B aligned, cols % 16 == 0
+ *   f_min, f_max    window as in ss_quantize_nvfp4_ex (clamped to +-126)
+ *   d_global_scale  DEVICE float G (y = RN(x * G), R9), nullable => G = 1;
+ *                   e.g. 2688 / amax, or a fixed scale for bounded data
+ *   out_codes       [rows][cols/2] u8; out_scales [rows][cols/16] u8 (linear)
+ *   out_err         nullable float2 [nb] {err_best, err_base}; out_offset
+ *                   nullable int8 [nb] f*
+ * Same contract as the bf16 path: for bf16-representable inputs and the
+ * same G, outputs are bit-identical to ss_quantize_nvfp4_ex.  A non-finite
+ * input sets SS_FLAG_NONFINITE (poll ss_get_device_status).  Enqueued on
+ * `stream`, no host sync.
+ */
+SS_API ss_status ss_quantize_nvfp4_f32(const float* in, int64_t rows, int64_t cols, int f_min,
+                                       int f_max, const float* d_global_scale, uint8_t* out_codes,
+                                       uint8_t* out_scales, float* out_err, int8_t* out_offset,
+                                       void* stream);
+
 SS_API ss_status ss_dequantize_nvfp4(const uint8_t* codes, const uint8_t* scales, int64_t rows,
                               int64_t cols, const float* d_global_scale, void* out_bf16,
                               void* stream);

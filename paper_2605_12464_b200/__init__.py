@@ -20,6 +20,7 @@ from ._binding import (  # noqa: F401
     lib,
     quantize,
     quantize_batched,
+    quantize_f32,
     quantize_host,
     quantize_host_batched,
     quantize_simple,

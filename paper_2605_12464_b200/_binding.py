@@ -135,6 +135,8 @@ def lib():
             L.ss_code_bytes.argtypes = [i64, i64, I]
             L.ss_quantize_batched_fmt.restype = I
             L.ss_quantize_batched_fmt.argtypes = [ctypes.POINTER(TensorIO), I, I, I, I, I, P]
+            L.ss_quantize_nvfp4_f32.restype = I
+            L.ss_quantize_nvfp4_f32.argtypes = [P, i64, i64, I, I, P, P, P, P, P, P]
             L.ss_dequantize_nvfp4.restype = I
             L.ss_dequantize_nvfp4.argtypes = [P, P, i64, i64, P, P, P]
             L.ss_quantize_nvfp4_host.restype = I
@@ -288,6 +290,27 @@ def quantize_batched(xs, outs, radius=None, fmin=None, fmax=None, gmode: str = "
         _check(lib().ss_quantize_batched_fmt(arr, n, lo, hi, gm, FORMATS[fmt][0], _stream_ptr(stream)),
                "ss_quantize_batched_fmt")
     return outs
+
+
+def quantize_f32(x, radius=None, fmin=None, fmax=None, G=None, want_err: bool = True,
+                 want_offsets: bool = True, stream=None):
+    """FP32 [rows][cols] CUDA tensor through the one-thread block routine
+    (ss_quantize_nvfp4_f32); ``G``: device float32 [1] global scale or None (G = 1).
+    Returns QuantOut (sums / G fields None)."""
+    import torch
+    assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+    rows, cols = x.shape
+    lo, hi = _window(radius, fmin, fmax)
+    dev = x.device
+    out = QuantOut(torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev),
+                   torch.empty(rows, cols // 16, dtype=torch.uint8, device=dev),
+                   torch.empty(rows * cols // 16, 2, dtype=torch.float32, device=dev) if want_err else None,
+                   torch.empty(rows * cols // 16, dtype=torch.int8, device=dev) if want_offsets else None,
+                   None, None)
+    _check(lib().ss_quantize_nvfp4_f32(_ptr(x), rows, cols, lo, hi, _ptr(G), _ptr(out.codes),
+                                       _ptr(out.scales), _ptr(out.err), _ptr(out.offsets),
+                                       _stream_ptr(stream)), "ss_quantize_nvfp4_f32")
+    return out
 
 
 def quantize_simple(x, radius: int, gmode: str, codes, scales, err=None, stream=None):

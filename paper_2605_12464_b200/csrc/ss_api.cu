@@ -408,9 +408,17 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     if (row_fused(io[i], gmode)) ri = 2;
   }
   // fused only where the search is ALU-bound (>= 4 offsets; the HBM crossover is ~3
-  // candidates): there the second read of the input is free
+  // candidates) and where most of the amax can overlap a search:
+  // the first tensor's amax is exposed, so not when it holds most of the elements
+  // (a single tensor: the dedicated amax kernel is faster)
+  int64_t n_all = 0, n_first = -1;
+  for (int i = 0; i < count; i++) {
+    const int64_t n = io[i].rows * io[i].cols;
+    if (n > 0 && n_first < 0) n_first = n;
+    n_all += n;
+  }
   const bool af = gmode == SS_GLOBAL_TENSOR && ri == 0 && format == SS_FMT_NVFP4 && fmax - fmin >= 3 &&
-                  amax_fusion_enabled();
+                  2 * n_first <= n_all && amax_fusion_enabled();
 
   // sizes of the largest launch (workspace grown once, before any launch)
   int64_t max_tasks = 0, max_segs = 0;
@@ -752,6 +760,45 @@ ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {
     case SS_FMT_NVFP4_B256: ss::dequant_kernel<ss::kFmtNVFP4B256><<<grid, 256, 0, cs>>>(p); break;
     default: ss::dequant_kernel<ss::kFmtNVFP4><<<grid, 256, 0, cs>>>(p); break;
   }
+  return launch_status();
+}
+
+ss_status ss_quantize_nvfp4_f32(const float* in, int64_t rows, int64_t cols, int f_min, int f_max,
+                                const float* d_global_scale, uint8_t* out_codes, uint8_t* out_scales,
+                                float* out_err, int8_t* out_offset, void* stream) {
+  if (rows < 0 || cols < 0 || cols % 16 != 0 || f_min > 0 || f_max < 0) return SS_ERR_INVALID_ARG;
+  const int64_t nb = rows * cols / 16;
+  if (nb > 0 && (!in || !out_codes || !out_scales)) return SS_ERR_INVALID_ARG;
+  if (!aligned(in, 16) || !aligned(out_codes, 8) || !aligned(out_err, 8) || !aligned(d_global_scale, 4))
+    return SS_ERR_ALIGNMENT;
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  if (nb == 0) return SS_OK;
+  Workspace* ws = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (ss_status s = get_ws(dev, stream, &ws)) return s;
+  }
+  ss::F32Params p;
+  p.in = reinterpret_cast<const float4*>(in);
+  p.nb = nb;
+  p.fmin = std::max(f_min, -126);
+  p.fmax = std::min(f_max, 126);
+  p.g = d_global_scale;
+  p.codes = reinterpret_cast<uint2*>(out_codes);
+  p.scales = out_scales;
+  p.err = reinterpret_cast<float2*>(out_err);
+  p.offsets = out_offset;
+  p.flags = ws->flags;
+  void (*k)(ss::F32Params) = ss::quant_f32_kernel<-1, -1>;
+  if (p.fmin == -8 && p.fmax == 8) k = ss::quant_f32_kernel<8, 8>;
+  else if (p.fmin == -2 && p.fmax == 6) k = ss::quant_f32_kernel<2, 6>;
+  else if (p.fmin == -1 && p.fmax == 1) k = ss::quant_f32_kernel<1, 1>;
+  else if (p.fmin == 0 && p.fmax == 0) k = ss::quant_f32_kernel<0, 0>;
+  const int64_t want = (nb + 255) / 256;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)info.sms * 8));
+  k<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   return launch_status();
 }
 

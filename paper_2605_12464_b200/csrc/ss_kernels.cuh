@@ -15,6 +15,8 @@
 //   ss_fused_amax.cuh    the amax warps of the fused-amax quantize kernel (a2)
 //   ss_quant_kernel.cuh  the search-quantize kernel (a1, a3-a7)
 //   ss_aux_kernels.cuh   amax (a2), error sums, per-row scale, dequantize (a8)
+//   ss_block.cuh         the one-thread block-search routine (include/ss_device.cuh)
+//                        and the FP32-input kernel built on it
 //
 // Work decomposition: a WARP TASK is 64 consecutive
 // 16-element blocks of one tensor, two per lane; a launch covers a batch of up
@@ -41,3 +43,4 @@
 #include "ss_search.cuh"
 #include "ss_quant_kernel.cuh"
 #include "ss_aux_kernels.cuh"
+#include "ss_block.cuh"

@@ -19,6 +19,21 @@ namespace ss {
 // ---------------------------------------------------------------------------
 // UE8M0 (SF = 1): one half of 255 + 2*Pad entries, code = clamp(k, 0, 254),
 // entry = {rho, rho, code << 16, bits(-s)} (every code is a scale, R19).
+// UE4M3 candidate for unclamped code k: half 0 (c0 == 0) maps k <= 0 to the
+// zero scale, half 1 clamps to [1, 126]; both clamp at 126.
+__device__ __forceinline__ int clamp_code(int half, int k) {
+  const int code = half == 0 ? (k <= 0 ? 0 : k) : (k < 1 ? 1 : k);
+  return code > 126 ? 126 : code;
+}
+// {rho, rho, (-s as f16) | code << 16, 0} of UE4M3 code 0..126 (code 0: the zero scale)
+__device__ __forceinline__ uint4 cand_entry(int code) {
+  if (code == 0) return make_uint4(0u, 0u, 0x8000u, 0u);
+  const uint16_t sh = e4m3_to_f16((uint32_t)code);
+  const float rho = __frcp_rn(f16_to_f32(sh));  // IEEE RN(1/s), not MUFU (R7)
+  return make_uint4(__float_as_uint(rho), __float_as_uint(rho),
+                    (uint32_t)(sh ^ 0x8000u) | ((uint32_t)code << 16), 0u);
+}
+
 template <int Pad, int SF>
 __device__ __forceinline__ void build_cand_table(uint4* tab) {
   if constexpr (SF == 1) {
@@ -34,19 +49,7 @@ __device__ __forceinline__ void build_cand_table(uint4* tab) {
   constexpr int TabW = 127 + 2 * Pad;
   for (int i = threadIdx.x; i < 2 * TabW; i += blockDim.x) {
     const int half = i / TabW;
-    const int k = i - half * TabW - Pad;
-    int code = half == 0 ? (k <= 0 ? 0 : k) : (k < 1 ? 1 : k);
-    code = code > 126 ? 126 : code;
-    uint4 e;
-    if (code == 0) {
-      e = make_uint4(0u, 0u, 0x8000u, 0u);
-    } else {
-      const uint16_t sh = e4m3_to_f16((uint32_t)code);
-      const float rho = __frcp_rn(f16_to_f32(sh));  // IEEE RN(1/s), not MUFU (R7)
-      e = make_uint4(__float_as_uint(rho), __float_as_uint(rho),
-                     (uint32_t)(sh ^ 0x8000u) | ((uint32_t)code << 16), 0u);
-    }
-    tab[i] = e;
+    tab[i] = cand_entry(clamp_code(half, i - half * TabW - Pad));
   }
 }
 

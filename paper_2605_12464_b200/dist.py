@@ -27,6 +27,14 @@ def shard_rows(rows: int, rank: int, world: int) -> tuple:
     return lo, min(rows, lo + per)
 
 
+def amax_fused(numels: Sequence[int], fmin: int, fmax: int) -> bool:
+    """Whether libss fuses the amax into the quantize launch for a TENSOR-mode
+    NVFP4 batch (the rule of ss_api.cu quantize_core): >= 4 offsets and a
+    first tensor holding at most half of the elements."""
+    live = [n for n in numels if n > 0]
+    return bool(live) and fmax - fmin >= 3 and 2 * live[0] <= sum(live)
+
+
 class CudaOps:
     """libss.so batched calls on the current CUDA stream.  Sharded (N > 1):
     one amax launch and one quantize launch per 128 tensors of a step, the
@@ -56,7 +64,7 @@ class CudaOps:
         self.B.quantize_batched([xs[k] for k in live], [outs[k] for k in live], fmin=self.fmin,
                                 fmax=self.fmax, gmode="tensor")
         launches = (len(live) + 127) // 128
-        fused = self.fmax - self.fmin >= 3      # ss_api.cu: fusion where the search is ALU-bound
+        fused = amax_fused([xs[k].numel() for k in live], self.fmin, self.fmax)
         return launches * ((2 if self.want_sums else 1) + (0 if fused else 1))
 
     def quantize_all(self, xs, buf, outs) -> int:

@@ -99,3 +99,28 @@ def test_binding_raises_not_falls_back():
     from paper_2605_12464_b200 import _binding as B
     e = B.SSError(B.SS_ERR_UNSUPPORTED_DEVICE, "x")
     assert isinstance(e, RuntimeError)
+
+
+def test_device_header_compiles_standalone(tmp_path):
+    """include/ss_device.cuh is usable from a user's own kernel (nvcc, sm_100a),
+    with no library symbols needed."""
+    import shutil
+    import subprocess
+    if not shutil.which("nvcc"):
+        pytest.skip("nvcc not available")
+    src = tmp_path / "user.cu"
+    src.write_text(
+        '#include "ss_device.cuh"\n'
+        "__global__ void user_kernel(const float* x, uint2* codes, unsigned char* scales) {\n"
+        "  float y[16];\n"
+        "  for (int i = 0; i < 16; i++) y[i] = x[16 * threadIdx.x + i];\n"
+        "  if (threadIdx.x & 1) return;   // divergent callers are fine\n"
+        "  ss::Nvfp4Block r = ss::search_nvfp4_block<8, 8>(y);\n"
+        "  ss::Nvfp4Block q = ss::search_nvfp4_block<-1, -1>(y, -2, 6);\n"
+        "  codes[threadIdx.x] = r.codes;\n"
+        "  scales[threadIdx.x] = (unsigned char)(r.scale ^ q.scale);\n"
+        "}\n")
+    res = subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-c",
+                          "-I", os.path.join(ROOT, "include"), "-o", str(tmp_path / "user.o"), str(src)],
+                         capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr

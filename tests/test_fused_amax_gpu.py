@@ -78,7 +78,7 @@ def test_fused_corner_tensors(ss):
 
 @pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
 def test_fused_nonfinite_flag(ss, bad):
-    xs = _batch(6, seed=8)
+    xs = [torch.ones(1, 16, dtype=torch.bfloat16, device="cuda")] + _batch(6, seed=8)   # small first: fused
     xs[3] = xs[3].clone()
     xs[3].view(-1)[xs[3].numel() // 2] = bad
     a, fa = _run(ss, xs, -8, 8, fused=True)
