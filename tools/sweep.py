@@ -54,9 +54,15 @@ def measure(torch, ss, groups, fmin, fmax, reps=5, fmt="nvfp4"):
             ss.quantize_batched(groups[i], outs[i], fmin=fmin, fmax=fmax, gmode="device_amax",
                                 amax=amax[i], fmt=fmt)
 
-    def e2e(i):
+    def e2e_sep(i):
         ss.tensor_amax_batched(groups[i], out=amax[i])
         q_only(i)
+
+    def e2e(i):   # the library's per-tensor-G call (amax fused into the launch where it pays)
+        if mx:
+            q_only(i)
+        else:
+            ss.quantize_batched(groups[i], outs[i], fmin=fmin, fmax=fmax, gmode="tensor", fmt=fmt)
 
     for i in range(len(groups)):
         ss.tensor_amax_batched(groups[i], out=amax[i])
@@ -69,7 +75,7 @@ def measure(torch, ss, groups, fmin, fmax, reps=5, fmt="nvfp4"):
         q_only(0)
         nb = sum(x.numel() for x in groups[0]) // 16
         res["evaluated_per_block"] = L.ss_debug_take_evals() / nb * (2 if mx else 1)
-    for name, fn in (("quant", q_only), ("amax_quant", e2e)):
+    for name, fn in (("quant", q_only), ("amax_quant_sep", e2e_sep), ("amax_quant", e2e)):
         for w in range(2):
             fn(w % len(groups))
         torch.cuda.synchronize()
@@ -127,7 +133,9 @@ def report(cfg, fmin, fmax, res, n, ceff, s_best, s_base, hist, hbm, mhz, extra=
     t_roof = max(bytes_q / (hbm * 1e9), ops / alu_peak)
     line = {"config": cfg, "format": fmt, "window": [fmin, fmax], "elements": n, "c_eff": ceff,
             "quant_ms": res["quant"], "amax_quant_ms": res["amax_quant"],
+            "amax_quant_sep_ms": res.get("amax_quant_sep"),
             "quant_bf16_gbs": 2 * n / tq / 1e9, "e2e_bf16_gbs": 2 * n / te / 1e9,
+            "e2e_sep_bf16_gbs": 2 * n / (res["amax_quant_sep"] * 1e-3) / 1e9 if res.get("amax_quant_sep") else None,
             "bound": "alu" if ops / alu_peak > bytes_q / (hbm * 1e9) else "hbm",
             "roofline_frac": t_roof / tq, "alu_frac": ops / alu_peak / tq,
             "hbm_frac": bytes_q / (hbm * 1e9) / tq,
@@ -150,7 +158,7 @@ def main():
     import ssgen
     import paper_2605_12464_b200 as ss
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,c2,c3,c4,c5,formats")
+    ap.add_argument("--configs", default="c1,c2,c3,c4,f32,c5,formats")
     ap.add_argument("--c5-gib", default="1,8")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -187,6 +195,39 @@ def main():
         xs = gen(ssgen.workload("c4_llama70b_kv"))
         lines.append(report("c4_llama70b_kv", -8, 8, *measure(torch, ss, [xs], -8, 8, reps=3), hbm, mhz))
         del xs
+        torch.cuda.empty_cache()
+    if "f32" in cfgs:   # the one-thread block routine through ss_quantize_nvfp4_f32
+        x = gen(ssgen.workload("c3_act_student_t"))[0]
+        xf = x.float()
+        amax = ss.tensor_amax(x)
+        out = ss.quantize(x, radius=8, gmode="tensor")
+        G = out.G
+        for w in [(-8, 8), (-2, 6), (0, 0)]:
+            def run_f32():
+                ss.quantize_f32(xf, fmin=w[0], fmax=w[1], G=G)
+
+            def run_bf16():
+                ss.quantize(x, fmin=w[0], fmax=w[1], gmode="device_amax", amax=amax, out=out)
+            t = {}
+            for name, fn in (("f32", run_f32), ("bf16", run_bf16)):
+                for _ in range(3):
+                    fn()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(10):
+                    fn()
+                e1.record()
+                torch.cuda.synchronize()
+                t[name] = e0.elapsed_time(e1) / 10
+            n = x.numel()
+            line = {"config": "f32_routine_c3_shape", "window": list(w), "elements": n,
+                    "f32_ms": t["f32"], "bf16_kernel_ms": t["bf16"],
+                    "f32_gelem_s": n / t["f32"] / 1e6, "bf16_gelem_s": n / t["bf16"] / 1e6,
+                    "f32_in_gbs": 4 * n / t["f32"] / 1e6}
+            print(json.dumps(line), flush=True)
+            lines.append(line)
+        del x, xf, out
         torch.cuda.empty_cache()
     if "c5" in cfgs:
         for gib in [int(v) for v in a.c5_gib.split(",")]:
