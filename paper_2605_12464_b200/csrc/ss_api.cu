@@ -136,6 +136,29 @@ ss_status launch_status() {
   return e == cudaSuccess ? SS_OK : SS_ERR_CUDA;
 }
 
+// Launch with programmatic stream serialization (PDL): the grid may start
+// while the previous kernel in the stream is finishing; the kernel itself
+// calls griddepcontrol.wait before touching anything the predecessor
+// produces (quant_kernel, sums_kernel).
+template <typename Arg>
+ss_status launch_pdl(void (*k)(Arg), int grid, int block, cudaStream_t st, const Arg& arg) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, k, arg) != cudaSuccess) {
+    cudaGetLastError();
+    return SS_ERR_CUDA;
+  }
+  return SS_OK;
+}
+
 // ---- amax --------------------------------------------------------------------
 int amax_grid(int sms) {
   static int occ = 0;
@@ -567,12 +590,10 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.nsegs = gr;
     const int64_t want = (tk + ss::kWarps - 1) / ss::kWarps;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, slots));
-    k<<<grid, ss::kThreads, 0, cs>>>(b);
-    if (ss_status s = launch_status()) return s;
+    if (ss_status s = launch_pdl(k, grid, ss::kThreads, cs, b)) return s;
     if (sums) {
       const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(gr, sums_grid(info.sms)));
-      ss::sums_kernel<<<g2, ss::kThreads, 0, cs>>>(b);
-      if (ss_status s = launch_status()) return s;
+      if (ss_status s = launch_pdl(ss::sums_kernel, g2, ss::kThreads, cs, b)) return s;
     }
   }
   return SS_OK;

@@ -14,6 +14,7 @@ namespace ss {
 // same and reduced (warp redux + smem) into ONE atomicMax per (CTA, tensor).
 __global__ void __launch_bounds__(kThreads) amax_kernel(const __grid_constant__ AmaxBatch p) {
   __shared__ uint32_t red[kWarps];
+  pdl_launch_dependents();  // the quantize grid may launch now; it waits for this one (pdl_wait)
   const uint32_t M = 0x7FFF7FFFu;
   const int64_t per = (p.nchunks + gridDim.x - 1) / gridDim.x;
   const int64_t c_lo = (int64_t)blockIdx.x * per;
@@ -91,6 +92,7 @@ __device__ __forceinline__ double2 cta_sum(const double2* src, int64_t n, double
 __global__ void __launch_bounds__(kThreads) sums_kernel(const __grid_constant__ QuantBatch p) {
   __shared__ double2 red[kWarps];
   __shared__ uint32_t last;
+  pdl_wait();  // launched early (PDL): the quantize grid's partials must be complete
   int ti = 0;
   for (int64_t sg = blockIdx.x; sg < p.nsegs; sg += gridDim.x) {
     while (ti + 1 < p.n && p.t[ti + 1].seg0 <= sg) ti++;
@@ -144,6 +146,7 @@ struct RowBatch {
 };
 
 __global__ void __launch_bounds__(kThreads) rowscale_kernel(const __grid_constant__ RowBatch p) {
+  pdl_launch_dependents();
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * kWarps;
   int ti = 0;

@@ -116,6 +116,16 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// The dependent grid may start before its predecessor finishes; pdl_wait()
+// blocks until the predecessor grid has completed and its writes are visible
+// (a no-op without the launch attribute).  pdl_launch_dependents() lets the
+// next grid in the stream launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- inter-warp signalling (the fused amax of quant_kernel<..., AF>) -------
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;

@@ -35,6 +35,11 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 
   build_cand_table<Pad, F::SF>(tab);
   __syncthreads();
+  // Launched with PDL: everything above overlaps the predecessor (amax /
+  // row-scale / previous sums grid); the scheduler counters, amax slots and
+  // outputs are touched only after it has completed.
+  pdl_wait();
+  pdl_launch_dependents();  // the error-sum grid may launch early (it waits for this one)
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWarps + w;
