@@ -14,7 +14,9 @@ namespace ss {
 // same and reduced (warp redux + smem) into ONE atomicMax per (CTA, tensor).
 __global__ void __launch_bounds__(kThreads) amax_kernel(const __grid_constant__ AmaxBatch p) {
   __shared__ uint32_t red[kWarps];
+#if SS_AMAX_PDL_TRIGGER
   pdl_launch_dependents();  // the quantize grid may launch now; it waits for this one (pdl_wait)
+#endif
   const uint32_t M = 0x7FFF7FFFu;
   const int64_t per = (p.nchunks + gridDim.x - 1) / gridDim.x;
   const int64_t c_lo = (int64_t)blockIdx.x * per;
@@ -146,7 +148,9 @@ struct RowBatch {
 };
 
 __global__ void __launch_bounds__(kThreads) rowscale_kernel(const __grid_constant__ RowBatch p) {
+#if SS_AMAX_PDL_TRIGGER
   pdl_launch_dependents();
+#endif
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * kWarps;
   int ti = 0;

@@ -26,6 +26,13 @@ constexpr int kPruneFrom = 3;                 // exact pruning for offsets f <= 
 constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
 constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
 constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk (32 KiB)
+#ifndef SS_AMAX_PDL_TRIGGER
+// 1: the amax / row-scale grids let the quantize grid launch early (PDL
+// trigger).  Measured slower (C3 r = 8: 339 vs 313 us per amax + quantize call),
+// so the quantize grid launches when they complete; its own PDL launch still
+// hides the launch gap (C1 r = 8 quantize: 52 -> 47 us).
+#define SS_AMAX_PDL_TRIGGER 0
+#endif
 #ifndef SS_AMAX_WARPS
 #define SS_AMAX_WARPS 2  // fused amax: 1 -> +0.8 %, 2 -> +4.6 %, 3 slower (C2 step, r = 8)
 #endif
