@@ -158,7 +158,7 @@ def main():
     import ssgen
     import paper_2605_12464_b200 as ss
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,c2,c3,c4,f32,c5,formats")
+    ap.add_argument("--configs", default="c1,c2,c3,c4,f32,paper_tab,c5,formats")
     ap.add_argument("--c5-gib", default="1,8")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -228,6 +228,52 @@ def main():
             print(json.dumps(line), flush=True)
             lines.append(line)
         del x, xf, out
+        torch.cuda.empty_cache()
+    if "paper_tab" in cfgs:   # tab:quant_overhead: FP32 2048x2048 Gaussian, G given
+        gen_ = torch.Generator(device="cpu").manual_seed(seed)
+        x32 = torch.randn(2048, 2048, generator=gen_).to(dev)
+        xb = x32.to(torch.bfloat16)
+        amax = ss.tensor_amax(xb)
+        G = ss.quantize(xb, radius=0, gmode="tensor").G
+        copies = 64                                   # 64 x 16.8 MB > L2 for the cold runs
+        x32s = [x32] + [x32.clone() for _ in range(copies - 1)]
+        xbs = [xb] + [xb.clone() for _ in range(copies - 1)]
+        out_b = ss.alloc_out(xb, want_err=False, want_offsets=False, want_sums=False, want_g=False)
+        for w in [(0, 0), (-1, 1), (-2, 6)]:
+            t = {}
+            fns = (("f32", lambda i: ss.quantize_f32(x32s[i], fmin=w[0], fmax=w[1], G=G, want_err=False,
+                                                     want_offsets=False)),
+                   ("bf16", lambda i: ss.quantize(xbs[i], fmin=w[0], fmax=w[1], gmode="device_amax",
+                                                  amax=amax, out=out_b)))
+            for name, fn in fns:
+                for mode, rot in (("hot", 1), ("cold", copies)):
+                    # 64 calls captured in a CUDA graph: device time without host launch overhead
+                    st = torch.cuda.Stream()
+                    st.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(st):
+                        for i in range(3):
+                            fn(i % rot)
+                    torch.cuda.synchronize()
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=st):
+                        for i in range(64):
+                            fn(i % rot)
+                    g.replay()
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(5):
+                        g.replay()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    t["%s_%s_ms" % (name, mode)] = e0.elapsed_time(e1) / (5 * 64)
+                    del g
+            paper = {(0, 0): 0.0258, (-1, 1): 0.0328, (-2, 6): 0.0449}[w]
+            line = {"config": "paper_tab_quant_overhead_2048sq_fp32", "window": list(w),
+                    "elements": x32.numel(), "paper_ms_unstated_hw": paper, **t}
+            print(json.dumps(line), flush=True)
+            lines.append(line)
+        del x32s, xbs
         torch.cuda.empty_cache()
     if "c5" in cfgs:
         for gib in [int(v) for v in a.c5_gib.split(",")]:
