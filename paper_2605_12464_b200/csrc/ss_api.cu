@@ -401,6 +401,86 @@ inline int64_t parts_of(const ss_tensor_io& t, int gmode) {
 }
 inline int64_t psegs_of(int64_t parts) { return (parts + ss::kSegTasks - 1) / ss::kSegTasks; }
 
+// ---- small single tensors ------------------------------------------------------
+// Up to SS_SMALL_MAX_BLOCKS (env; default kSmallMaxBlocks) NVFP4 blocks in one
+// tensor go to quant_small_kernel: one thread per block over every resident
+// thread, no candidate table.
+constexpr int64_t kSmallMaxBlocks = 1 << 19;  // 8.4 M elements (C1 = 2^20 blocks: the persistent kernel wins at r = 8)
+int64_t small_max_blocks() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SS_SMALL_MAX_BLOCKS");
+    v = e ? std::max<int64_t>(0, std::atoll(e)) : kSmallMaxBlocks;
+  }
+  return v;
+}
+
+typedef void (*SmallKernel)(ss::SmallParams);
+SmallKernel pick_small(int fmin, int fmax) {
+  if (fmin == -8 && fmax == 8) return ss::quant_small_kernel<8, 8>;
+  if (fmin == -2 && fmax == 6) return ss::quant_small_kernel<2, 6>;
+  if (fmin == -1 && fmax == 1) return ss::quant_small_kernel<1, 1>;
+  if (fmin == 0 && fmax == 0) return ss::quant_small_kernel<0, 0>;
+  return ss::quant_small_kernel<-1, -1>;
+}
+
+ss_status small_launch(const ss_tensor_io& t, int fmin, int fmax, int gmode, const uint32_t* amax, float numer,
+                       Workspace* ws, cudaStream_t cs, int sms) {
+  const int64_t nb = t.rows * t.cols / 16;
+  const int64_t chunks = (nb + 255) / 256;
+  SmallKernel k = pick_small(fmin, fmax);
+  static std::mutex mu;
+  static std::map<SmallKernel, int> occ_cache;
+  int occ;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ_cache.find(k);
+    if (it == occ_cache.end()) {
+      int o = 1;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 256, 0) != cudaSuccess) {
+        cudaGetLastError();
+        o = 1;
+      }
+      it = occ_cache.emplace(k, std::max(o, 1)).first;
+    }
+    occ = it->second;
+  }
+  ss::SmallParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.in = reinterpret_cast<const uint4*>(t.in_bf16);
+  p.nb = nb;
+  p.fmin = fmin;
+  p.fmax = fmax;
+  p.gmode = gmode;
+  p.amax = amax;
+  p.g_numer = numer;
+  p.codes = reinterpret_cast<uint2*>(t.out_codes);
+  p.scales = t.out_scales;
+  p.err = reinterpret_cast<float2*>(t.out_err);
+  p.offsets = t.out_offset;
+  p.g_out = t.d_global_scale;
+  p.part1 = t.d_err_sums ? ws->part1 : nullptr;
+  p.flags = ws->flags;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)sms * occ));
+  if (ss_status s = launch_pdl(k, grid, 256, cs, p)) return s;
+  if (t.d_err_sums) {  // reduce the per-chunk partials (fixed order) into the tensor's sums
+    QuantBatch b;
+    std::memset(&b, 0, sizeof(b));
+    b.n = 1;
+    b.part1 = ws->part1;
+    b.part2 = ws->part2;
+    b.tick = ws->tick;
+    b.t[0].sums = t.d_err_sums;
+    b.t[0].part0 = 0;
+    b.t[0].npart = (int32_t)chunks;
+    b.t[0].seg0 = 0;
+    b.nsegs = (chunks + ss::kSegTasks - 1) / ss::kSegTasks;
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(b.nsegs, sums_grid(sms)));
+    if (ss_status s = launch_pdl(ss::sums_kernel, g2, ss::kThreads, cs, b)) return s;
+  }
+  return SS_OK;
+}
+
 // The one quantization path behind every entry point.
 ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
                         void* stream, int format = SS_FMT_NVFP4) {
@@ -502,6 +582,24 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         cudaMemsetAsync(t.out_scales, 0, (size_t)scale_bytes(t.rows, t.cols, t.scale_layout, fi.bs), cs) !=
             cudaSuccess)
       return SS_ERR_CUDA;
+  }
+
+  // one small NVFP4 tensor: one thread per block (quant_small_kernel)
+  {
+    int live = -1, nlive = 0;
+    for (int i = 0; i < count; i++)
+      if (io[i].rows * io[i].cols > 0) {
+        live = i;
+        nlive++;
+      }
+    if (nlive == 1 && format == SS_FMT_NVFP4 && ri == 0 && !af &&
+        io[live].rows * io[live].cols / 16 <= small_max_blocks()) {
+      for (int i = 0; i < count; i++)
+        if (i != live && io[i].d_err_sums && cudaMemsetAsync(io[i].d_err_sums, 0, 16, cs) != cudaSuccess)
+          return SS_ERR_CUDA;
+      return small_launch(io[live], fmin, fmax, gmode == SS_GLOBAL_NONE ? 0 : 1, amax[live], numer, ws, cs,
+                          info.sms);
+    }
   }
 
   QuantKernel k = pick_kernel(fmin, fmax, ri, format, af);

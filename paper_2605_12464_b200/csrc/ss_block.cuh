@@ -145,4 +145,74 @@ __global__ void __launch_bounds__(256) quant_f32_kernel(const __grid_constant__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small-tensor bf16 kernel (quantize_core picks it for one NVFP4 tensor of at
+// most kSmallMaxBlocks blocks, linear scales, G per tensor or 1): one thread
+// per block through the same routine, so a small tensor spreads over every
+// resident thread (48 registers) instead of 2 blocks per lane of the
+// persistent grid, and no candidate table is built.  Outputs equal
+// quant_kernel's bit for bit; the FP64 error sums are reduced per 256-block
+// chunk (fixed tree) and then by sums_kernel.
+// ---------------------------------------------------------------------------
+struct SmallParams {
+  const uint4* in;        // [nb][2] uint4 (16 bf16)
+  int64_t nb;
+  int fmin, fmax;
+  int gmode;              // 0: G = 1; 1: G from *amax
+  const uint32_t* amax;
+  float g_numer;
+  uint2* codes;
+  uint8_t* scales;
+  float2* err;            // nullable
+  int8_t* offsets;        // nullable
+  float* g_out;           // nullable
+  double2* part1;         // nullable: per 256-block chunk {sum best, sum base}
+  uint32_t* flags;
+};
+
+template <int NEG, int POS>
+__global__ void __launch_bounds__(256) quant_small_kernel(const __grid_constant__ SmallParams p) {
+  __shared__ double2 red[8];
+  pdl_wait();  // the amax grid (PDL predecessor) has completed
+  pdl_launch_dependents();
+  const float G = p.gmode == 1 ? global_scale(*p.amax, p.flags, blockIdx.x == 0 && threadIdx.x == 0, p.g_numer)
+                               : 1.0f;
+  if (p.g_out && blockIdx.x == 0 && threadIdx.x == 0) *p.g_out = G;
+  const uint64_t GG = pack2(G, G);
+  for (int64_t c = blockIdx.x; c * 256 < p.nb; c += gridDim.x) {  // CTA-uniform chunks of 256 blocks
+    const int64_t b = c * 256 + threadIdx.x;
+    double sb = 0.0, sc = 0.0;
+    if (b < p.nb) {
+      const uint4 v0 = __ldcs(p.in + 2 * b), v1 = __ldcs(p.in + 2 * b + 1);
+      const uint32_t wd[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      float y[16];
+#pragma unroll
+      for (int k = 0; k < 8; k++)  // a1 + a3: exact bf16 -> f32, y = RN(x * G)
+        unpack2(fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), GG), y[2 * k], y[2 * k + 1]);
+      const Nvfp4Block r = search_nvfp4_block<NEG, POS>(y, p.fmin, p.fmax);
+      __stcs(p.codes + b, r.codes);
+      p.scales[b] = (uint8_t)r.scale;
+      if (p.err) __stcs(p.err + b, make_float2(r.err_best, r.err_base));
+      if (p.offsets) p.offsets[b] = (int8_t)r.offset;
+      sb = r.err_best;
+      sc = r.err_base;
+    }
+    if (p.part1) {  // fixed-order CTA tree: lanes, then warps 0..7
+      sb = warp_sum(sb);
+      sc = warp_sum(sc);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(sb, sc);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double2 t = red[0];
+        for (int w = 1; w < 8; w++) {
+          t.x += red[w].x;
+          t.y += red[w].y;
+        }
+        p.part1[c] = t;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 }  // namespace ss
