@@ -22,7 +22,10 @@ constexpr int kTaskBytes = kTaskBlocks * 32;  // bf16 input bytes per task
 constexpr int kStages = kBPL >= 4 ? 2 : 4 / kBPL;  // per-warp smem buffers (tasks in flight)
 constexpr int kSegTasks = 4096;               // tasks per CTA of the error-sum kernel
 constexpr int kCounters = 256;                // task counters of the dynamic scheduler
-constexpr int kPruneFrom = 3;                 // exact pruning for offsets f <= -kPruneFrom
+#ifndef SS_PRUNE_FROM
+#define SS_PRUNE_FROM 3
+#endif
+constexpr int kPruneFrom = SS_PRUNE_FROM;     // exact pruning for offsets f <= -kPruneFrom
 constexpr int kMaxTensors = 128;              // tensors per launch (kernel-parameter space)
 constexpr int kAmaxVecs = 8;                  // 16-B vectors per thread per amax chunk
 constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk (32 KiB)

@@ -25,6 +25,12 @@ VARIANTS = {
     "base": [],
     "noprune": ["SS_NO_PRUNE=1"],
     "count": ["SS_COUNT_EVALS=1"],
+    "cilp1": ["SS_CILP=1"],
+    "cilp3": ["SS_CILP=3"],
+    "cilp4": ["SS_CILP=4"],
+    "mb3": ["SS_MIN_BLOCKS=3"],
+    "prune2": ["SS_PRUNE_FROM=2"],
+    "prune4": ["SS_PRUNE_FROM=4"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
 
