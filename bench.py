@@ -330,7 +330,9 @@ def run_ours(a, rank, world, local_rank):
     start.record()
     launches = 0
     for i in range(a.steps):
+        torch.cuda.nvtx.range_push("ss_step_%d" % i)       # NVTX ranges for nsys / ncu --nvtx
         launches += q.step(shard_sets[i % copies], outs, hooks)
+        torch.cuda.nvtx.range_pop()
     stop.record()
     torch.cuda.synchronize()
     if dist_on:
