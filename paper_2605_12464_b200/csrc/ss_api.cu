@@ -368,24 +368,20 @@ ss_status rowscale_launch(const ss_tensor_io* io, int count, const std::vector<c
 // so the quantize reads after the warp's own amax pass hit L2.  Shorter rows
 // would leave lanes idle, longer ones would re-read HBM: those use the
 // separate rowscale pass.  SS_ROW_FUSION=0 disables it (A/B measurement).
+bool env_off(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] == '0';
+}
 bool row_fusion_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("SS_ROW_FUSION");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
+  static const bool on = !env_off("SS_ROW_FUSION");  // thread-safe one-time init
+  return on;
 }
 // SS_GLOBAL_TENSOR, NVFP4, plain layout: the amax pass runs inside the quantize
 // launch (quant_kernel<..., AF>).  SS_AMAX_FUSION=0 restores the separate
 // amax launch (A/B measurement).
 bool amax_fusion_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("SS_AMAX_FUSION");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
+  static const bool on = !env_off("SS_AMAX_FUSION");
+  return on;
 }
 inline int64_t amax_units(int64_t nb) { return (2 * nb + ss::kAmaxUnitVecs - 1) / ss::kAmaxUnitVecs; }
 
@@ -407,11 +403,10 @@ inline int64_t psegs_of(int64_t parts) { return (parts + ss::kSegTasks - 1) / ss
 // thread, no candidate table.
 constexpr int64_t kSmallMaxBlocks = 1 << 19;  // 8.4 M elements (C1 = 2^20 blocks: the persistent kernel wins at r = 8)
 int64_t small_max_blocks() {
-  static int64_t v = -1;
-  if (v < 0) {
+  static const int64_t v = [] {
     const char* e = std::getenv("SS_SMALL_MAX_BLOCKS");
-    v = e ? std::max<int64_t>(0, std::atoll(e)) : kSmallMaxBlocks;
-  }
+    return e ? std::max<int64_t>(0, std::atoll(e)) : kSmallMaxBlocks;
+  }();
   return v;
 }
 
