@@ -158,7 +158,7 @@ def main():
     import ssgen
     import paper_2605_12464_b200 as ss
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,c2,c3,c4,f32,paper_tab,c5,formats")
+    ap.add_argument("--configs", default="c1,oracle,c2,c3,c4,f32,paper_tab,c5,formats")
     ap.add_argument("--c5-gib", default="1,8")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -178,6 +178,29 @@ def main():
         for w in [(-8, 8), (0, 0), (-1, 1), (-2, 6), (-126, 126)]:
             lines.append(report("c1_gauss4096", *w, *measure(torch, ss, groups, *w, reps=80), hbm, mhz))
         del groups
+        torch.cuda.empty_cache()
+    if "oracle" in cfgs:   # the oracle on the full C1 tensor, 1 thread and all cores,
+        import time       # plus a full-tensor bit-exact check of the GPU output against it
+        import numpy as np
+        import oracle
+        oracle.build()
+        x = gen(ssgen.workload("c1_gauss4096"))[0]
+        xc = x.cpu()
+        o = ss.quantize(x, radius=8, gmode="tensor")
+        torch.cuda.synchronize()
+        for th in (1, os.cpu_count()):
+            t0 = time.perf_counter()
+            r = oracle.quantize(xc, 4096, 4096, -8, 8, "tensor", threads=th)
+            dt = time.perf_counter() - t0
+            same = (np.array_equal(o.codes.cpu().numpy(), r.codes) and
+                    np.array_equal(o.scales.cpu().numpy(), r.scales) and
+                    np.array_equal(o.err.cpu().numpy().view(np.uint32), r.err.view(np.uint32)))
+            line = {"config": "oracle_c1_gauss4096", "window": [-8, 8], "threads": th,
+                    "cpu": os.cpu_count(), "oracle_s": dt, "oracle_gbs_bf16": 2 * x.numel() / dt / 1e9,
+                    "gpu_equals_oracle_full_tensor": bool(same)}
+            print(json.dumps(line), flush=True)
+            lines.append(line)
+        del x, xc, o
         torch.cuda.empty_cache()
     if "c2" in cfgs:
         xs = gen(ssgen.workload("c2_qwen3_8b_weights"))
