@@ -378,3 +378,37 @@ def test_bench_launch_configuration_c2_sampled(ss, oracle_lib):
         assert np.array_equal(o.scales[r_t].cpu().numpy(), ref.scales)
         assert o.G.item() == np.float32(ref.G)
     del xs, outs
+
+
+@pytest.mark.parametrize("shapes", [[(16, 64), (64, 256), (33, 4096), (1, 16)],   # fused amax (AF)
+                                    [(512, 1024)]])                              # small-tensor path
+def test_cuda_graph_tensor_mode_replays_fresh_inputs(ss, oracle_lib, shapes):
+    # The per-tensor-G call (fused amax with in-kernel counters, or the
+    # one-thread small path with PDL launches) captured once and replayed on
+    # new input contents: the counters re-arm inside the graph and every
+    # replay matches the oracle on the inputs it saw.
+    xd = [torch.empty(r, c, dtype=torch.bfloat16, device="cuda") for r, c in shapes]
+    outs = [ss.alloc_out(x) for x in xd]
+    s = torch.cuda.Stream()
+
+    def fill(seed):
+        xs = [ssgen.generate("weight_outlier", r, c, seed=seed, tid=970 + k) for k, (r, c) in enumerate(shapes)]
+        for d, x in zip(xd, xs):
+            d.copy_(x)
+        return xs
+
+    fill(1)
+    with torch.cuda.stream(s):
+        ss.quantize_batched(xd, outs, fmin=-2, fmax=6, gmode="tensor")     # warm-up: workspace allocated
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ss.quantize_batched(xd, outs, fmin=-2, fmax=6, gmode="tensor")
+    for seed in (2, 3):
+        xs = fill(seed)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        for x, o in zip(xs, outs):
+            ref = oracle_lib.quantize(x, *x.shape, -2, 6, "tensor")
+            _cmp(o, ref, *x.shape)
