@@ -43,7 +43,14 @@ constexpr int kAmaxChunk = kThreads * kAmaxVecs;  // 16-B vectors per amax chunk
 // fused amax (quant_kernel<..., AF>): warps per CTA that start as amax warps,
 // and the 16-B vectors of one amax unit (32 KiB)
 constexpr int kAmaxWarps = SS_AMAX_WARPS;
-constexpr int kAmaxUnitVecs = 2048;
+#ifndef SS_AMAX_UNIT
+#define SS_AMAX_UNIT 2048
+#endif
+#ifndef SS_AMAXW_VECS
+#define SS_AMAXW_VECS 8
+#endif
+constexpr int kAmaxUnitVecs = SS_AMAX_UNIT;    // 16-B vectors per amax unit (32 KiB)
+constexpr int kAmaxWarpVecs = SS_AMAXW_VECS;  // 16-B loads in flight per lane of an amax warp
 
 constexpr uint32_t kOneSixthBits = 0x3E2AAAABu;  // RN(1/6) (Alg. 1 line 2; R8)
 constexpr float kGlobalNumer = 2688.0f;          // 6 * 448: largest NVFP4 magnitude (R9)

@@ -50,7 +50,7 @@ __device__ __forceinline__ void amax_unit(const QuantBatch& p, uint32_t u, int& 
   v1 = min(2 * A.nb, v0 + kAmaxUnitVecs);
 }
 
-// One amax warp: 8 coalesced 16-B loads in flight per lane; the next unit is
+// One amax warp: kAmaxWarpVecs coalesced 16-B loads in flight per lane; the next unit is
 // drawn one ahead and bulk-prefetched into L2 (TMA, no registers or shared
 // memory), so these loads mostly hit L2.  (Staging the units through
 // shared memory with TMA bulk copies instead was measured slower: 2.4 vs
@@ -72,13 +72,13 @@ __device__ __forceinline__ void amax_warp(const QuantBatch& p, int lane) {
     amax_unit(p, idx, ta, v0, v1);
     const uint4* src = reinterpret_cast<const uint4*>(p.t[ta].in);
     uint32_t m = 0;
-    for (int64_t v = v0 + lane; v < v1; v += 32 * kAmaxVecs) {
-      uint4 a[kAmaxVecs];
+    for (int64_t v = v0 + lane; v < v1; v += 32 * kAmaxWarpVecs) {
+      uint4 a[kAmaxWarpVecs];
 #pragma unroll
-      for (int k = 0; k < kAmaxVecs; k++)
+      for (int k = 0; k < kAmaxWarpVecs; k++)
         a[k] = v + 32 * k < v1 ? __ldcs(src + v + 32 * k) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-      for (int k = 0; k < kAmaxVecs; k++) m = hmax_abs_vec(m, a[k]);
+      for (int k = 0; k < kAmaxWarpVecs; k++) m = hmax_abs_vec(m, a[k]);
     }
     amax_publish(p, ta, m, lane);
   }
