@@ -77,6 +77,13 @@ def test_argument_errors_are_synchronous(L):
     ns[1] = -1
     ptrs[1] = base
     assert L.ss_tensor_amax_batched(ptrs, ns, 2, P(base), 0, None) == B.SS_ERR_INVALID_ARG
+    # FP32 block-routine entry point (ss_quantize_nvfp4_f32)
+    F = L.ss_quantize_nvfp4_f32
+    assert F(P(base), 4, 24, -8, 8, None, P(base), P(base), None, None, None) == B.SS_ERR_INVALID_ARG
+    assert F(P(base), 4, 32, 1, 8, None, P(base), P(base), None, None, None) == B.SS_ERR_INVALID_ARG
+    assert F(P(base), 4, 32, -8, 8, None, None, P(base), None, None, None) == B.SS_ERR_INVALID_ARG
+    assert F(P(base + 4), 4, 32, -8, 8, None, P(base), P(base), None, None, None) == B.SS_ERR_ALIGNMENT
+    assert F(P(base), 4, 32, -8, 8, P(base + 2), P(base), P(base), None, None, None) == B.SS_ERR_ALIGNMENT
 
 
 @pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) is None and
@@ -93,6 +100,8 @@ def test_no_fallback_without_device(L):
     io = (B.TensorIO * 1)(B.TensorIO(base, 2, 32, None, base + 1024, base + 2048, None, None, None,
                                      None))
     assert L.ss_quantize_nvfp4_batched(io, 1, -8, 8, 1, None) == B.SS_ERR_UNSUPPORTED_DEVICE
+    assert L.ss_quantize_nvfp4_f32(P(base), 2, 32, -8, 8, None, P(base + 1024), P(base + 2048), None, None,
+                                   None) == B.SS_ERR_UNSUPPORTED_DEVICE
 
 
 def test_binding_raises_not_falls_back():
@@ -124,3 +133,16 @@ def test_device_header_compiles_standalone(tmp_path):
                           "-I", os.path.join(ROOT, "include"), "-o", str(tmp_path / "user.o"), str(src)],
                          capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
+
+
+def test_amax_fusion_rule():
+    """The Python mirror of ss_api.cu's fusion rule (bench.py's roofline bytes
+    and launch counts depend on it): >= 4 offsets and a first tensor holding
+    at most half of the batch."""
+    from paper_2605_12464_b200.dist import amax_fused
+    assert amax_fused([100, 100], -8, 8)
+    assert amax_fused([0, 100, 100], -2, 1)          # empty tensors are skipped
+    assert not amax_fused([101, 100], -8, 8)         # first tensor dominates
+    assert not amax_fused([100], -8, 8)              # a single tensor: separate amax kernel
+    assert not amax_fused([100, 100], -1, 1)         # HBM-bound window
+    assert not amax_fused([], -8, 8)
