@@ -315,7 +315,9 @@ SS_API ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* args);
 
 /* Synchronizes `stream`, returns and clears the sticky device flags of this
  * (device, stream) workspace: bit 0 = non-finite input seen (SS_ERR_NONFINITE),
- * bit 1 = global scale out of range (SS_ERR_RANGE). */
+ * bit 1 = global scale out of range (SS_ERR_RANGE), bit 2 = a fused-amax
+ * search warp gave up waiting for its tensor's amax after ~10 s (a
+ * watchdog against a stalled GPU; that tensor's outputs are meaningless). */
 SS_API ss_status ss_get_device_status(int* flags, void* stream);
 
 #ifdef __cplusplus

@@ -73,6 +73,6 @@ struct Fmt {
 };
 __host__ __device__ constexpr float global_numer(int vf) { return vf ? 3360.0f : kGlobalNumer; }
 
-enum : uint32_t { kFlagNonFinite = 1u, kFlagRange = 2u };
+enum : uint32_t { kFlagNonFinite = 1u, kFlagRange = 2u, kFlagAmaxTimeout = 4u };
 
 }  // namespace ss

@@ -219,7 +219,14 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 #ifdef SS_AF_TRACE
         const unsigned long long t0 = gtime();
 #endif
-        while (ld_acquire_gpu(p.done + ti) < (uint32_t)T.na) __nanosleep(256);
+        // watchdog: the amax warps never wait, so this only trips on a stalled GPU
+        for (uint32_t spins = 0; ld_acquire_gpu(p.done + ti) < (uint32_t)T.na; spins++) {
+          if (spins == (1u << 25)) {  // ~10 s of 256-ns sleeps
+            if (lane == 0) atomicOr(p.flags, kFlagAmaxTimeout);
+            break;
+          }
+          __nanosleep(256);
+        }
 #ifdef SS_AF_TRACE
         if (lane == 0) atomicAdd(p.evals + 2, gtime() - t0);
 #endif
