@@ -227,6 +227,25 @@ typedef struct {
 SS_API ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min,
                                     int f_max, int global_scale_mode, void* stream);
 
+/*
+ * One group of a sharded step: quantize `tensors` with
+ * SS_GLOBAL_DEVICE_AMAX (each d_amax_bits already all-reduced) and, inside
+ * the same launch, compute the LOCAL amax (FP32 bits of max|x|) of the
+ * next group's shards into next_amax_bits[0..next_count) — overwritten —
+ * ready for that group's all-reduce.  The amax pass of the next group thus
+ * runs under this group's search (the amax warps of §4.2a), so a pipelined
+ * step exposes only the first group's amax.
+ *   next_in[j]   DEVICE bf16, 16-B aligned, next_n[j] elements (multiple of 16)
+ *   next_count   <= 128
+ * NVFP4, linear scales; any other case (or SS_AMAX_FUSION=0) computes the
+ * next amaxes with a separate launch first.  Results are bit-identical to
+ * ss_tensor_amax_batched + ss_quantize_nvfp4_batched.
+ */
+SS_API ss_status ss_quantize_nvfp4_batched_next_amax(const ss_tensor_io* tensors, int count, int f_min,
+                                                     int f_max, const void* const* next_in,
+                                                     const int64_t* next_n, int next_count,
+                                                     uint32_t* next_amax_bits, void* stream);
+
 /* The same for any block format (SS_FMT_*); windows are clamped to +-126
  * (UE4M3) or +-254 (UE8M0) code steps. */
 SS_API ss_status ss_quantize_batched_fmt(const ss_tensor_io* tensors, int count, int f_min,

@@ -20,6 +20,7 @@ from ._binding import (  # noqa: F401
     lib,
     quantize,
     quantize_batched,
+    quantize_batched_next_amax,
     quantize_f32,
     quantize_host,
     quantize_host_batched,
@@ -31,6 +32,7 @@ from ._binding import (  # noqa: F401
 )
 
 __all__ = [
-    "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host", "quantize_host_batched",
+    "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "quantize_batched_next_amax", "quantize_f32",
+    "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host", "quantize_host_batched",
     "device_status", "scale_bytes", "SCALE_LAYOUTS", "FORMATS", "status_string", "SSError", "QuantOut", "GMODES",
 ]

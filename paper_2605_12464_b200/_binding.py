@@ -135,6 +135,8 @@ def lib():
             L.ss_code_bytes.argtypes = [i64, i64, I]
             L.ss_quantize_batched_fmt.restype = I
             L.ss_quantize_batched_fmt.argtypes = [ctypes.POINTER(TensorIO), I, I, I, I, I, P]
+            L.ss_quantize_nvfp4_batched_next_amax.restype = I
+            L.ss_quantize_nvfp4_batched_next_amax.argtypes = [ctypes.POINTER(TensorIO), I, I, I, P, P, I, P, P]
             L.ss_quantize_nvfp4_f32.restype = I
             L.ss_quantize_nvfp4_f32.argtypes = [P, i64, i64, I, I, P, P, P, P, P, P]
             L.ss_dequantize_nvfp4.restype = I
@@ -311,6 +313,30 @@ def quantize_f32(x, radius=None, fmin=None, fmax=None, G=None, want_err: bool = 
                                        _ptr(out.scales), _ptr(out.err), _ptr(out.offsets),
                                        _stream_ptr(stream)), "ss_quantize_nvfp4_f32")
     return out
+
+
+def quantize_batched_next_amax(xs, outs, amax, next_xs, next_amax, radius=None, fmin=None, fmax=None,
+                               stream=None):
+    """Quantize ``xs`` with their (all-reduced) ``amax`` and compute, in the same
+    launch, the local amax of ``next_xs`` into ``next_amax`` (device int32
+    [len(next_xs)], overwritten) -- ss_quantize_nvfp4_batched_next_amax."""
+    import torch
+    lo, hi = _window(radius, fmin, fmax)
+    n, m = len(xs), len(next_xs)
+    arr = (TensorIO * max(n, 1))()
+    for i, (x, o) in enumerate(zip(xs, outs)):
+        assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+        rows, cols = x.shape
+        arr[i] = TensorIO(_ptr(x), rows, cols, amax.data_ptr() + 4 * i, _ptr(o.codes), _ptr(o.scales),
+                          _ptr(o.err), _ptr(o.offsets), _ptr(o.sums), _ptr(o.G), SCALE_LAYOUTS["linear"])
+    for x in next_xs:
+        assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous()
+    ptrs = (ctypes.c_void_p * max(m, 1))(*[x.data_ptr() for x in next_xs])
+    ns = (ctypes.c_int64 * max(m, 1))(*[x.numel() for x in next_xs])
+    _check(lib().ss_quantize_nvfp4_batched_next_amax(arr, n, lo, hi, ptrs, ns, m, _ptr(next_amax),
+                                                      _stream_ptr(stream)),
+           "ss_quantize_nvfp4_batched_next_amax")
+    return outs
 
 
 def quantize_simple(x, radius: int, gmode: str, codes, scales, err=None, stream=None):

@@ -477,8 +477,17 @@ ss_status small_launch(const ss_tensor_io& t, int fmin, int fmax, int gmode, con
 }
 
 // The one quantization path behind every entry point.
+// The next group's tensors whose local amaxes a sharded step wants while this
+// call searches (ss_quantize_nvfp4_batched_next_amax).
+struct NextAmax {
+  const void* const* in;
+  const int64_t* n;
+  int count;
+  uint32_t* out;
+};
+
 ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
-                        void* stream, int format = SS_FMT_NVFP4) {
+                        void* stream, int format = SS_FMT_NVFP4, const NextAmax* next = nullptr) {
   FmtInfo fi;
   if (!fmt_info(format, &fi)) return SS_ERR_INVALID_ARG;
   if (count < 0 || (count > 0 && !io)) return SS_ERR_INVALID_ARG;
@@ -490,7 +499,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   int dev;
   DeviceInfo info;
   if (ss_status s = device_check(&dev, &info)) return s;
-  if (count == 0) return SS_OK;
+  if (count == 0 && !(next && next->count > 0)) return SS_OK;
   const int lim = fi.sf ? 254 : 126;
   const int fmin = std::max(f_min, -lim), fmax = std::min(f_max, lim);
   const float numer = ss::global_numer(fi.vf);
@@ -515,8 +524,22 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     if (n > 0 && n_first < 0) n_first = n;
     n_all += n;
   }
-  const bool af = gmode == SS_GLOBAL_TENSOR && ri == 0 && format == SS_FMT_NVFP4 && fmax - fmin >= 3 &&
-                  2 * n_first <= n_all && amax_fusion_enabled();
+  const bool af_self = gmode == SS_GLOBAL_TENSOR && ri == 0 && format == SS_FMT_NVFP4 && fmax - fmin >= 3 &&
+                       2 * n_first <= n_all && amax_fusion_enabled();
+  // next-group amaxes ride in the first launch of this call (AF kernel, no waits)
+  const bool af_next = next && next->count > 0 && n_all > 0 && gmode == SS_GLOBAL_DEVICE_AMAX && ri == 0 &&
+                       format == SS_FMT_NVFP4 && amax_fusion_enabled();
+  if (next && next->count > 0) {
+    if (af_next) {
+      if (cudaMemsetAsync(next->out, 0, 4 * (size_t)next->count, reinterpret_cast<cudaStream_t>(stream)) !=
+          cudaSuccess)
+        return SS_ERR_CUDA;
+    } else if (ss_status s = amax_launch(next->in, next->n, next->out, next->count, false,
+                                         reinterpret_cast<cudaStream_t>(stream), info.sms)) {
+      return s;  // not fusable here: a plain amax launch first
+    }
+  }
+  const bool af = af_self || af_next;
 
   // sizes of the largest launch (workspace grown once, before any launch)
   int64_t max_tasks = 0, max_segs = 0;
@@ -580,7 +603,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   }
 
   // one small NVFP4 tensor: one thread per block (quant_small_kernel)
-  {
+  if (!af_next) {
     int live = -1, nlive = 0;
     for (int i = 0; i < count; i++)
       if (io[i].rows * io[i].cols > 0) {
@@ -599,6 +622,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
 
   QuantKernel k = pick_kernel(fmin, fmax, ri, format, af);
   const int64_t slots = (int64_t)info.sms * occupancy(k);
+  const QuantKernel k_plain = af_next ? pick_kernel(fmin, fmax, ri, format, false) : k;
+  bool next_done = false;
   int i = 0;
   while (i < count) {
     QuantBatch b;
@@ -644,7 +669,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       }
       const int64_t parts = parts_of(t, gmode);
       // the kernel indexes units, partials and amax units with 32 bits: close the batch before overflow
-      const int64_t au = af ? amax_units(nb) : 0;
+      const int64_t au = af_self ? amax_units(nb) : 0;
       if (b.n > 0 && (tk + units > (int64_t)INT32_MAX - ss::kCounters || pk + parts > (int64_t)INT32_MAX ||
                       b.namax + au > (int64_t)INT32_MAX - ss::kWarps * 65536))
         break;
@@ -670,7 +695,14 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       q.part0 = (int32_t)pk;
       q.npart = (int32_t)parts;
       q.seg0 = gr;
-      q.a0 = b.namax;
+      if (af_self) {  // this tensor's own amax, counted into done[b.n - 1]
+        ss::AmaxTask& a = b.am[b.nam++];
+        a.in = reinterpret_cast<const uint4*>(t.in_bf16);
+        a.nvec = 2 * nb;
+        a.slot = const_cast<uint32_t*>(amax[i]);
+        a.a0 = b.namax;
+        a.done = b.n - 1;
+      }
       q.na = (int32_t)au;
       b.namax += (int32_t)au;
       tk += units;
@@ -679,11 +711,26 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       sums |= t.d_err_sums != nullptr;
     }
     if (b.n == 0) break;
+    if (af_next && !next_done) {  // the next group's shards: local amaxes, nobody waits
+      for (int j = 0; j < next->count; j++) {
+        const int64_t nv = next->n[j] / 8;
+        if (nv == 0) continue;
+        ss::AmaxTask& a = b.am[b.nam++];
+        a.in = reinterpret_cast<const uint4*>(next->in[j]);
+        a.nvec = nv;
+        a.slot = next->out + j;
+        a.a0 = b.namax;
+        a.done = -1;
+        b.namax += (int32_t)((nv + ss::kAmaxUnitVecs - 1) / ss::kAmaxUnitVecs);
+      }
+      next_done = true;
+    }
     b.ntasks = tk;
     b.nsegs = gr;
     const int64_t want = (tk + ss::kWarps - 1) / ss::kWarps;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, slots));
-    if (ss_status s = launch_pdl(k, grid, ss::kThreads, cs, b)) return s;
+    // later launches of a next-amax call carry no amax tasks: the plain kernel
+    if (ss_status s = launch_pdl(b.nam ? k : (af_self ? k : k_plain), grid, ss::kThreads, cs, b)) return s;
     if (sums) {
       const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(gr, sums_grid(info.sms)));
       if (ss_status s = launch_pdl(ss::sums_kernel, g2, ss::kThreads, cs, b)) return s;
@@ -834,6 +881,21 @@ int64_t ss_code_bytes(int64_t rows, int64_t cols, int format) {
 ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min, int f_max,
                                     int global_scale_mode, void* stream) {
   return quantize_core(tensors, count, f_min, f_max, global_scale_mode, stream);
+}
+
+ss_status ss_quantize_nvfp4_batched_next_amax(const ss_tensor_io* tensors, int count, int f_min, int f_max,
+                                              const void* const* next_in, const int64_t* next_n,
+                                              int next_count, uint32_t* next_amax_bits, void* stream) {
+  if (next_count < 0 || next_count > ss::kMaxTensors ||
+      (next_count > 0 && (!next_in || !next_n || !next_amax_bits)))
+    return SS_ERR_INVALID_ARG;
+  for (int j = 0; j < next_count; j++) {
+    if (next_n[j] < 0 || next_n[j] % 16 != 0 || (next_n[j] > 0 && !next_in[j])) return SS_ERR_INVALID_ARG;
+    if (!aligned(next_in[j], 16)) return SS_ERR_ALIGNMENT;
+  }
+  if (!aligned(next_amax_bits, 4)) return SS_ERR_ALIGNMENT;
+  NextAmax nx{next_in, next_n, next_count, next_amax_bits};
+  return quantize_core(tensors, count, f_min, f_max, SS_GLOBAL_DEVICE_AMAX, stream, SS_FMT_NVFP4, &nx);
 }
 
 ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {

@@ -2,11 +2,15 @@
 // (quant_kernel<..., AF>): step a2 (tensor amax) for a batch, run by
 // kAmaxWarps warps per CTA ahead of the search.
 //
-// Units of kAmaxUnitVecs 16-B vectors are drawn in tensor order from one
-// counter (QuantBatch::done[kMaxTensors]).  Each unit's max of |x| is folded
-// into its tensor's amax slot (atomicMax of the FP32 bit pattern; exact, and
-// non-finite inputs sort above every finite value, R14), then done[i] is
-// release-incremented; search warps acquire done[i] == na before using G.
+// Units of kAmaxUnitVecs 16-B vectors of the amax tasks (QuantBatch::am) are
+// drawn in order from one counter (QuantBatch::done[kMaxTensors]).  Each
+// unit's max of |x| is folded into its task's slot (atomicMax of the FP32 bit
+// pattern; exact, and non-finite inputs sort above every finite value, R14),
+// then done[i] is release-incremented; search warps acquire done[i] == na
+// before using G.  The tasks are the launch's own tensors (per-tensor G on
+// one GPU), or the NEXT group's shards of a sharded step, whose local amaxes
+// then go to the all-reduce while this launch searches
+// (ss_quantize_nvfp4_batched_next_amax).
 // Reductions use HMNMX2 (max.NaN.xorsign.abs.bf16x2): the magnitude max of
 // bf16 pairs with NaN propagation in one instruction; the sign bits it leaves
 // are masked off once per unit.
@@ -25,14 +29,14 @@ __device__ __forceinline__ uint32_t hmax_abs_vec(uint32_t m, const uint4& a) {
   return hmax_abs2(m, hmax_abs2(hmax_abs2(a.x, a.y), hmax_abs2(a.z, a.w)));
 }
 
-// Fold a unit's per-lane magnitude maxima into tensor ta's amax, then count the unit.
+// Fold a unit's per-lane magnitude maxima into task ta's amax, then count the unit.
 __device__ __forceinline__ void amax_publish(const QuantBatch& p, int ta, uint32_t m, int lane) {
   m &= 0x7FFF7FFFu;
   const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, max(m & 0xFFFFu, m >> 16));
   if (lane == 0) {
-    uint32_t* slot = const_cast<uint32_t*>(p.t[ta].amax);
-    if (r && (r << 16) > ld_relaxed_gpu(slot)) atomicMax(slot, r << 16);
-    red_release_add_gpu(p.done + ta, 1u);
+    const AmaxTask& A = p.am[ta];
+    if (r && (r << 16) > ld_relaxed_gpu(A.slot)) atomicMax(A.slot, r << 16);
+    if (A.done >= 0) red_release_add_gpu(p.done + A.done, 1u);
   }
 }
 
@@ -42,12 +46,12 @@ __device__ __forceinline__ uint32_t amax_draw(const QuantBatch& p, int lane) {
   return __shfl_sync(0xFFFFFFFFu, idx, 0);
 }
 
-// Unit u -> its tensor (forward walk from `t`) and 16-B vector range [v0, v1).
+// Unit u -> its task (forward walk from `t`) and 16-B vector range [v0, v1).
 __device__ __forceinline__ void amax_unit(const QuantBatch& p, uint32_t u, int& t, int64_t& v0, int64_t& v1) {
-  while (t + 1 < p.n && p.t[t + 1].a0 <= (int)u) t++;
-  const QTensor& A = p.t[t];
+  while (t + 1 < p.nam && p.am[t + 1].a0 <= (int)u) t++;
+  const AmaxTask& A = p.am[t];
   v0 = (int64_t)((int)u - A.a0) * kAmaxUnitVecs;
-  v1 = min(2 * A.nb, v0 + kAmaxUnitVecs);
+  v1 = min(A.nvec, v0 + kAmaxUnitVecs);
 }
 
 // One amax warp: kAmaxWarpVecs coalesced 16-B loads in flight per lane; the next unit is
@@ -60,7 +64,7 @@ __device__ __forceinline__ void amax_warp(const QuantBatch& p, int lane) {
   auto prefetch = [&](uint32_t u) {
     int64_t v0, v1;
     amax_unit(p, u, tn, v0, v1);
-    if (lane == 0) prefetch_l2_bulk(reinterpret_cast<const uint4*>(p.t[tn].in) + v0, (uint32_t)(16 * (v1 - v0)));
+    if (lane == 0) prefetch_l2_bulk(p.am[tn].in + v0, (uint32_t)(16 * (v1 - v0)));
   };
   uint32_t nxt = amax_draw(p, lane);
   if (nxt < (uint32_t)p.namax) prefetch(nxt);
@@ -70,7 +74,7 @@ __device__ __forceinline__ void amax_warp(const QuantBatch& p, int lane) {
     if (nxt < (uint32_t)p.namax) prefetch(nxt);
     int64_t v0, v1;
     amax_unit(p, idx, ta, v0, v1);
-    const uint4* src = reinterpret_cast<const uint4*>(p.t[ta].in);
+    const uint4* src = p.am[ta].in;
     uint32_t m = 0;
     for (int64_t v = v0 + lane; v < v1; v += 32 * kAmaxWarpVecs) {
       uint4 a[kAmaxWarpVecs];

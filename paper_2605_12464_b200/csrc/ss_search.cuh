@@ -114,9 +114,20 @@ struct QTensor {
   int16_t hpr, cpr, upr, cpu;
   int32_t part0;            // first error-sum partial (one per work item) of this tensor
   int32_t npart;            // error-sum partials of this tensor
-  // fused amax (AF launches, gmode 1): amax units [a0, a0 + na) of
-  // kAmaxUnitVecs 16-B vectors; their completion count goes to QuantBatch::done[i]
-  int32_t a0, na;
+  // fused amax (AF launches): the search of this tensor waits until
+  // QuantBatch::done[i] == na (0: G needs no in-launch amax)
+  int32_t na;
+};
+
+// A tensor whose amax the AF amax warps compute: units [a0, next a0) of
+// kAmaxUnitVecs 16-B vectors, folded into *slot (atomicMax of FP32 bits) and,
+// when done >= 0, counted into QuantBatch::done[done].
+struct AmaxTask {
+  const uint4* in;
+  int64_t nvec;             // 16-B vectors (2 per 16-element block)
+  uint32_t* slot;
+  int32_t a0;
+  int32_t done;
 };
 
 struct QuantBatch {
@@ -134,6 +145,8 @@ struct QuantBatch {
   uint32_t* done;           // AF launches: [kMaxTensors] finished amax units per tensor, then the
                             // amax unit counter (zero, re-armed)
   int32_t namax;            // AF launches: amax units of the batch
+  int32_t nam;              // AF launches: amax tasks (am[0..nam))
+  AmaxTask am[kMaxTensors];
   unsigned long long* evals;  // SS_COUNT_EVALS builds: block-candidate evaluations executed
   QTensor t[kMaxTensors];
 };

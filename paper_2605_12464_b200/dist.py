@@ -35,6 +35,32 @@ def amax_fused(numels: Sequence[int], fmin: int, fmax: int) -> bool:
     return bool(live) and fmax - fmin >= 3 and 2 * live[0] <= sum(live)
 
 
+def amax_groups(numels: Sequence[int], fractions=(0.04, 0.2), max_group: int = 128) -> List[tuple]:
+    """Contiguous tensor groups for the grouped sharded step: the first holds
+    >= 4 % of the elements (its amax is exposed), the second reaches 20 %
+    (its amax runs under the first group's search), the rest follow in
+    groups of <= 128 tensors (the amax of each under the previous search;
+    the search costs ~4x the amax per element at r = 8)."""
+    total = sum(numels)
+    if total == 0 or len(numels) < 2:
+        return [(0, len(numels))]
+    bounds, lo, acc = [], 0, 0
+    for f in fractions:
+        hi = lo
+        while hi < len(numels) and (acc + numels[hi] < f * total or hi == lo) and hi - lo < max_group:
+            acc += numels[hi]
+            hi += 1
+        if hi >= len(numels):
+            break
+        bounds.append((lo, hi))
+        lo = hi
+    while lo < len(numels):
+        hi = min(len(numels), lo + max_group)
+        bounds.append((lo, hi))
+        lo = hi
+    return bounds
+
+
 class CudaOps:
     """libss.so batched calls on the current CUDA stream.  Sharded (N > 1):
     one amax launch and one quantize launch per 128 tensors of a step, the
@@ -66,6 +92,16 @@ class CudaOps:
         launches = (len(live) + 127) // 128
         fused = amax_fused([xs[k].numel() for k in live], self.fmin, self.fmax)
         return launches * ((2 if self.want_sums else 1) + (0 if fused else 1))
+
+    def quantize_next_amax(self, xs, buf, outs, next_xs, next_buf) -> int:
+        """Quantize ``xs`` (all-reduced amaxes in ``buf``) and, in the same launch,
+        the local amaxes of ``next_xs`` into ``next_buf`` (ss_quantize_nvfp4_batched_next_amax)."""
+        live = [k for k, x in enumerate(xs) if x.shape[0] > 0]
+        self.B.quantize_batched_next_amax([xs[k] for k in live], [outs[k] for k in live],
+                                          buf if len(live) == len(xs) else buf[live].contiguous(),
+                                          next_xs, next_buf, fmin=self.fmin, fmax=self.fmax)
+        launches = (len(live) + 127) // 128
+        return launches * (2 if self.want_sums else 1) + (0 if live else 1)
 
     def quantize_all(self, xs, buf, outs) -> int:
         live = [k for k, x in enumerate(xs) if x.shape[0] > 0]
@@ -101,6 +137,7 @@ class RowShardQuantizer:
         self.amax_buf = ops.new_amax(len(plan.shapes), device)
         self.pipeline_groups = pipeline_groups
         self._side = None
+        self.groups = amax_groups([r * c for r, c in plan.shapes])
 
     def step(self, shards: List[torch.Tensor], outs: List, hooks=None) -> int:
         """One pass over every tensor; returns the number of kernels launched.
@@ -130,6 +167,8 @@ class RowShardQuantizer:
         if not self.collective and self.pipeline_groups > 1 and torch.cuda.is_available() \
                 and len(shards) > 1 and shards[0].is_cuda:
             return self._pipelined(shards, outs, hooks)
+        if self.collective and len(self.groups) > 1 and hasattr(self.ops, "quantize_next_amax"):
+            return self._grouped(shards, outs, hooks)
         n = self.ops.amax_all(shards, self.amax_buf)
         if self.collective:
             dist.all_reduce(self.amax_buf, op=dist.ReduceOp.MAX, group=self.group)
@@ -138,6 +177,30 @@ class RowShardQuantizer:
         n += self.ops.quantize_all(shards, self.amax_buf, outs)
         if hooks is not None:
             hooks.after()
+        return n
+
+    def _grouped(self, shards, outs, hooks) -> int:
+        """Sharded step in groups: amax(g0) -> all-reduce(g0) -> [quantize(g_k) with
+        the local amax of g_{k+1} inside the same launch -> all-reduce(g_{k+1})]* ->
+        quantize(g_last).  Only the first group's amax pass is exposed."""
+        import torch.distributed as dist
+        buf, gs = self.amax_buf, self.groups
+        lo, hi = gs[0]
+        n = self.ops.amax_all(shards[lo:hi], buf[lo:hi])
+        dist.all_reduce(buf[lo:hi], op=dist.ReduceOp.MAX, group=self.group)
+        for k, (lo, hi) in enumerate(gs):
+            if hooks is not None:
+                hooks.before()
+            if k + 1 < len(gs):
+                nlo, nhi = gs[k + 1]
+                n += self.ops.quantize_next_amax(shards[lo:hi], buf[lo:hi], outs[lo:hi],
+                                                 shards[nlo:nhi], buf[nlo:nhi])
+            else:
+                n += self.ops.quantize_all(shards[lo:hi], buf[lo:hi], outs[lo:hi])
+            if hooks is not None:
+                hooks.after()
+            if k + 1 < len(gs):
+                dist.all_reduce(buf[nlo:nhi], op=dist.ReduceOp.MAX, group=self.group)
         return n
 
     def _pipelined(self, shards, outs, hooks) -> int:

@@ -40,6 +40,11 @@ class OracleOps:
     def alloc_out(self, x):
         return {}
 
+    def quantize_next_amax(self, xs, buf, outs, next_xs, next_buf):
+        # the grouped step's fused call: quantize this group, local amaxes of the next
+        self.amax_all(next_xs, next_buf)
+        return self.quantize_all(xs, buf, outs)
+
     def quantize_all(self, xs, buf, outs):
         for x, slot, out in zip(xs, buf, outs):
             if x.shape[0] == 0:
@@ -118,3 +123,20 @@ def test_shard_plan_covers_rows():
             assert got[0][0] == 0 and got[-1][1] == rows
             assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
             assert all(lo <= hi for lo, hi in got)
+
+
+def test_amax_groups_partition():
+    """The grouped sharded step's groups cover every tensor once, in order,
+    with <= 128 tensors each; the first is small (its amax is exposed)."""
+    import ssgen
+    from paper_2605_12464_b200.dist import amax_groups
+    for numels in ([s.rows * s.cols for s in ssgen.workload("c2_qwen3_8b_weights")],
+                   [s.rows * s.cols for s in ssgen.workload("c4_llama70b_kv")],
+                   [7, 0, 3, 100, 5], [1, 1], [0, 0, 0]):
+        g = amax_groups(numels)
+        assert g[0][0] == 0 and g[-1][1] == len(numels)
+        assert all(a[1] == b[0] for a, b in zip(g, g[1:]))
+        assert all(0 < hi - lo <= 128 for lo, hi in g)
+        if len(g) > 1 and sum(numels):
+            assert sum(numels[g[0][0]:g[0][1]]) <= 0.5 * sum(numels) or g[0][1] - g[0][0] == 1
+    assert amax_groups([5]) == [(0, 1)]

@@ -98,3 +98,34 @@ def test_fused_repeated_calls_rearm(ss):
         out, f = _run(ss, ys, -4, 4, fused=True)
         assert f == 0
         _same(out[:min(k, 20)], ref[:min(k, 20)])
+
+
+@pytest.mark.parametrize("window", [(-8, 8), (0, 0)])
+def test_next_amax_call(ss, window):
+    """ss_quantize_nvfp4_batched_next_amax: this group's outputs equal the
+    two-launch path, and the next group's local amaxes equal
+    ss_tensor_amax_batched (empty next tensors give 0; NaN propagates)."""
+    xs = _batch(40, seed=31)
+    nxt = _batch(12, seed=32) + [torch.zeros(0, 16, dtype=torch.bfloat16, device="cuda")]
+    nxt[5] = nxt[5].clone()
+    nxt[5].view(-1)[7] = float("nan")
+    amax = ss.tensor_amax_batched(xs)
+    ref, _ = _run(ss, xs, *window, fused=False)
+    outs = [ss.alloc_out(x) for x in xs]
+    next_amax = torch.full((len(nxt),), 12345, dtype=torch.int32, device="cuda")
+    ss.quantize_batched_next_amax(xs, outs, amax, nxt, next_amax, fmin=window[0], fmax=window[1])
+    torch.cuda.synchronize()
+    _same(outs, ref)
+    want = ss.tensor_amax_batched(nxt)
+    got = next_amax.cpu().numpy().view(np.uint32)
+    exp = want.cpu().numpy().view(np.uint32)
+    for j in range(len(nxt)):
+        if j == 5:
+            assert got[j] >= 0x7F800000 and exp[j] >= 0x7F800000   # NaN sorts above every finite value
+        else:
+            assert got[j] == exp[j], j
+    # no tensors to quantize: only the next amaxes (separate launch)
+    next_amax.fill_(7)
+    ss.quantize_batched_next_amax([], [], amax, nxt[:3], next_amax[:3], radius=8)
+    torch.cuda.synchronize()
+    assert np.array_equal(next_amax[:3].cpu().numpy(), want[:3].cpu().numpy())
