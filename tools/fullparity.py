@@ -1,0 +1,94 @@
+#!/usr/bin/env python
+"""Full-size parity (tools; run on the GPU box): every block of the BASELINE
+workloads through the product call, compared bit for bit with the CPU oracle
+on the box's host cores (OpenMP over blocks).
+
+    python tools/fullparity.py [--configs c2,c4,c3,c5] [--out FILE]
+
+C2 goes layer by layer (the 7 projections of a layer in one batched
+SS_GLOBAL_TENSOR call: the fused-amax persistent kernel), C4 layer by layer
+(K and V in one call), C3 at several radii (one tensor: the two-launch
+path), C5 1 GiB at r = 8.  Inputs are generated once on the device (ssgen,
+seeded) and copied to the host for the oracle, so both sides see the same
+bytes.  One JSON line per config: blocks compared, mismatching codes /
+scales / per-block errors (all must be 0), the worst relative difference of
+the FP64 error sums, and the oracle's time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c2,c4,c3,c5")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    import ssgen
+    import oracle
+    import paper_2605_12464_b200 as ss
+    oracle.build()
+    dev = torch.device("cuda", 0)
+    seed = ssgen.workloads.BASE_SEED
+    lines = []
+
+    def check(name, specs, groups, fmin, fmax):
+        t_or = 0.0
+        nb = bad_c = bad_s = bad_e = 0
+        worst = 0.0
+        for g in groups:
+            xs = [ssgen.generate(specs[k].kind, specs[k].rows, specs[k].cols, seed=seed, tid=specs[k].tid,
+                                 device=dev) for k in g]
+            outs = [ss.alloc_out(x) for x in xs]
+            ss.quantize_batched(xs, outs, fmin=fmin, fmax=fmax, gmode="tensor")
+            torch.cuda.synchronize()
+            assert ss.device_status() == 0
+            for x, o in zip(xs, outs):
+                xc = x.cpu()
+                t0 = time.perf_counter()
+                r = oracle.quantize(xc, x.shape[0], x.shape[1], fmin, fmax, "tensor")
+                t_or += time.perf_counter() - t0
+                nb += x.numel() // 16
+                bad_c += int((o.codes.cpu().numpy().reshape(-1, 8) != r.codes.reshape(-1, 8)).any(1).sum())
+                bad_s += int((o.scales.cpu().numpy().reshape(-1) != r.scales.reshape(-1)).sum())
+                bad_e += int((o.err.cpu().numpy().view(np.uint32) != r.err.view(np.uint32)).any(1).sum())
+                s = o.sums.cpu().numpy()
+                worst = max(worst, float(np.max(np.abs(s - r.sums) / np.maximum(np.abs(r.sums), 1e-300))))
+            del xs, outs
+        line = {"config": name, "window": [fmin, fmax], "blocks": nb, "code_mismatch_blocks": bad_c,
+                "scale_mismatches": bad_s, "err_mismatch_blocks": bad_e, "sums_max_rel_diff": worst,
+                "oracle_s": t_or, "oracle_threads": os.cpu_count(), "ok": bad_c == bad_s == bad_e == 0}
+        print(json.dumps(line), flush=True)
+        lines.append(line)
+
+    cfgs = a.configs.split(",")
+    if "c2" in cfgs:
+        specs = ssgen.workload("c2_qwen3_8b_weights")
+        check("c2_qwen3_8b_weights", specs, [list(range(7 * l, 7 * l + 7)) for l in range(36)], -8, 8)
+    if "c4" in cfgs:
+        specs = ssgen.workload("c4_llama70b_kv")
+        check("c4_llama70b_kv", specs, [[2 * l, 2 * l + 1] for l in range(80)], -8, 8)
+    if "c3" in cfgs:
+        specs = ssgen.workload("c3_act_student_t")
+        for r in (0, 1, 2, 8, 16):
+            check("c3_act_student_t", specs, [[0]], -r, r)
+    if "c5" in cfgs:
+        specs = ssgen.workload("c5_gauss_1gib")
+        check("c5_gauss_1gib", specs, [[0]], -8, 8)
+    if a.out:
+        with open(a.out, "w") as f:
+            for l in lines:
+                f.write(json.dumps(l) + "\n")
+
+
+if __name__ == "__main__":
+    main()
