@@ -29,8 +29,15 @@
  * scales (SS_GLOBAL_ROW, R9b) and other block formats (SS_FMT_*, R19, R20)
  * are opt-in through the _ex / _batched / _fmt entry points.
  *
- * Implementation note: candidates that provably cannot win are skipped
- * (exact branch and bound); outputs are unaffected.
+ * Implementation notes (outputs are unaffected by all of them):
+ *  - candidates that provably cannot win are skipped (exact branch and
+ *    bound);
+ *  - with SS_GLOBAL_TENSOR the amax pass of a multi-tensor batch runs inside
+ *    the quantize launch (§4.2a);
+ *  - a single small tensor (<= 2^19 blocks) takes a one-thread-per-block
+ *    kernel built on the device routine of ss_device.cuh (§4.8);
+ *  - FP32 input: ss_quantize_nvfp4_f32; sharded steps:
+ *    ss_quantize_nvfp4_batched_next_amax (§5).
  *
  * Conventions for every entry point:
  *  - All array arguments are DEVICE pointers owned by the caller unless the
