@@ -28,7 +28,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c2,c4,c3,c5")
+    ap.add_argument("--configs", default="c2,c4,c3,c5,c3row,c5fmt")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     import numpy as np
@@ -70,6 +70,36 @@ def main():
         print(json.dumps(line), flush=True)
         lines.append(line)
 
+    def check_single(name, spec, fmin, fmax, gmode, fmt):
+        x = ssgen.generate(spec.kind, spec.rows, spec.cols, seed=seed, tid=spec.tid, device=dev)
+        o = ss.quantize(x, fmin=fmin, fmax=fmax, gmode=gmode, fmt=fmt)
+        torch.cuda.synchronize()
+        assert ss.device_status() == 0
+        xc = x.cpu()
+        t0 = time.perf_counter()
+        if fmt == "nvfp4":
+            r = oracle.quantize(xc, x.shape[0], x.shape[1], fmin, fmax, gmode)
+        else:
+            r = oracle.quantize_fmt(xc, x.shape[0], x.shape[1], fmin, fmax, fmt=fmt, gmode=gmode)
+        t_or = time.perf_counter() - t0
+        bs = {"nvfp4": 16, "mxfp4": 32, "mxfp6_e2m3": 32, "nvfp6_e2m3": 16}[fmt]
+        nb = x.numel() // bs
+        gc = o.codes.cpu().numpy().reshape(nb, -1)
+        bad_c = int((gc != r.codes.reshape(nb, -1)).any(1).sum())
+        bad_s = int((o.scales.cpu().numpy().reshape(-1) != r.scales.reshape(-1)).sum())
+        bad_e = int((o.err.cpu().numpy().view(np.uint32) != r.err.view(np.uint32)).any(1).sum())
+        bad_g = 0
+        if gmode == "row":
+            bad_g = int((o.G.cpu().numpy().view(np.uint32) != np.asarray(r.G, np.float32).view(np.uint32)).sum())
+        s_ = o.sums.cpu().numpy()
+        worst = float(np.max(np.abs(s_ - r.sums) / np.maximum(np.abs(r.sums), 1e-300)))
+        line = {"config": name, "format": fmt, "gmode": gmode, "window": [fmin, fmax], "blocks": nb,
+                "code_mismatch_blocks": bad_c, "scale_mismatches": bad_s, "err_mismatch_blocks": bad_e,
+                "row_g_mismatches": bad_g, "sums_max_rel_diff": worst, "oracle_s": t_or,
+                "oracle_threads": os.cpu_count(), "ok": bad_c == bad_s == bad_e == bad_g == 0}
+        print(json.dumps(line), flush=True)
+        lines.append(line)
+
     cfgs = a.configs.split(",")
     if "c2" in cfgs:
         specs = ssgen.workload("c2_qwen3_8b_weights")
@@ -84,6 +114,15 @@ def main():
     if "c5" in cfgs:
         specs = ssgen.workload("c5_gauss_1gib")
         check("c5_gauss_1gib", specs, [[0]], -8, 8)
+    if "c3row" in cfgs:     # per-row global scale (row-fused kernel)
+        spec = ssgen.workload("c3_act_student_t")[0]
+        for r in (0, 8):
+            check_single("c3_act_student_t", spec, -r, r, "row", "nvfp4")
+    if "c5fmt" in cfgs:     # the other block formats on C5 1 GiB
+        spec = ssgen.workload("c5_gauss_1gib")[0]
+        check_single("c5_gauss_1gib", spec, -1, 1, "none", "mxfp4")
+        check_single("c5_gauss_1gib", spec, -1, 1, "none", "mxfp6_e2m3")
+        check_single("c5_gauss_1gib", spec, -8, 8, "tensor", "nvfp6_e2m3")
     if a.out:
         with open(a.out, "w") as f:
             for l in lines:
