@@ -385,14 +385,17 @@ bool amax_fusion_enabled() {
 }
 inline int64_t amax_units(int64_t nb) { return (2 * nb + ss::kAmaxUnitVecs - 1) / ss::kAmaxUnitVecs; }
 
-inline bool row_fused(const ss_tensor_io& t, int gmode) {
+// `wide`: the window has >= 4 offsets.  For narrower windows the two-pass path
+// (row-scale grid, then the quantize grid launched with PDL) is faster: C3
+// r = 0 1792 vs 1719 GB/s, r = 1 1462 vs 1427 (profiles/r01/rowbench_v10.jsonl).
+inline bool row_fused(const ss_tensor_io& t, int gmode, bool wide) {
   const int64_t hpr = t.cols / 16;
-  return gmode == SS_GLOBAL_ROW && t.rows > 0 && hpr >= ss::kTaskBlocks && hpr <= 8 * ss::kTaskBlocks &&
-         row_fusion_enabled();
+  return gmode == SS_GLOBAL_ROW && wide && t.rows > 0 && hpr >= ss::kTaskBlocks &&
+         hpr <= 8 * ss::kTaskBlocks && row_fusion_enabled();
 }
-inline int64_t parts_of(const ss_tensor_io& t, int gmode) {
+inline int64_t parts_of(const ss_tensor_io& t, int gmode, bool wide) {
   const int64_t nb = t.rows * t.cols / 16;
-  if (!row_fused(t, gmode)) return tasks_of(nb);
+  if (!row_fused(t, gmode, wide)) return tasks_of(nb);
   return t.rows * ((t.cols / 16 + ss::kTaskBlocks - 1) / ss::kTaskBlocks);
 }
 inline int64_t psegs_of(int64_t parts) { return (parts + ss::kSegTasks - 1) / ss::kSegTasks; }
@@ -509,10 +512,11 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   Workspace* ws = nullptr;
   if (ss_status s = get_ws(dev, stream, &ws)) return s;
 
+  const bool wide = fmax - fmin >= 3;
   int ri = gmode == SS_GLOBAL_ROW ? 1 : 0;
   for (int i = 0; i < count; i++) {
     if (io[i].scale_layout == SS_SCALE_SWIZZLED) ri = std::max(ri, 1);
-    if (row_fused(io[i], gmode)) ri = 2;
+    if (row_fused(io[i], gmode, wide)) ri = 2;
   }
   // fused only where the search is ALU-bound (>= 4 offsets; the HBM crossover is ~3
   // candidates) and where most of the amax can overlap a search:
@@ -556,8 +560,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         tk = gr = 0;
         in_batch = 0;
       }
-      tk += parts_of(io[i], gmode);
-      gr += psegs_of(parts_of(io[i], gmode));
+      tk += parts_of(io[i], gmode, wide);
+      gr += psegs_of(parts_of(io[i], gmode, wide));
       in_batch++;
       any_sums |= io[i].d_err_sums != nullptr;
     }
@@ -589,7 +593,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     for (int i = 0; i < count; i++) amax[i] = io[i].d_amax_bits;
   } else if (gmode == SS_GLOBAL_ROW) {
     std::vector<char> fused(count);
-    for (int i = 0; i < count; i++) fused[i] = row_fused(io[i], gmode);
+    for (int i = 0; i < count; i++) fused[i] = row_fused(io[i], gmode, wide);
     if (ss_status s = rowscale_launch(io, count, fused, ws->flags, numer, cs, info.sms)) return s;
   }
   // swizzled scales: zero the padding of partial 128x4 tiles first
@@ -651,7 +655,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         if (t.d_err_sums && cudaMemsetAsync(t.d_err_sums, 0, 16, cs) != cudaSuccess) return SS_ERR_CUDA;
         continue;
       }
-      const bool rf = row_fused(t, gmode);
+      const bool rf = row_fused(t, gmode, wide);
       int hpr = 0, cpr = 0, upr = 0, cpu = 0;
       int64_t units = tasks_of(nb);
       if (rf) {
@@ -667,7 +671,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         upr = (cpr + cpu - 1) / cpu;
         units = t.rows * upr;
       }
-      const int64_t parts = parts_of(t, gmode);
+      const int64_t parts = parts_of(t, gmode, wide);
       // the kernel indexes units, partials and amax units with 32 bits: close the batch before overflow
       const int64_t au = af_self ? amax_units(nb) : 0;
       if (b.n > 0 && (tk + units > (int64_t)INT32_MAX - ss::kCounters || pk + parts > (int64_t)INT32_MAX ||
