@@ -114,6 +114,9 @@ def main():
     if "c5" in cfgs:
         specs = ssgen.workload("c5_gauss_1gib")
         check("c5_gauss_1gib", specs, [[0]], -8, 8)
+    if "c5big" in cfgs:     # maximum size (8 GiB) and the full brute force (r = 126) on 1 GiB
+        check("c5_gauss_8gib", ssgen.workload("c5_gauss_8gib"), [[0]], -8, 8)
+        check("c5_gauss_1gib", ssgen.workload("c5_gauss_1gib"), [[0]], -126, 126)
     if "c3row" in cfgs:     # per-row global scale (row-fused kernel)
         spec = ssgen.workload("c3_act_student_t")[0]
         for r in (0, 8):
