@@ -1,6 +1,6 @@
 #!/bin/bash
 # One gpurun session: GPU tests, kernel sweep, a bench line, the ncu launch
-# list of our kernels and one full ncu capture of the quantize kernel.
+# list of our kernels, full ncu captures, full-size parity, sharded benches.
 #   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh TAG [steps]'
 TAG=${1:-r01}
 STEPS=${2:-all}
@@ -35,6 +35,10 @@ if has ncu; then
 fi
 if has sweep; then
   timeout 1500 python tools/sweep.py --out gpurun_out/sweep_$TAG.jsonl > gpurun_out/sweep_$TAG.log 2>&1; echo "sweep exit $?" >> gpurun_out/sweep_$TAG.log
+fi
+if has fullparity; then
+  # every block of the BASELINE workloads (and the NEXT rows) against the oracle on the host cores
+  timeout 2400 python tools/fullparity.py --configs c2,c4,c3,c5,c5big,c3row,c5fmt --out gpurun_out/fullparity_$TAG.jsonl > gpurun_out/fullparity_$TAG.log 2>&1; echo "fullparity exit $?" >> gpurun_out/fullparity_$TAG.log
 fi
 if has mrank; then
   # the sharded bench path with 2 ranks sharing the one GPU (gloo carries the amax all-reduce)
