@@ -53,6 +53,12 @@ def parse():
     ap.add_argument("--force-dist", action="store_true",
                     help="test only: initialise the process group and run the sharded path "
                          "(NCCL all-reduces) even with one rank")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: several ranks may share one GPU (testing the sharded path on a "
+                         "1-GPU box); the product uses nccl")
+    ap.add_argument("--exchange", default="grouped", choices=["grouped", "single"],
+                    help="sharded steps: the amax exchange as ONE all-reduce per step (single) or "
+                         "per tensor group with the amax inside the previous quantize launch")
     a = ap.parse_args()
     if a.fmin is None and a.fmax is None:
         a.fmin, a.fmax = -min(a.radius, 126), min(a.radius, 126)
@@ -151,6 +157,18 @@ def oracle_sample(specs, frac_rows: float):
     return out
 
 
+def cpu_model() -> str:
+    """The host CPU (model and core count beside the oracle figure)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def time_oracle(sample, fmin, fmax, threads=0):
     import oracle
     t0 = time.perf_counter()
@@ -187,6 +205,7 @@ def run_reference(a, rank, world):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_dict(a, specs, world),
             "cpu_baseline": {"value": gbs, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": desc},
             "e2e": {"value": gbs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line, a)
@@ -285,9 +304,9 @@ def run_ours(a, rank, world, local_rank):
     import paper_2605_12464_b200 as ss
     from paper_2605_12464_b200.dist import CudaOps, RowShardQuantizer, ShardPlan
 
-    # one process per GPU; SS_DIST_BACKEND=gloo lets several ranks share one
+    # one process per GPU; --dist-backend gloo lets several ranks share one
     # device for testing the sharded path on a 1-GPU box (the product uses NCCL)
-    backend = os.environ.get("SS_DIST_BACKEND", "nccl")
+    backend = a.dist_backend
     dev_idx = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev_idx)
     dev = torch.device("cuda", dev_idx)
@@ -297,6 +316,12 @@ def run_ours(a, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        # every rank announces itself (a scaling run's log shows that N ranks joined)
+        nccl_v = ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None
+        sys.stderr.write("[bench] rank %d/%d on cuda:%d (%s), backend %s%s\n" % (
+            rank, world, dev_idx, torch.cuda.get_device_name(dev), backend,
+            " (NCCL %s)" % nccl_v if nccl_v else ""))
+        sys.stderr.flush()
     ss.lib()
     specs = ssgen.workload(a.workload)
     plan = ShardPlan([(s.rows, s.cols) for s in specs], rank, world)
@@ -307,7 +332,7 @@ def run_ours(a, rank, world, local_rank):
                                      tid=s.tid, row_start=lo, row_end=hi, device=dev))
     ops = CudaOps(a.fmin, a.fmax, want_err=True, want_sums=True)
     outs = [ops.alloc_out(x) for x in shards]
-    q = RowShardQuantizer(plan, ops, group=None, device=dev, collective=dist_on)
+    q = RowShardQuantizer(plan, ops, group=None, device=dev, collective=dist_on, exchange=a.exchange)
     hooks = QuantEvents(torch)
     copies = l2_copies(2 * plan.local_numel())
     shard_sets = [shards] + [[x.clone() for x in shards] for _ in range(copies - 1)]
@@ -367,22 +392,26 @@ def run_ours(a, rank, world, local_rank):
     peak = 148 * FP32_LANES_PER_SM * pk["sm_max_mhz"] * 1e6 / 1e12
     # unsharded runs fuse the amax pass into the quantize launch when the window has
     # >= 4 offsets (ss_api.cu): that kernel reads the input twice
-    from paper_2605_12464_b200.dist import amax_fused
-    fused = not dist_on and amax_fused([x.numel() for x in shards], a.fmin, a.fmax)
+    # the library's own launch plan (ss_quantize_plan): whether the amax ran
+    # inside the quantize launch (it then reads the input twice)
+    fused = not dist_on and bool(ss.plan([tuple(x.shape) for x in shards if x.shape[0]],
+                                         fmin=a.fmin, fmax=a.fmax, gmode="tensor").amax_fused)
     bytes_q = n_local * ((2.0 if fused else 0.0) + 2.0 + 0.5 + 0.0625 + 0.5)  # [amax] + in + codes + scales + err
     hbm_achieved = bytes_q / (quant_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "quant_traffic.json")
     if os.path.exists(tf):
         try:
             with open(tf) as f:
                 tj = json.load(f)
-            traffic = tj["fused" if fused else "plain"]["dram_bytes_per_elem"] * n_local / \
-                ((len(shards) + 127) // 128)
+            tk = tj["fused" if fused else "plain"]
+            traffic = tk["dram_bytes_per_elem"] * n_local / ((len(shards) + 127) // 128)
+            traffic_src = "not measured in this run: DRAM bytes/element of %s scaled to this launch" % (
+                tk.get("source", "profiles/quant_traffic.json"))
         except Exception:
             traffic = None
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
-            "frac": achieved / peak, "traffic": traffic,
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "kernel": "ss::quant_kernel<%d,%d,0,0,%s>" % (-a.fmin, a.fmax, "true" if fused else "false"),
             "amax_fused": fused, "bytes_per_elem": bytes_q / n_local,
             "ops_per_elem": ops_per_elem, "c_eff": ceff,
@@ -438,6 +467,7 @@ def run_ours(a, rank, world, local_rank):
             n, dt, passes = n + dn, dt + ddt, passes + 1
         line["cpu_baseline"] = {
             "value": 2.0 * n / dt / 1e9, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "cpu_model": cpu_model(),
             "threads": "OpenMP over blocks, all %d host cores" % os.cpu_count(),
             "sample": "first 1/8 of the rows of layer 0's 7 projections (%d bf16 elements), "
                       "amax + search, window [%d, %d], %d passes in %.1f s"

@@ -59,6 +59,20 @@
  *  - Reentrant; calls on distinct streams may run concurrently.
  *  - There is no CPU fallback: without an sm_100 device every call returns
  *    SS_ERR_UNSUPPORTED_DEVICE.
+ *  - No environment input: every choice is an argument or compile-time
+ *    (tools build their A/B variants as separate libss_<variant>.so files).
+ *
+ * Differences from the interface sketched in SURVEY.md §8(b) (itself mapped
+ * from SPEC S:150-158):
+ *  - every enqueueing call takes an explicit trailing `stream` argument (or
+ *    an ss_quant_args.stream field) instead of a thread-local stream set by
+ *    ss_set_stream(): a call's stream is visible at the call site, and
+ *    calls from several threads need no per-thread state;
+ *  - ss_tensor_amax takes an `accumulate` flag, so the amaxes of several
+ *    chunks or row shards can be folded into one slot before the all-reduce;
+ *  - ss_quantize_nvfp4 takes the north star's argument list plus `stream`;
+ *    the optional outputs (f*, FP64 sums, G), explicit windows, formats and
+ *    layouts are in ss_quantize_nvfp4_ex / the batched calls.
  */
 #ifndef SS_H
 #define SS_H
@@ -78,7 +92,8 @@ extern "C" {
 typedef enum {
   SS_OK = 0,
   SS_ERR_INVALID_ARG = 1,        /* null pointer, bad size, cols % 16, f_min > 0 or f_max < 0 */
-  SS_ERR_ALIGNMENT = 2,          /* in_bf16 / out_bf16 not 16-B aligned, codes not 8-B aligned */
+  SS_ERR_ALIGNMENT = 2,          /* in_bf16 / out_bf16 not 16-B aligned, E2M1 codes not 8-B   */
+                                 /* aligned, E2M3 codes not 16-B aligned, err not 8-B aligned */
   SS_ERR_CUDA = 3,               /* a CUDA runtime call or launch failed                      */
   SS_ERR_NONFINITE = 4,          /* (device flag) NaN/Inf seen by an amax pass                */
   SS_ERR_RANGE = 5,              /* (device flag) 0 < amax < 2688/FLT_MAX: G overflows        */
@@ -188,7 +203,8 @@ typedef struct {
                                 /* paper's production [-2, 6]                        */
   int global_scale_mode;        /* SS_GLOBAL_*                                              */
   const uint32_t* d_amax_bits;  /* SS_GLOBAL_DEVICE_AMAX: device u32 FP32 bits of the amax  */
-  uint8_t* out_codes;           /* ss_code_bytes(): [rows][cols/2] u8 for E2M1, 8-B aligned */
+  uint8_t* out_codes;           /* ss_code_bytes(): [rows][cols/2] u8 for E2M1, 8-B aligned;*/
+                                /* [rows][cols] u8 for E2M3, 16-B aligned                   */
   uint8_t* out_scales;          /* ss_scale_bytes_fmt(): [rows][cols/bs] u8 or swizzled     */
   float* out_err;               /* nullable: [nb][2] f32 {err_best, err_base}, 8-B aligned; */
                                 /* nb = rows * cols / block size                            */
@@ -210,7 +226,8 @@ typedef struct {
   const void* in_bf16;          /* [rows][cols] bf16, 16-B aligned                         */
   int64_t rows, cols;           /* rows >= 0, cols % 16 == 0                                */
   const uint32_t* d_amax_bits;  /* SS_GLOBAL_DEVICE_AMAX: device u32 amax bits of THIS tensor */
-  uint8_t* out_codes;           /* [rows][cols/2] u8, 8-B aligned                           */
+  uint8_t* out_codes;           /* [rows][cols/2] u8, 8-B aligned (E2M3 formats:             */
+                                /* [rows][cols] u8, 16-B aligned)                           */
   uint8_t* out_scales;          /* [rows][cols/16] u8                                       */
   float* out_err;               /* nullable: [nb][2] f32 {err_best, err_base}, 8-B aligned  */
   int8_t* out_offset;           /* nullable: [nb] f* = c* - c0                               */
@@ -226,10 +243,11 @@ typedef struct {
  * as possible (one persistent grid per 128 tensors, so a step over many
  * small tensors has no per-tensor tail).  SS_GLOBAL_TENSOR computes each
  * tensor's amax inside the quantize launch when the format is NVFP4,
- * the scales are linear and the window has >= 4 offsets (amax warps run ahead
- * of the search; SS_AMAX_FUSION=0 in the environment
- * disables it), else in one batched amax launch first.  Results are
- * bit-identical either way and to per-tensor calls.
+ * the scales are linear, the window has >= 4 offsets and the first tensor
+ * holds at most half of the elements (amax warps run ahead of the search;
+ * DESIGN.md §4.2a), else in one batched amax launch first.  Results are
+ * bit-identical either way and to per-tensor calls; ss_quantize_plan reports
+ * which was chosen.
  */
 SS_API ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min,
                                     int f_max, int global_scale_mode, void* stream);
@@ -244,8 +262,8 @@ SS_API ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int coun
  * step exposes only the first group's amax.
  *   next_in[j]   DEVICE bf16, 16-B aligned, next_n[j] elements (multiple of 16)
  *   next_count   <= 128
- * NVFP4, linear scales; any other case (or SS_AMAX_FUSION=0) computes the
- * next amaxes with a separate launch first.  Results are bit-identical to
+ * NVFP4, linear scales; any other case computes the next amaxes with a
+ * separate launch first.  Results are bit-identical to
  * ss_tensor_amax_batched + ss_quantize_nvfp4_batched.
  */
 SS_API ss_status ss_quantize_nvfp4_batched_next_amax(const ss_tensor_io* tensors, int count, int f_min,
@@ -253,16 +271,27 @@ SS_API ss_status ss_quantize_nvfp4_batched_next_amax(const ss_tensor_io* tensors
                                                      const int64_t* next_n, int next_count,
                                                      uint32_t* next_amax_bits, void* stream);
 
+/*
+ * The launch plan of a batched call, without enqueueing anything (no device
+ * needed; pointers are validated for null / alignment but never read):
+ * which kernels ss_quantize_batched_fmt / ss_quantize_nvfp4_batched would
+ * launch for these arguments.  bench.py reads it for its gpu_launches count
+ * and its traffic model (a fused amax reads the input twice).
+ */
+typedef struct {
+  int amax_fused;   /* 1: SS_GLOBAL_TENSOR amax inside the quantize launch   */
+  int small_path;   /* 1: one small tensor through the one-thread-per-block kernel (§4.8)      */
+  int row_fused;    /* tensors whose per-row amax runs inside the quantize pass (§4.4)         */
+  int launches;     /* kernels the call enqueues (amax, row-scale, quantize, error-sum)        */
+} ss_plan;
+SS_API ss_status ss_quantize_plan(const ss_tensor_io* tensors, int count, int f_min, int f_max,
+                                  int global_scale_mode, int format, ss_plan* out);
+
 /* The same for any block format (SS_FMT_*); windows are clamped to +-126
  * (UE4M3) or +-254 (UE8M0) code steps. */
 SS_API ss_status ss_quantize_batched_fmt(const ss_tensor_io* tensors, int count, int f_min,
                                   int f_max, int global_scale_mode, int format, void* stream);
 
-/*
- * Dequantization (step a8; P:154-162): xhat = RNE_bf16(RN((q * s) / G)).
- *   codes [rows][cols/2] u8 (8-B aligned), scales [rows][cols/16] u8,
- *   d_global_scale nullable (NULL => G = 1), out_bf16 [rows][cols] (16-B aligned).
- */
 /*
  * FP32-input ScaleSearch NVFP4 through the one-thread block routine of
  * include/ss_device.cuh (the search a fused producer, e.g. attention's P
@@ -284,6 +313,11 @@ SS_API ss_status ss_quantize_nvfp4_f32(const float* in, int64_t rows, int64_t co
                                        uint8_t* out_scales, float* out_err, int8_t* out_offset,
                                        void* stream);
 
+/*
+ * Dequantization (step a8; P:154-162): xhat = RNE_bf16(RN((q * s) / G)).
+ *   codes [rows][cols/2] u8 (8-B aligned), scales [rows][cols/16] u8,
+ *   d_global_scale nullable (NULL => G = 1), out_bf16 [rows][cols] (16-B aligned).
+ */
 SS_API ss_status ss_dequantize_nvfp4(const uint8_t* codes, const uint8_t* scales, int64_t rows,
                               int64_t cols, const float* d_global_scale, void* out_bf16,
                               void* stream);
@@ -326,7 +360,7 @@ SS_API ss_status ss_quantize_nvfp4_host_batched(const ss_host_tensor_io* tensors
 
 /* Dequantization with per-row global scales and / or the swizzled layout. */
 typedef struct {
-  const uint8_t* codes;         /* [rows][cols/2] u8, 8-B aligned                           */
+  const uint8_t* codes;         /* [rows][cols/2] u8, 8-B aligned (E2M3: [rows][cols], 16-B) */
   const uint8_t* scales;        /* layout per scale_layout                                  */
   int64_t rows, cols;
   const float* d_global_scale;  /* nullable (G = 1); [1] or, with g_per_row, [rows]         */

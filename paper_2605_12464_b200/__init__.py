@@ -11,13 +11,13 @@ from ._binding import (  # noqa: F401
     GMODES,
     SCALE_LAYOUTS,
     FORMATS,
-    LIB_PATH,
     QuantOut,
     SSError,
     alloc_out,
     dequantize,
     device_status,
     lib,
+    plan,
     quantize,
     quantize_batched,
     quantize_batched_next_amax,
@@ -34,5 +34,5 @@ from ._binding import (  # noqa: F401
 __all__ = [
     "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "quantize_batched_next_amax", "quantize_f32",
     "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host", "quantize_host_batched",
-    "device_status", "scale_bytes", "SCALE_LAYOUTS", "FORMATS", "status_string", "SSError", "QuantOut", "GMODES",
+    "device_status", "scale_bytes", "plan", "SCALE_LAYOUTS", "FORMATS", "status_string", "SSError", "QuantOut", "GMODES",
 ]

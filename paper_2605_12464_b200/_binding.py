@@ -12,10 +12,16 @@ import threading
 from typing import NamedTuple, Optional
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-# SS_LIB_VARIANT selects an alternative in-tree build of the same library
-# (tools/kbench.py compiles kernel-tuning variants as libss_<variant>.so).
-LIB_PATH = os.path.join(PKG, "libss%s.so" % (("_" + os.environ["SS_LIB_VARIANT"])
-                                              if os.environ.get("SS_LIB_VARIANT") else ""))
+LIB_PATH = os.path.join(PKG, "libss.so")
+
+
+def use_variant(name: Optional[str]) -> None:
+    """Tools only: load libss_<name>.so (a tuning / counting build of the same
+    sources, tools/kbench.py) instead of libss.so.  Must precede the first call."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("libss already loaded")
+    LIB_PATH = os.path.join(PKG, "libss%s.so" % ("_" + name if name and name != "base" else ""))
 
 SS_OK, SS_ERR_INVALID_ARG, SS_ERR_ALIGNMENT, SS_ERR_CUDA = 0, 1, 2, 3
 SS_ERR_NONFINITE, SS_ERR_RANGE, SS_ERR_UNSUPPORTED_DEVICE = 4, 5, 6
@@ -86,6 +92,16 @@ class QuantArgs(ctypes.Structure):
     ]
 
 
+class Plan(ctypes.Structure):
+    """ss_plan: the launches a batched call would make (ss_quantize_plan)."""
+    _fields_ = [
+        ("amax_fused", ctypes.c_int),
+        ("small_path", ctypes.c_int),
+        ("row_fused", ctypes.c_int),
+        ("launches", ctypes.c_int),
+    ]
+
+
 class DequantArgs(ctypes.Structure):
     _fields_ = [
         ("codes", ctypes.c_void_p),
@@ -145,6 +161,8 @@ def lib():
             L.ss_quantize_nvfp4_host.argtypes = [P, i64, i64, I, I, I, P, P, P]
             L.ss_quantize_nvfp4_host_batched.restype = I
             L.ss_quantize_nvfp4_host_batched.argtypes = [ctypes.POINTER(HostTensorIO), I, I, I, I]
+            L.ss_quantize_plan.restype = I
+            L.ss_quantize_plan.argtypes = [ctypes.POINTER(TensorIO), I, I, I, I, I, ctypes.POINTER(Plan)]
             L.ss_get_device_status.restype = I
             L.ss_get_device_status.argtypes = [ctypes.POINTER(ctypes.c_int), P]
             _lib = L
@@ -387,3 +405,21 @@ def device_status(stream=None) -> int:
     f = ctypes.c_int(0)
     _check(lib().ss_get_device_status(ctypes.byref(f), _stream_ptr(stream)), "ss_get_device_status")
     return f.value
+
+
+def plan(shapes, radius=None, fmin=None, fmax=None, gmode: str = "tensor", fmt: str = "nvfp4",
+         want_err: bool = True, want_sums: bool = True, scale_layout: str = "linear") -> Plan:
+    """The library's launch plan for a batched call over tensors of these
+    (rows, cols) shapes (ss_quantize_plan; no device needed, nothing runs)."""
+    lo, hi = _window(radius, fmin, fmax)
+    n = len(shapes)
+    dummy = 1 << 20                     # aligned placeholder: the plan never reads pointers
+    arr = (TensorIO * max(n, 1))()
+    gm = GMODES[gmode]
+    for i, (rows, cols) in enumerate(shapes):
+        arr[i] = TensorIO(dummy, rows, cols, dummy if gm == 2 else None, dummy, dummy,
+                          dummy if want_err else None, None, dummy if want_sums else None,
+                          dummy if gm == 3 else None, SCALE_LAYOUTS[scale_layout])
+    out = Plan()
+    _check(lib().ss_quantize_plan(arr, n, lo, hi, gm, FORMATS[fmt][0], ctypes.byref(out)), "ss_quantize_plan")
+    return out

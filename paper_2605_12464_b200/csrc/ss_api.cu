@@ -37,9 +37,14 @@ struct Workspace {
   int64_t part1_cap = 0;
   double2* part2 = nullptr;      // per-segment partial sums
   int64_t part2_cap = 0;
+  // Held while a call grows and uses this workspace and enqueues its
+  // launches.  Calls on distinct streams use distinct workspaces and never
+  // wait for each other; a grow synchronizes only this workspace's stream.
+  std::mutex mu;
 };
 
-std::mutex g_mu;
+std::mutex g_mu;      // the workspace map (lookup / insertion only)
+std::mutex g_dev_mu;  // one-time device queries
 #if defined(SS_COUNT_EVALS) || defined(SS_AF_TRACE)
 unsigned long long* g_evals = nullptr;  // tools-only counting / tracing builds
 #endif
@@ -59,7 +64,7 @@ ss_status device_check(int* dev_out, DeviceInfo* info_out) {
     cudaGetLastError();
     return SS_ERR_UNSUPPORTED_DEVICE;
   }
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(g_dev_mu);
   if (!g_dev_init[dev]) {
     int major = 0, sms = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
@@ -96,7 +101,10 @@ ss_status grow_dev(T** p, int64_t* cap, int64_t need, bool zero, cudaStream_t st
   return SS_OK;
 }
 
+// Workspace of (dev, stream), created on first use.  std::map nodes never
+// move, so the pointer stays valid after g_mu is released.
 ss_status get_ws(int dev, void* stream, Workspace** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
   Workspace& w = g_ws[std::make_pair(dev, stream)];
   if (!w.flags) {
     void* p = nullptr;
@@ -161,15 +169,14 @@ ss_status launch_pdl(void (*k)(Arg), int grid, int block, cudaStream_t st, const
 
 // ---- amax --------------------------------------------------------------------
 int amax_grid(int sms) {
-  static int occ = 0;
-  if (!occ) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ss::amax_kernel, ss::kThreads, 0) !=
-        cudaSuccess) {
+  static const int occ = [] {  // thread-safe one-time query
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ss::amax_kernel, ss::kThreads, 0) != cudaSuccess) {
       cudaGetLastError();
-      occ = 4;
+      o = 4;
     }
-    occ = std::max(occ, 1);
-  }
+    return std::max(o, 1);
+  }();
   return sms * occ;
 }
 
@@ -277,15 +284,14 @@ int occupancy(QuantKernel k) {
 inline int64_t tasks_of(int64_t nb) { return (nb + ss::kTaskBlocks - 1) / ss::kTaskBlocks; }
 
 int sums_grid(int sms) {
-  static int occ = 0;
-  if (!occ) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ss::sums_kernel, ss::kThreads, 0) !=
-        cudaSuccess) {
+  static const int occ = [] {  // thread-safe one-time query
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ss::sums_kernel, ss::kThreads, 0) != cudaSuccess) {
       cudaGetLastError();
-      occ = 4;
+      o = 4;
     }
-    occ = std::max(occ, 1);
-  }
+    return std::max(o, 1);
+  }();
   return sms * occ;
 }
 
@@ -298,7 +304,9 @@ ss_status validate_io(const ss_tensor_io& t, int gmode, const FmtInfo& f) {
   if (t.scale_layout != SS_SCALE_LINEAR && t.scale_layout != SS_SCALE_SWIZZLED)
     return SS_ERR_INVALID_ARG;
   if (nb >= ((int64_t)1 << 31)) return SS_ERR_INVALID_ARG;  // 32-bit block index per tensor
-  if (!aligned(t.in_bf16, 16) || !aligned(t.out_codes, 8) || !aligned(t.out_err, 8) ||
+  // E2M1 codes are stored as one 8-B word per 16-element part, E2M3 codes
+  // (one byte each) as one 16-B vector
+  if (!aligned(t.in_bf16, 16) || !aligned(t.out_codes, f.vf ? 16 : 8) || !aligned(t.out_err, 8) ||
       !aligned(t.d_err_sums, 8) || !aligned(t.d_amax_bits, 4) || !aligned(t.d_global_scale, 4))
     return SS_ERR_ALIGNMENT;
   return SS_OK;
@@ -317,15 +325,14 @@ void row_geometry(int64_t cols, uint32_t* nbr, uint32_t* magic, uint32_t* nkt, i
 }
 
 int rows_grid(int sms) {
-  static int occ = 0;
-  if (!occ) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ss::rowscale_kernel, ss::kThreads, 0) !=
-        cudaSuccess) {
+  static const int occ = [] {  // thread-safe one-time query
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ss::rowscale_kernel, ss::kThreads, 0) != cudaSuccess) {
       cudaGetLastError();
-      occ = 4;
+      o = 4;
     }
-    occ = std::max(occ, 1);
-  }
+    return std::max(o, 1);
+  }();
   return sms * occ;
 }
 
@@ -367,22 +374,21 @@ ss_status rowscale_launch(const ss_tensor_io* io, int count, const std::vector<c
 // and the rows a whole grid has in flight fit in L2 (<= 4736 warps x 16 KB),
 // so the quantize reads after the warp's own amax pass hit L2.  Shorter rows
 // would leave lanes idle, longer ones would re-read HBM: those use the
-// separate rowscale pass.  SS_ROW_FUSION=0 disables it (A/B measurement).
-bool env_off(const char* name) {
-  const char* e = std::getenv(name);
-  return e && e[0] == '0';
-}
-bool row_fusion_enabled() {
-  static const bool on = !env_off("SS_ROW_FUSION");  // thread-safe one-time init
-  return on;
-}
+// separate rowscale pass.  Tools-only builds compile -DSS_ROW_FUSION=0 for
+// the A/B measurement; the library takes no environment input.
+#ifndef SS_ROW_FUSION
+#define SS_ROW_FUSION 1
+#endif
 // SS_GLOBAL_TENSOR, NVFP4, plain layout: the amax pass runs inside the quantize
-// launch (quant_kernel<..., AF>).  SS_AMAX_FUSION=0 restores the separate
-// amax launch (A/B measurement).
-bool amax_fusion_enabled() {
-  static const bool on = !env_off("SS_AMAX_FUSION");
-  return on;
-}
+// launch (quant_kernel<..., AF>); -DSS_AMAX_FUSION=0 (tools-only builds)
+// restores the separate amax launch.
+#ifndef SS_AMAX_FUSION
+#define SS_AMAX_FUSION 1
+#endif
+// Row-fused scheduling units per row (0 = automatic, ~6 units per warp)
+#ifndef SS_ROW_UPR
+#define SS_ROW_UPR 0
+#endif
 inline int64_t amax_units(int64_t nb) { return (2 * nb + ss::kAmaxUnitVecs - 1) / ss::kAmaxUnitVecs; }
 
 // `wide`: the window has >= 4 offsets.  For narrower windows the two-pass path
@@ -391,7 +397,7 @@ inline int64_t amax_units(int64_t nb) { return (2 * nb + ss::kAmaxUnitVecs - 1) 
 inline bool row_fused(const ss_tensor_io& t, int gmode, bool wide) {
   const int64_t hpr = t.cols / 16;
   return gmode == SS_GLOBAL_ROW && wide && t.rows > 0 && hpr >= ss::kTaskBlocks &&
-         hpr <= 8 * ss::kTaskBlocks && row_fusion_enabled();
+         hpr <= 8 * ss::kTaskBlocks && SS_ROW_FUSION;
 }
 inline int64_t parts_of(const ss_tensor_io& t, int gmode, bool wide) {
   const int64_t nb = t.rows * t.cols / 16;
@@ -401,17 +407,14 @@ inline int64_t parts_of(const ss_tensor_io& t, int gmode, bool wide) {
 inline int64_t psegs_of(int64_t parts) { return (parts + ss::kSegTasks - 1) / ss::kSegTasks; }
 
 // ---- small single tensors ------------------------------------------------------
-// Up to SS_SMALL_MAX_BLOCKS (env; default kSmallMaxBlocks) NVFP4 blocks in one
-// tensor go to quant_small_kernel: one thread per block over every resident
-// thread, no candidate table.
-constexpr int64_t kSmallMaxBlocks = 1 << 19;  // 8.4 M elements (C1 = 2^20 blocks: the persistent kernel wins at r = 8)
-int64_t small_max_blocks() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("SS_SMALL_MAX_BLOCKS");
-    return e ? std::max<int64_t>(0, std::atoll(e)) : kSmallMaxBlocks;
-  }();
-  return v;
-}
+// Up to SS_SMALL_MAX_BLOCKS NVFP4 blocks in one tensor go to quant_small_kernel:
+// one thread per block over every resident thread, no candidate table
+// (DESIGN.md §4.8).  2^19 blocks = 8.4 M elements (C1 = 2^20 blocks: the
+// persistent kernel wins at r = 8).
+#ifndef SS_SMALL_MAX_BLOCKS
+#define SS_SMALL_MAX_BLOCKS (1 << 19)
+#endif
+constexpr int64_t kSmallMaxBlocks = SS_SMALL_MAX_BLOCKS;
 
 typedef void (*SmallKernel)(ss::SmallParams);
 SmallKernel pick_small(int fmin, int fmax) {
@@ -489,6 +492,54 @@ struct NextAmax {
   uint32_t* out;
 };
 
+// Launch decisions of one call (shared by quantize_core and ss_quantize_plan).
+struct Plan {
+  bool wide;       // >= 4 offsets: the search is ALU-bound (HBM crossover ~3 candidates)
+  int ri;          // per-block row index level of the quantize kernel (quant_kernel RI)
+  bool af_self;    // SS_GLOBAL_TENSOR: the amax pass inside the quantize launch (§4.2a)
+  bool af_next;    // next-group amaxes inside the first quantize launch (§5)
+  int small;       // index of the one small tensor for quant_small_kernel (§4.8), or -1
+  int n_rowfused;  // tensors whose per-row amax runs inside the quantize pass (§4.4)
+};
+
+Plan make_plan(const ss_tensor_io* io, int count, int fmin, int fmax, int gmode, int format,
+               const NextAmax* next) {
+  Plan p;
+  p.wide = fmax - fmin >= 3;
+  p.ri = gmode == SS_GLOBAL_ROW ? 1 : 0;
+  p.n_rowfused = 0;
+  for (int i = 0; i < count; i++) {
+    if (io[i].scale_layout == SS_SCALE_SWIZZLED) p.ri = std::max(p.ri, 1);
+    if (row_fused(io[i], gmode, p.wide)) {
+      p.ri = 2;
+      p.n_rowfused++;
+    }
+  }
+  // fused only where the search is ALU-bound and where most of the amax can
+  // overlap a search: the first tensor's amax is exposed, so not when it holds
+  // most of the elements (a single tensor: the dedicated amax kernel is faster)
+  int64_t n_all = 0, n_first = -1;
+  int live = -1, nlive = 0;
+  for (int i = 0; i < count; i++) {
+    const int64_t n = io[i].rows * io[i].cols;
+    if (n > 0 && n_first < 0) n_first = n;
+    if (n > 0) {
+      live = i;
+      nlive++;
+    }
+    n_all += n;
+  }
+  p.af_self = gmode == SS_GLOBAL_TENSOR && p.ri == 0 && format == SS_FMT_NVFP4 && p.wide &&
+              2 * n_first <= n_all && SS_AMAX_FUSION;
+  p.af_next = next && next->count > 0 && n_all > 0 && gmode == SS_GLOBAL_DEVICE_AMAX && p.ri == 0 &&
+              format == SS_FMT_NVFP4 && SS_AMAX_FUSION;
+  p.small = (!p.af_next && nlive == 1 && format == SS_FMT_NVFP4 && p.ri == 0 && !p.af_self &&
+             io[live].rows * io[live].cols / 16 <= kSmallMaxBlocks)
+                ? live
+                : -1;
+  return p;
+}
+
 ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
                         void* stream, int format = SS_FMT_NVFP4, const NextAmax* next = nullptr) {
   FmtInfo fi;
@@ -508,31 +559,13 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   const float numer = ss::global_numer(fi.vf);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
 
-  std::lock_guard<std::mutex> lk(g_mu);
   Workspace* ws = nullptr;
   if (ss_status s = get_ws(dev, stream, &ws)) return s;
+  std::lock_guard<std::mutex> wlk(ws->mu);
 
-  const bool wide = fmax - fmin >= 3;
-  int ri = gmode == SS_GLOBAL_ROW ? 1 : 0;
-  for (int i = 0; i < count; i++) {
-    if (io[i].scale_layout == SS_SCALE_SWIZZLED) ri = std::max(ri, 1);
-    if (row_fused(io[i], gmode, wide)) ri = 2;
-  }
-  // fused only where the search is ALU-bound (>= 4 offsets; the HBM crossover is ~3
-  // candidates) and where most of the amax can overlap a search:
-  // the first tensor's amax is exposed, so not when it holds most of the elements
-  // (a single tensor: the dedicated amax kernel is faster)
-  int64_t n_all = 0, n_first = -1;
-  for (int i = 0; i < count; i++) {
-    const int64_t n = io[i].rows * io[i].cols;
-    if (n > 0 && n_first < 0) n_first = n;
-    n_all += n;
-  }
-  const bool af_self = gmode == SS_GLOBAL_TENSOR && ri == 0 && format == SS_FMT_NVFP4 && fmax - fmin >= 3 &&
-                       2 * n_first <= n_all && amax_fusion_enabled();
-  // next-group amaxes ride in the first launch of this call (AF kernel, no waits)
-  const bool af_next = next && next->count > 0 && n_all > 0 && gmode == SS_GLOBAL_DEVICE_AMAX && ri == 0 &&
-                       format == SS_FMT_NVFP4 && amax_fusion_enabled();
+  const Plan pl = make_plan(io, count, fmin, fmax, gmode, format, next);
+  const bool wide = pl.wide, af_self = pl.af_self, af_next = pl.af_next;
+  const int ri = pl.ri;
   if (next && next->count > 0) {
     if (af_next) {
       if (cudaMemsetAsync(next->out, 0, 4 * (size_t)next->count, reinterpret_cast<cudaStream_t>(stream)) !=
@@ -607,21 +640,13 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   }
 
   // one small NVFP4 tensor: one thread per block (quant_small_kernel)
-  if (!af_next) {
-    int live = -1, nlive = 0;
+  if (pl.small >= 0) {
+    const int live = pl.small;
     for (int i = 0; i < count; i++)
-      if (io[i].rows * io[i].cols > 0) {
-        live = i;
-        nlive++;
-      }
-    if (nlive == 1 && format == SS_FMT_NVFP4 && ri == 0 && !af &&
-        io[live].rows * io[live].cols / 16 <= small_max_blocks()) {
-      for (int i = 0; i < count; i++)
-        if (i != live && io[i].d_err_sums && cudaMemsetAsync(io[i].d_err_sums, 0, 16, cs) != cudaSuccess)
-          return SS_ERR_CUDA;
-      return small_launch(io[live], fmin, fmax, gmode == SS_GLOBAL_NONE ? 0 : 1, amax[live], numer, ws, cs,
-                          info.sms);
-    }
+      if (i != live && io[i].d_err_sums && cudaMemsetAsync(io[i].d_err_sums, 0, 16, cs) != cudaSuccess)
+        return SS_ERR_CUDA;
+    return small_launch(io[live], fmin, fmax, gmode == SS_GLOBAL_NONE ? 0 : 1, amax[live], numer, ws, cs,
+                        info.sms);
   }
 
   QuantKernel k = pick_kernel(fmin, fmax, ri, format, af);
@@ -641,7 +666,10 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.tick = ws->tick;
     b.ctr = ws->ctr;
 #if defined(SS_COUNT_EVALS) || defined(SS_AF_TRACE)
-    if (!g_evals && cudaMalloc(&g_evals, 32) == cudaSuccess) cudaMemset(g_evals, 0, 32);
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (!g_evals && cudaMalloc(&g_evals, 32) == cudaSuccess) cudaMemset(g_evals, 0, 32);
+    }
     b.evals = g_evals;
 #endif
     b.flags = ws->flags;
@@ -666,7 +694,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         cpr = (hpr + ss::kTaskBlocks - 1) / ss::kTaskBlocks;
         const int64_t want = (6 * slots * ss::kWarps + t.rows - 1) / t.rows;
         upr = (int)std::min<int64_t>(cpr, std::max<int64_t>(1, want));
-        if (const char* e = std::getenv("SS_ROW_UPR")) upr = std::max(1, std::min(cpr, std::atoi(e)));
+        if (SS_ROW_UPR > 0) upr = std::max(1, std::min(cpr, (int)SS_ROW_UPR));
         cpu = (cpr + upr - 1) / upr;
         upr = (cpr + cpu - 1) / cpu;
         units = t.rows * upr;
@@ -812,7 +840,7 @@ const char* ss_status_string(int s) {
   }
 }
 
-int ss_version(void) { return 400; }
+int ss_version(void) { return 500; }
 
 int64_t ss_scale_bytes(int64_t rows, int64_t cols, int scale_layout) {
   if (rows < 0 || cols < 0 || cols % 16 != 0) return -1;
@@ -902,6 +930,52 @@ ss_status ss_quantize_nvfp4_batched_next_amax(const ss_tensor_io* tensors, int c
   return quantize_core(tensors, count, f_min, f_max, SS_GLOBAL_DEVICE_AMAX, stream, SS_FMT_NVFP4, &nx);
 }
 
+ss_status ss_quantize_plan(const ss_tensor_io* tensors, int count, int f_min, int f_max,
+                          int global_scale_mode, int format, ss_plan* out) {
+  FmtInfo fi;
+  if (!out || !fmt_info(format, &fi)) return SS_ERR_INVALID_ARG;
+  if (count < 0 || (count > 0 && !tensors)) return SS_ERR_INVALID_ARG;
+  if (f_min > 0 || f_max < 0) return SS_ERR_INVALID_ARG;
+  if (global_scale_mode < SS_GLOBAL_NONE || global_scale_mode > SS_GLOBAL_ROW) return SS_ERR_INVALID_ARG;
+  if (fi.sf == 1 && global_scale_mode != SS_GLOBAL_NONE) return SS_ERR_INVALID_ARG;
+  for (int i = 0; i < count; i++)
+    if (ss_status s = validate_io(tensors[i], global_scale_mode, fi)) return s;
+  const int lim = fi.sf ? 254 : 126;
+  const int fmin = std::max(f_min, -lim), fmax = std::min(f_max, lim);
+  const Plan pl = make_plan(tensors, count, fmin, fmax, global_scale_mode, format, nullptr);
+  int live = 0, plain_rows = 0;
+  for (int i = 0; i < count; i++) {
+    if (tensors[i].rows * tensors[i].cols == 0) continue;
+    live++;
+    if (global_scale_mode == SS_GLOBAL_ROW && !row_fused(tensors[i], global_scale_mode, pl.wide)) plain_rows++;
+  }
+  const int per = ss::kMaxTensors;
+  int launches = 0;
+  if (global_scale_mode == SS_GLOBAL_TENSOR && !pl.af_self) launches += (live + per - 1) / per;  // amax_kernel
+  if (global_scale_mode == SS_GLOBAL_ROW) launches += (plain_rows + per - 1) / per;              // rowscale_kernel
+  if (pl.small >= 0) {
+    launches += 1 + (tensors[pl.small].d_err_sums ? 1 : 0);  // quant_small_kernel (+ sums_kernel)
+  } else {
+    int k = 0;
+    bool sums = false;
+    for (int i = 0; i < count; i++) {  // batches of 128 live tensors: quant_kernel (+ sums_kernel)
+      if (tensors[i].rows * tensors[i].cols == 0) continue;
+      sums |= tensors[i].d_err_sums != nullptr;
+      if (++k == per) {
+        launches += 1 + (sums ? 1 : 0);
+        k = 0;
+        sums = false;
+      }
+    }
+    if (k) launches += 1 + (sums ? 1 : 0);
+  }
+  out->amax_fused = pl.af_self ? 1 : 0;
+  out->small_path = pl.small >= 0 ? 1 : 0;
+  out->row_fused = pl.n_rowfused;
+  out->launches = launches;
+  return SS_OK;
+}
+
 ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {
   if (!a) return SS_ERR_INVALID_ARG;
   FmtInfo fi;
@@ -913,7 +987,7 @@ ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {
   if (nb > 0 && (!a->codes || !a->scales || !a->out_bf16)) return SS_ERR_INVALID_ARG;
   if (a->g_per_row && nb > 0 && !a->d_global_scale) return SS_ERR_INVALID_ARG;
   if (nb >= ((int64_t)1 << 31)) return SS_ERR_INVALID_ARG;
-  if (!aligned(a->codes, 8) || !aligned(a->out_bf16, 16)) return SS_ERR_ALIGNMENT;
+  if (!aligned(a->codes, fi.vf ? 16 : 8) || !aligned(a->out_bf16, 16)) return SS_ERR_ALIGNMENT;
   int dev;
   DeviceInfo info;
   if (ss_status s = device_check(&dev, &info)) return s;
@@ -956,10 +1030,7 @@ ss_status ss_quantize_nvfp4_f32(const float* in, int64_t rows, int64_t cols, int
   if (ss_status s = device_check(&dev, &info)) return s;
   if (nb == 0) return SS_OK;
   Workspace* ws = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (ss_status s = get_ws(dev, stream, &ws)) return s;
-  }
+  if (ss_status s = get_ws(dev, stream, &ws)) return s;
   ss::F32Params p;
   p.in = reinterpret_cast<const float4*>(in);
   p.nb = nb;
@@ -1003,10 +1074,7 @@ ss_status ss_get_device_status(int* flags, void* stream) {
   DeviceInfo info;
   if (ss_status s = device_check(&dev, &info)) return s;
   Workspace* ws = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (ss_status s = get_ws(dev, stream, &ws)) return s;
-  }
+  if (ss_status s = get_ws(dev, stream, &ws)) return s;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   uint32_t h = 0;
   if (cudaMemcpyAsync(&h, ws->flags, 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess) return SS_ERR_CUDA;
@@ -1139,8 +1207,12 @@ ss_status ss_quantize_nvfp4_host_batched(const ss_host_tensor_io* t, int count, 
           cudaEventCreateWithFlags(&R.slot_free[k], cudaEventDisableTiming) != cudaSuccess)
         return SS_ERR_CUDA;
   }
-  const size_t per_slot = (size_t)max_n * 2 + (size_t)max_n / 2 + (size_t)max_n / 16 +
-                          (any_err ? (size_t)max_n / 2 : 0) + 256;
+  // every sub-buffer of a slot (and every slot) starts on a 256-B boundary:
+  // the kernels load the input and store E2M1 codes / errors as 16-B and 8-B
+  // vectors
+  auto up256 = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t per_slot = up256((size_t)max_n * 2) + up256((size_t)max_n / 2) + up256((size_t)max_n / 16) +
+                          (any_err ? up256((size_t)max_n / 2) : 0);
   if (per_slot > R.slot_bytes) {
     cudaStreamSynchronize(R.s_h2d);
     cudaStreamSynchronize(R.s_comp);
@@ -1159,11 +1231,9 @@ ss_status ss_quantize_nvfp4_host_batched(const ss_host_tensor_io* t, int count, 
     const int k = i % HostRing::kSlots;
     char* base = reinterpret_cast<char*>(R.mem) + (size_t)k * R.slot_bytes;
     void* d_in = base;
-    uint8_t* d_codes = reinterpret_cast<uint8_t*>(base + (((size_t)n * 2 + 255) & ~(size_t)255));
-    uint8_t* d_scales = d_codes + nb * 8;
-    float* d_err = t[i].h_err ? reinterpret_cast<float*>(
-                                    (reinterpret_cast<uintptr_t>(d_scales + nb) + 7) & ~(uintptr_t)7)
-                              : nullptr;
+    uint8_t* d_codes = reinterpret_cast<uint8_t*>(base + up256((size_t)n * 2));
+    uint8_t* d_scales = d_codes + up256((size_t)nb * 8);
+    float* d_err = t[i].h_err ? reinterpret_cast<float*>(d_scales + up256((size_t)nb)) : nullptr;
     // the slot's previous tensor must be fully copied out before reuse
     if (cudaStreamWaitEvent(R.s_h2d, R.slot_free[k], 0) != cudaSuccess) return SS_ERR_CUDA;
     if (cudaMemcpyAsync(d_in, t[i].h_in_bf16, (size_t)n * 2, cudaMemcpyHostToDevice, R.s_h2d) !=

@@ -27,12 +27,12 @@ def shard_rows(rows: int, rank: int, world: int) -> tuple:
     return lo, min(rows, lo + per)
 
 
-def amax_fused(numels: Sequence[int], fmin: int, fmax: int) -> bool:
-    """Whether libss fuses the amax into the quantize launch for a TENSOR-mode
-    NVFP4 batch (the rule of ss_api.cu quantize_core): >= 4 offsets and a
-    first tensor holding at most half of the elements."""
-    live = [n for n in numels if n > 0]
-    return bool(live) and fmax - fmin >= 3 and 2 * live[0] <= sum(live)
+def amax_fused(shapes: Sequence[tuple], fmin: int, fmax: int) -> bool:
+    """Whether libss runs the amax inside the quantize launch for a TENSOR-mode
+    NVFP4 batch of these (rows, cols) shapes (asked from the library:
+    ss_quantize_plan, so no rule is duplicated here)."""
+    from . import _binding as B
+    return bool(B.plan(list(shapes), fmin=fmin, fmax=fmax, gmode="tensor").amax_fused)
 
 
 def amax_groups(numels: Sequence[int], fractions=(0.04, 0.2), max_group: int = 128) -> List[tuple]:
@@ -89,9 +89,9 @@ class CudaOps:
         live = [k for k, x in enumerate(xs) if x.shape[0] > 0]
         self.B.quantize_batched([xs[k] for k in live], [outs[k] for k in live], fmin=self.fmin,
                                 fmax=self.fmax, gmode="tensor")
-        launches = (len(live) + 127) // 128
-        fused = amax_fused([xs[k].numel() for k in live], self.fmin, self.fmax)
-        return launches * ((2 if self.want_sums else 1) + (0 if fused else 1))
+        p = self.B.plan([tuple(xs[k].shape) for k in live], fmin=self.fmin, fmax=self.fmax, gmode="tensor",
+                        want_err=self.want_err, want_sums=self.want_sums)
+        return p.launches
 
     def quantize_next_amax(self, xs, buf, outs, next_xs, next_buf) -> int:
         """Quantize ``xs`` (all-reduced amaxes in ``buf``) and, in the same launch,
@@ -129,11 +129,23 @@ class ShardPlan:
 class RowShardQuantizer:
     """Quantize a list of tensors whose rows are sharded over ``world`` ranks."""
 
+    EXCHANGES = ("grouped", "single")
+
     def __init__(self, plan: ShardPlan, ops, group=None, device=None, pipeline_groups: int = 1,
-                 collective: bool | None = None):
+                 collective: bool | None = None, exchange: str = "grouped"):
+        """``exchange`` (sharded steps): "single" = the north star's one max
+        all-reduce of every tensor's amax per step (amax launch -> all-reduce ->
+        quantize launch); "grouped" = the same exchange cut into tensor groups
+        so that each group's amax runs inside the previous group's quantize
+        launch (a few all-reduces per step, only the first amax exposed).
+        Outputs are bit-identical either way."""
+        if exchange not in self.EXCHANGES:
+            raise ValueError("exchange must be one of %s" % (self.EXCHANGES,))
         self.plan, self.ops, self.group = plan, ops, group
+        self.exchange = exchange
         # the amax all-reduce runs whenever ranks > 1 (or when forced, to test it with one rank)
         self.collective = plan.world > 1 if collective is None else collective
+        self.allreduces = 0   # all-reduces issued by the last step
         self.amax_buf = ops.new_amax(len(plan.shapes), device)
         self.pipeline_groups = pipeline_groups
         self._side = None
@@ -156,6 +168,7 @@ class RowShardQuantizer:
         events there).
         """
         import torch.distributed as dist
+        self.allreduces = 0
         if not self.collective and self.pipeline_groups <= 1 and hasattr(self.ops, "quantize_local"):
             # unsharded: amax and quantize in one launch per 128 tensors
             if hooks is not None:
@@ -167,11 +180,13 @@ class RowShardQuantizer:
         if not self.collective and self.pipeline_groups > 1 and torch.cuda.is_available() \
                 and len(shards) > 1 and shards[0].is_cuda:
             return self._pipelined(shards, outs, hooks)
-        if self.collective and len(self.groups) > 1 and hasattr(self.ops, "quantize_next_amax"):
+        if self.collective and self.exchange == "grouped" and len(self.groups) > 1 and \
+                hasattr(self.ops, "quantize_next_amax"):
             return self._grouped(shards, outs, hooks)
         n = self.ops.amax_all(shards, self.amax_buf)
-        if self.collective:
+        if self.collective:   # the one exchange step: every tensor's amax in ONE all-reduce
             dist.all_reduce(self.amax_buf, op=dist.ReduceOp.MAX, group=self.group)
+            self.allreduces = 1
         if hooks is not None:
             hooks.before()
         n += self.ops.quantize_all(shards, self.amax_buf, outs)
@@ -188,6 +203,7 @@ class RowShardQuantizer:
         lo, hi = gs[0]
         n = self.ops.amax_all(shards[lo:hi], buf[lo:hi])
         dist.all_reduce(buf[lo:hi], op=dist.ReduceOp.MAX, group=self.group)
+        self.allreduces = len(gs)
         for k, (lo, hi) in enumerate(gs):
             if hooks is not None:
                 hooks.before()

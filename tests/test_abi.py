@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_status_strings(L):
-    assert L.ss_version() == 400
+    assert L.ss_version() == 500
     for s in range(7):
         assert L.ss_status_string(s)
     assert L.ss_status_string(6).decode().startswith("unsupported device")
@@ -135,14 +135,46 @@ def test_device_header_compiles_standalone(tmp_path):
     assert res.returncode == 0, res.stderr
 
 
-def test_amax_fusion_rule():
-    """The Python mirror of ss_api.cu's fusion rule (bench.py's roofline bytes
-    and launch counts depend on it): >= 4 offsets and a first tensor holding
-    at most half of the batch."""
-    from paper_2605_12464_b200.dist import amax_fused
-    assert amax_fused([100, 100], -8, 8)
-    assert amax_fused([0, 100, 100], -2, 1)          # empty tensors are skipped
-    assert not amax_fused([101, 100], -8, 8)         # first tensor dominates
-    assert not amax_fused([100], -8, 8)              # a single tensor: separate amax kernel
-    assert not amax_fused([100, 100], -1, 1)         # HBM-bound window
-    assert not amax_fused([], -8, 8)
+def test_quantize_plan(L):
+    """ss_quantize_plan (no device needed): the fused-amax rule (>= 4 offsets,
+    first tensor <= half of the batch), the small-tensor path,
+    row fusion and the launch counts bench.py reports."""
+    from paper_2605_12464_b200 import _binding as B
+    p = B.plan([(10, 160), (10, 160)], radius=8)
+    assert p.amax_fused == 1 and p.small_path == 0 and p.launches == 2          # quant + sums
+    assert B.plan([(0, 16), (10, 160), (10, 160)], fmin=-2, fmax=1).amax_fused == 1
+    p = B.plan([(11, 160), (10, 160)], radius=8)                                  # first dominates
+    assert p.amax_fused == 0 and p.launches == 3                                  # amax + quant + sums
+    p = B.plan([(10, 160)], radius=8)                                             # one small tensor
+    assert p.amax_fused == 0 and p.small_path == 1 and p.launches == 3
+    assert B.plan([(10, 160)], radius=8, want_sums=False).launches == 2
+    p = B.plan([(4096, 4096)] * 2, radius=1)                                      # HBM-bound window
+    assert p.amax_fused == 0 and p.launches == 3
+    assert B.plan([], radius=8).launches == 0
+    p = B.plan([(64, 64)] * 130, radius=8)                                        # 2 launches of <= 128
+    assert p.amax_fused == 1 and p.launches == 4
+    p = B.plan([(64, 64)] * 130, radius=8, gmode="device_amax", want_sums=False)
+    assert p.launches == 2
+    p = B.plan([(8, 4096), (8, 256)], radius=8, gmode="row")                      # one row-fused tensor
+    assert p.row_fused == 1 and p.launches == 1 + 1 + 1                            # rowscale + quant + sums
+    assert B.plan([(8, 4096)], radius=1, gmode="row").row_fused == 0              # narrow: two-pass
+    with pytest.raises(B.SSError):
+        B.plan([(4, 24)], radius=8)
+
+
+def test_e2m3_codes_need_16_byte_alignment(L):
+    """E2M3 codes are stored as 16-B vectors: 8-B aligned code buffers are
+    rejected synchronously (quantize and dequantize), E2M1 ones accepted."""
+    from paper_2605_12464_b200 import _binding as B
+    buf = ctypes.create_string_buffer(8192)
+    base = (ctypes.addressof(buf) + 255) // 256 * 256
+    for fmt, want in (("nvfp6_e2m3", B.SS_ERR_ALIGNMENT), ("mxfp6_e2m3", B.SS_ERR_ALIGNMENT)):
+        io = (B.TensorIO * 1)(B.TensorIO(base, 2, 32, None, base + 1024 + 8, base + 2048, None, None, None,
+                                         None, 0))
+        assert L.ss_quantize_batched_fmt(io, 1, -1, 1, 0, B.FORMATS[fmt][0], None) == want
+        d = B.DequantArgs(base + 8, base + 2048, 2, 32, None, 0, 0, base + 4096, None, B.FORMATS[fmt][0])
+        assert L.ss_dequantize_nvfp4_ex(ctypes.byref(d)) == want
+    # an 8-B aligned E2M1 code buffer passes validation (then: no device here, or it runs)
+    io = (B.TensorIO * 1)(B.TensorIO(base, 2, 32, None, base + 1024 + 8, base + 2048, None, None, None,
+                                     None, 0))
+    assert L.ss_quantize_batched_fmt(io, 1, -1, 1, 0, B.FORMATS["mxfp4"][0], None) != B.SS_ERR_ALIGNMENT

@@ -28,13 +28,19 @@ class OracleOps:
     def __init__(self):
         import oracle
         self.o = oracle
+        self.nonfinite = set()     # tensors whose all-reduced amax was NaN/Inf (the library's flag)
 
     def new_amax(self, n, device):
         return torch.zeros(n, dtype=torch.int32)
 
     def amax_all(self, xs, buf):
         for k, x in enumerate(xs):
-            buf[k] = self.o.tensor_amax(x) if x.numel() else 0
+            if not x.numel():
+                buf[k] = 0
+            elif not torch.isfinite(x.float()).all():
+                buf[k] = 0x7FC00000           # |NaN| bits sort above every finite value (R14)
+            else:
+                buf[k] = self.o.tensor_amax(x)
         return 1
 
     def alloc_out(self, x):
@@ -47,10 +53,15 @@ class OracleOps:
 
     def quantize_all(self, xs, buf, outs):
         for x, slot, out in zip(xs, buf, outs):
+            bits = int(slot.item()) & 0xFFFFFFFF
+            out["amax_bits"] = bits
             if x.shape[0] == 0:
                 continue
-            r = self.o.quantize(x, x.shape[0], x.shape[1], FMIN, FMAX, "given",
-                                amax_bits=int(slot.item()) & 0xFFFFFFFF)
+            if bits >= 0x7F800000:            # the library: sticky flag, G = 1 (R14)
+                out["nonfinite"] = True
+                out["G"] = 1.0
+                continue
+            r = self.o.quantize(x, x.shape[0], x.shape[1], FMIN, FMAX, "given", amax_bits=bits)
             out.update(codes=r.codes, scales=r.scales, err=r.err, G=r.G)
         return 1
 
@@ -60,7 +71,7 @@ def _tensors():
             for k, (r, c) in enumerate(SHAPES)]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, exchange="grouped", nan_at=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -68,10 +79,14 @@ def _worker(rank, world, port, q):
         full = _tensors()
         plan = ShardPlan(SHAPES, rank, world)
         shards = [x[slice(*plan.rows(k))].contiguous() for k, x in enumerate(full)]
+        if nan_at is not None and nan_at[0] == rank:       # fault injection on ONE rank's shard
+            k, r, c = nan_at[1:]
+            shards[k][r, c] = float("nan")
         ops = OracleOps()
         outs = [ops.alloc_out(x) for x in shards]
-        qz = RowShardQuantizer(plan, ops, group=None, device="cpu")
+        qz = RowShardQuantizer(plan, ops, group=None, device="cpu", exchange=exchange)
         n = qz.step(shards, outs)
+        assert qz.allreduces == (1 if exchange == "single" else len(qz.groups))
         gathered = [None] * world
         dist.all_gather_object(gathered, [{k: (v if not isinstance(v, np.ndarray) else v.copy())
                                            for k, v in o.items()} for o in outs])
@@ -89,22 +104,36 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_row_shards_equal_whole_tensor(oracle_lib, world):
+def _run(world, exchange="grouped", nan_at=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, exchange, nan_at)) for r in range(world)]
     for p in procs:
         p.start()
-    n, gathered = q.get(timeout=300)
+    import queue
+    import time
+    t0 = time.time()
+    while True:                     # fail fast if a worker dies instead of waiting out the timeout
+        try:
+            n, gathered = q.get(timeout=2)
+            break
+        except queue.Empty:
+            assert all(p.exitcode in (None, 0) for p in procs), [p.exitcode for p in procs]
+            assert time.time() - t0 < 300
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return n, gathered
+
+
+@pytest.mark.parametrize("world,exchange", [(2, "grouped"), (3, "grouped"), (2, "single"), (3, "single")])
+def test_row_shards_equal_whole_tensor(oracle_lib, world, exchange):
+    n, gathered = _run(world, exchange)
     assert n > 0
     for k, x in enumerate(_tensors()):
         whole = oracle_lib.quantize(x, x.shape[0], x.shape[1], FMIN, FMAX, "tensor")
-        parts = [g[k] for g in gathered if g[k]]
+        parts = [g[k] for g in gathered if "codes" in g[k]]
         codes = np.concatenate([p["codes"] for p in parts], 0)
         scales = np.concatenate([p["scales"] for p in parts], 0)
         err = np.concatenate([p["err"] for p in parts], 0)
@@ -113,6 +142,32 @@ def test_row_shards_equal_whole_tensor(oracle_lib, world):
         assert np.array_equal(err.view(np.uint32), whole.err.view(np.uint32)), k
         # every rank derived the same global scale from the all-reduced amax
         assert all(np.float32(p["G"]) == np.float32(whole.G) for p in parts)
+
+
+@pytest.mark.parametrize("exchange", ["grouped", "single"])
+def test_nan_on_one_rank_flags_every_rank(oracle_lib, exchange):
+    """SURVEY §5 fault injection: a NaN in ONE rank's shard of tensor 3 reaches
+    every rank through the max all-reduce of the amax bit patterns (NaN bits
+    sort above every finite value, R14): every rank's slot for that tensor is
+    non-finite, so each flags it and uses G = 1; the other tensors are
+    untouched and still equal the whole-tensor quantization."""
+    world = 2
+    n, gathered = _run(world, exchange, nan_at=(1, 3, 8, 7))    # rank 1 holds rows 32..63 of tensor 3
+    for g in gathered:
+        assert g[3]["amax_bits"] >= 0x7F800000
+        if "codes" in g[3] or g[3].get("nonfinite"):
+            assert g[3].get("nonfinite") and g[3]["G"] == 1.0
+    for k, x in enumerate(_tensors()):
+        if k == 3:
+            continue
+        whole = oracle_lib.quantize(x, x.shape[0], x.shape[1], FMIN, FMAX, "tensor")
+        parts = [g[k] for g in gathered if "codes" in g[k]]
+        assert np.array_equal(np.concatenate([p["codes"] for p in parts], 0), whole.codes), k
+        assert all(g[k]["amax_bits"] == whole_amax(oracle_lib, x) for g in gathered)
+
+
+def whole_amax(o, x):
+    return o.tensor_amax(x)
 
 
 def test_shard_plan_covers_rows():

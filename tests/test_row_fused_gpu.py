@@ -6,7 +6,7 @@ chunks) instead of a separate rowscale pass.  Everything stays bit-exact
 against the oracle's mode "row": codes, scales, offsets, per-block errors and
 the G_r array, across
 - exact and ragged last chunks (cols % 1024 != 0),
-- rows split over several scheduling units (few rows: upr > 1; SS_ROW_UPR),
+- rows cut into units of one chunk (few rows) and of several chunks (many rows),
 - the size limits on both sides (hpr 63 / 64, 512 / 513: the two-pass path),
 - fixed and runtime windows, both scale layouts, E2M3 values and 64/256 blocks,
 - batches mixing fused, two-pass and per-tensor tensors, with error sums.
@@ -68,12 +68,13 @@ def test_row_fused_swizzled(ss, oracle_lib, shape):
     _cmp(g, oracle_lib.quantize(x, *shape, -8, 8, "row"), swz=True)
 
 
-@pytest.mark.parametrize("upr", ["1", "2", "3", "8"])
-def test_row_fused_unit_split(ss, oracle_lib, upr, monkeypatch):
-    """A row's chunks split over 1..8 scheduling units (each recomputes G_r)."""
-    monkeypatch.setenv("SS_ROW_UPR", upr)
-    shape = (77, 8192)
-    x = ssgen.generate("gaussian", *shape, seed=43, tid=int(upr))
+@pytest.mark.parametrize("shape", [(4096, 8192), (12000, 8192), (16384, 4096)])
+def test_row_fused_unit_split(ss, oracle_lib, shape):
+    """Large row counts: the library gives a scheduling unit several chunks of
+    a row (cpu > 1, about 6 units per warp of the grid), while the shapes
+    above give one chunk per unit (each unit recomputes G_r)."""
+    assert ss.plan([shape], radius=8, gmode="row").row_fused == 1
+    x = ssgen.generate("gaussian", *shape, seed=43, tid=shape[0])
     g = ss.quantize(x.cuda(), radius=8, gmode="row")
     torch.cuda.synchronize()
     _cmp(g, oracle_lib.quantize(x, *shape, -8, 8, "row"))

@@ -35,8 +35,8 @@ def main():
         for v, d in VARIANTS.items():
             build.build(variant=v, defines=d)
         return
-    if a.variant != "base":
-        os.environ["SS_LIB_VARIANT"] = a.variant
+    from paper_2605_12464_b200 import _binding
+    _binding.use_variant(a.variant)
     import torch
     import ssgen
     import paper_2605_12464_b200 as ss

@@ -10,8 +10,8 @@ fits in L2) of
   sep    ss_tensor_amax_batched + ss_quantize_nvfp4_batched(DEVICE_AMAX)
   fused  ss_quantize_nvfp4_batched(TENSOR)   (amax units inside the launch)
 and whether the fused outputs (codes, scales, errors, sums, G) equal the
-separate path's bit for bit.  Run with SS_AMAX_FUSION=0 to time the TENSOR
-call without fusion (the library reads it once per process).
+separate path's bit for bit.  --variant noamaxfusion (a build with
+-DSS_AMAX_FUSION=0, tools/kbench.py build) times the TENSOR call without fusion.
 """
 from __future__ import annotations
 
@@ -28,8 +28,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1_gauss4096,c2_qwen3_8b_weights,c4_llama70b_kv")
     ap.add_argument("--windows", default="-8:8,0:0")
+    ap.add_argument("--variant", default="base")
     ap.add_argument("--reps", type=int, default=7)
     a = ap.parse_args()
+    from paper_2605_12464_b200 import _binding
+    _binding.use_variant(a.variant)
     import torch
     import ssgen
     import paper_2605_12464_b200 as ss
@@ -77,7 +80,7 @@ def main():
                        for f in ("codes", "scales", "err", "offsets", "sums", "G")
                        if getattr(oa, f) is not None)
             print(json.dumps({"config": cfg, "window": [fmin, fmax], "tensors": len(xs), "elements": n,
-                              "fusion_env": os.environ.get("SS_AMAX_FUSION", "1"),
+                              "variant": a.variant,
                               "sep_ms": t_sep, "fused_ms": t_fused, "speedup": t_sep / t_fused,
                               "sep_gbs": 2 * n / t_sep / 1e6, "fused_gbs": 2 * n / t_fused / 1e6,
                               "bit_identical": bool(same),

@@ -5,7 +5,7 @@ builds (variants compiled with different -D flags) on a fixed synthetic batch.
     python tools/kbench.py build                 # here (CPU): compile the variants
     python tools/kbench.py run [--variants a,b]  # on the GPU box: one JSON line per case
 
-Each variant runs in its own process (SS_LIB_VARIANT selects libss_<v>.so).
+Each variant runs in its own process (_binding.use_variant loads libss_<v>.so).
 Timing: CUDA events on the launching stream, 3 warm-ups, median of 10; the
 batch (first LAYERS layers of the Qwen3-8B workload, > 1 GB) exceeds L2.
 Not the driver's bench: that is bench.py.
@@ -31,6 +31,13 @@ VARIANTS = {
     "mb3": ["SS_MIN_BLOCKS=3"],
     "prune2": ["SS_PRUNE_FROM=2"],
     "prune4": ["SS_PRUNE_FROM=4"],
+    # the library's former environment switches, now compile-time (A/B builds)
+    "noamaxfusion": ["SS_AMAX_FUSION=0"],
+    "norowfusion": ["SS_ROW_FUSION=0"],
+    "rowupr1": ["SS_ROW_UPR=1"],
+    "rowupr2": ["SS_ROW_UPR=2"],
+    "rowupr4": ["SS_ROW_UPR=4"],
+    "nosmall": ["SS_SMALL_MAX_BLOCKS=0"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
 
@@ -48,8 +55,8 @@ def build(names):
 def run_one(variant, layers, windows, reps, layout="linear"):
     import torch
     import ssgen
-    if variant != "base":
-        os.environ["SS_LIB_VARIANT"] = variant
+    from paper_2605_12464_b200 import _binding
+    _binding.use_variant(variant)
     import paper_2605_12464_b200 as ss
     dev = torch.device("cuda", 0)
     specs = ssgen.workload("c2_qwen3_8b_weights")[: 7 * layers]

@@ -77,6 +77,51 @@ def full(rep: str):
             print("| %s | %d | %.1f%% |" % (op, n, 100.0 * n / tot))
 
 
+def hot(rep: str, top: int = 60):
+    """SASS-line stall attribution from the source page: warp-stall samples per
+    stall reason, totals by opcode, and the hottest lines with their top reasons."""
+    src = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass"))))
+    if len(src) < 3:
+        print("no source page")
+        return
+    h = src[1]
+    sc, ss_, ie = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
+    reasons = [c for c in h if c.startswith("stall_") and not c.endswith("(Not Issued)")]
+    ri = [h.index(c) for c in reasons]
+    rows, tot_r, by_op, tot = [], Counter(), Counter(), 0
+    for k, r in enumerate(src[2:]):
+        try:
+            smp = int(r[ss_] or 0)
+        except (ValueError, IndexError):
+            continue
+        op = re.sub(r"^@!?U?P\w+\s+", "", r[sc].strip()).split()
+        opn = op[0] if op else "?"
+        rv = {}
+        for c, i in zip(reasons, ri):
+            try:
+                v = int(r[i] or 0)
+            except ValueError:
+                v = 0
+            if v:
+                rv[c[6:]] = v
+                tot_r[c[6:]] += v
+        by_op[opn] += smp
+        tot += smp
+        rows.append((smp, k, r[sc].strip(), int(r[ie] or 0) if r[ie].isdigit() else 0, rv))
+    print("warp-stall samples: %d\n" % tot)
+    print("| reason | samples | share |\n|---|---|---|")
+    for c, v in tot_r.most_common():
+        print("| %s | %d | %.1f%% |" % (c, v, 100.0 * v / max(tot, 1)))
+    print("\n| opcode | samples | share |\n|---|---|---|")
+    for c, v in by_op.most_common(25):
+        print("| %s | %d | %.1f%% |" % (c, v, 100.0 * v / max(tot, 1)))
+    print("\nhottest SASS lines (index in the listing, samples, executed, top reasons):\n")
+    print("| # | samples | share | executed | instruction | reasons |\n|---|---|---|---|---|---|")
+    for smp, k, txt, n, rv in sorted(rows, key=lambda t: -t[0])[:top]:
+        rs = ", ".join("%s %d" % kv for kv in sorted(rv.items(), key=lambda kv: -kv[1])[:3])
+        print("| %d | %d | %.2f%% | %d | `%s` | %s |" % (k, smp, 100.0 * smp / max(tot, 1), n, txt[:70], rs))
+
+
 def launches(path: str):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -99,4 +144,4 @@ def launches(path: str):
 
 
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2])
+    {"full": full, "launches": launches, "hot": hot}[sys.argv[1]](sys.argv[2])

@@ -16,6 +16,8 @@ import argparse
 import json
 import os
 import subprocess
+
+VARIANT = "base"
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -54,7 +56,7 @@ def one(mode, reps):
             ms = a.elapsed_time(b) / reps
             print(json.dumps({"shape": name, "mode": mode, "radius": r, "ms": ms,
                               "bf16_gbs": 2 * x.numel() / ms / 1e6,
-                              "upr": os.environ.get("SS_ROW_UPR", "auto")}), flush=True)
+                              "variant": VARIANT}), flush=True)
         del x, out
         torch.cuda.empty_cache()
 
@@ -64,17 +66,21 @@ def main():
     ap.add_argument("--one", default=None)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--variant", default="base")
     a = ap.parse_args()
+    global VARIANT
+    VARIANT = a.variant
+    from paper_2605_12464_b200 import _binding
+    _binding.use_variant(a.variant)
     if a.one:
         one(a.one, a.reps)
         return
-    runs = [("row_fused", {}), ("row_twopass", {"SS_ROW_FUSION": "0"}), ("tensor", {}),
-            ("row_fused", {"SS_ROW_UPR": "1"}), ("row_fused", {"SS_ROW_UPR": "2"}),
-            ("row_fused", {"SS_ROW_UPR": "4"})]
+    # A/B builds from tools/kbench.py build --variants norowfusion,rowupr1,rowupr2,rowupr4
+    runs = [("row_fused", "base"), ("row_twopass", "norowfusion"), ("tensor", "base"),
+            ("row_fused", "rowupr1"), ("row_fused", "rowupr2"), ("row_fused", "rowupr4")]
     lines = []
-    for mode, env in runs:
-        e = dict(os.environ, **env)
-        r = subprocess.run([sys.executable, __file__, "--one", mode, "--reps", str(a.reps)], env=e,
+    for mode, var in runs:
+        r = subprocess.run([sys.executable, __file__, "--one", mode, "--reps", str(a.reps), "--variant", var],
                            capture_output=True, text=True, timeout=900)
         sys.stderr.write(r.stderr[-2000:])
         for ln in r.stdout.splitlines():

@@ -6,7 +6,7 @@ ALU / HBM roofline fractions, valid-candidate count, and the MSE cut.
     python tools/sweep.py [--configs c1,c2,c3,c4,c5] [--out gpurun_out/sweep.jsonl]
 
 Timing: CUDA events on the launching stream around `reps` back-to-back calls
-(2 warm-ups first).  With SS_LIB_VARIANT=count (libss_count.so) each line also
+(2 warm-ups first).  With --variant count (libss_count.so) each line also
 carries the candidate evaluations the kernel executed per block (exact pruning
 skips the rest) and the ALU fraction of that executed work.
 C1 (33.5 MB) is rotated over 40 copies (> L2) between runs; the others
@@ -34,6 +34,9 @@ def peaks():
         return float(m["hbm_gbs"]), float(m["sm_max_mhz"])
     except Exception:
         return 6650.0, 1965.0
+
+
+VARIANT = "base"
 
 
 def med(ts):
@@ -67,7 +70,7 @@ def measure(torch, ss, groups, fmin, fmax, reps=5, fmt="nvfp4"):
     for i in range(len(groups)):
         ss.tensor_amax_batched(groups[i], out=amax[i])
     res = {}
-    if os.environ.get("SS_LIB_VARIANT") == "count":   # executed evaluations, one pass
+    if VARIANT == "count":   # executed evaluations, one pass
         import ctypes
         L = ss.lib()
         L.ss_debug_take_evals.restype = ctypes.c_ulonglong
@@ -161,7 +164,12 @@ def main():
     ap.add_argument("--configs", default="c1,oracle,c2,c3,c4,f32,paper_tab,c5,formats")
     ap.add_argument("--c5-gib", default="1,8")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--variant", default="base", help="tools build libss_<variant>.so (e.g. count)")
     a = ap.parse_args()
+    global VARIANT
+    VARIANT = a.variant
+    from paper_2605_12464_b200 import _binding
+    _binding.use_variant(a.variant)
     hbm, mhz = peaks()
     dev = torch.device("cuda", 0)
     lines = []
