@@ -28,9 +28,13 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--fmt", default="nvfp4")
     ap.add_argument("--tensors", type=int, default=0, help="first N tensors only (0 = all)")
+    ap.add_argument("--variant", default="base", help="libss_<variant>.so (tools/kbench.py build)")
     a = ap.parse_args()
     import torch
     import ssgen
+    if a.variant != "base":
+        from paper_2605_12464_b200 import _binding
+        _binding.use_variant(a.variant)
     import paper_2605_12464_b200 as ss
     fmin, fmax = (int(v) for v in a.window.split(":"))
     dev = torch.device("cuda", 0)
