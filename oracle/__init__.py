@@ -28,4 +28,12 @@ from .oracle import (  # noqa: F401
     quantize_fmt,
     dequantize_fmt,
     OracleError,
+    gen_value,
+    gen_encode,
+    gen_scale_value,
+    gen_scale_encode,
+    gen_numer,
+    search_block_gen,
+    quantize_gen,
+    dequantize_gen,
 )

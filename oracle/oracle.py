@@ -96,6 +96,24 @@ def lib():
                                             P, ctypes.c_int, P]
             L.so_dequantize.restype = ctypes.c_int
             L.so_dequantize.argtypes = [P, P, i64, i64, ctypes.c_float, P]
+            ci = ctypes.c_int
+            L.so_gen_value.restype = ctypes.c_double
+            L.so_gen_value.argtypes = [ci, ci, ci]
+            L.so_gen_encode.restype = ci
+            L.so_gen_encode.argtypes = [ci, ci, ctypes.c_float]
+            L.so_gen_scale_value.restype = ctypes.c_double
+            L.so_gen_scale_value.argtypes = [ci, ci, ci]
+            L.so_gen_scale_encode.restype = ci
+            L.so_gen_scale_encode.argtypes = [ci, ci, ctypes.c_float]
+            L.so_gen_numer.restype = ctypes.c_float
+            L.so_gen_numer.argtypes = [ci, ci, ci, ci]
+            L.so_search_block_gen.restype = ci
+            L.so_search_block_gen.argtypes = [ci, ci, ci, ci, ci, P, ci, ci, ctypes.POINTER(_BlockResultFmt)]
+            L.so_quantize_gen.restype = ci
+            L.so_quantize_gen.argtypes = [P, i64, i64, ci, ci, ci, P, ci, ci, ci, ci, ci, P, P, P, P, P,
+                                          P, P, ci]
+            L.so_dequantize_gen.restype = ci
+            L.so_dequantize_gen.argtypes = [P, P, i64, i64, ci, ci, ci, ci, ci, ctypes.c_float, P]
             _LIB = L
     return _LIB
 
@@ -288,4 +306,77 @@ def dequantize_fmt(codes, scales, rows: int, cols: int, fmt="mxfp4", G=1.0) -> n
     out = np.empty((rows, cols), np.uint16)
     _check(lib().so_dequantize_fmt(_ptr(codes), _ptr(scales), rows, cols, vf, sf, bs, _ptr(g),
                                    int(g.size > 1), _ptr(out)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Generic ExMy formats (fig:nvfp-scale / fig:nvfp-val /
+# fig:mxfp P:237-260; reading R21).  A format is
+# (value_e, value_m, scale_e, scale_m, block).
+# ---------------------------------------------------------------------------
+class _BlockResultFmt(ctypes.Structure):
+    _fields_ = [("c0", ctypes.c_int32), ("cstar", ctypes.c_int32), ("fstar", ctypes.c_int32),
+                ("n_evaluated", ctypes.c_int32), ("err_best", ctypes.c_float),
+                ("err_base", ctypes.c_float), ("code", ctypes.c_uint8 * 256)]
+
+
+def gen_value(e: int, m: int, code: int) -> float:
+    return lib().so_gen_value(int(e), int(m), int(code))
+
+
+def gen_encode(e: int, m: int, t: float) -> int:
+    return lib().so_gen_encode(int(e), int(m), float(t))
+
+
+def gen_scale_value(e: int, m: int, code: int) -> float:
+    return lib().so_gen_scale_value(int(e), int(m), int(code))
+
+
+def gen_scale_encode(e: int, m: int, v: float) -> int:
+    return lib().so_gen_scale_encode(int(e), int(m), float(v))
+
+
+def gen_numer(ve: int, vm: int, se: int, sm: int) -> float:
+    return lib().so_gen_numer(int(ve), int(vm), int(se), int(sm))
+
+
+def search_block_gen(y, fmt, fmin: int, fmax: int) -> BlockResult:
+    ve, vm, se, sm, bs = fmt
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float32))
+    assert y.shape == (bs,)
+    r = _BlockResultFmt()
+    _check(lib().so_search_block_gen(ve, vm, se, sm, bs, _ptr(y), int(fmin), int(fmax), ctypes.byref(r)))
+    return BlockResult(r.c0, r.cstar, r.fstar, r.n_evaluated, r.err_best, r.err_base,
+                       np.frombuffer(bytes(r.code), np.uint8)[:bs].copy())
+
+
+def quantize_gen(x, rows: int, cols: int, fmin: int, fmax: int, fmt, gmode="tensor",
+                 amax_bits: int | None = None, threads: int = 0) -> QuantResult:
+    """so_quantize_gen: codes [rows][cols] one per byte, scales [rows][cols/bs]."""
+    ve, vm, se, sm, bs = fmt
+    x = _as_u16(x).reshape(-1)
+    assert x.size == rows * cols
+    gm = {"none": 0, "tensor": 1, "given": 2}[gmode] if isinstance(gmode, str) else int(gmode)
+    nb = rows * cols // bs
+    codes = np.empty((rows, cols), np.uint8)
+    scales = np.empty((rows, cols // bs), np.uint8)
+    offs = np.empty(nb, np.int8)
+    err = np.empty((nb, 2), np.float32)
+    sums = np.zeros(2, np.float64)
+    neval = np.zeros(1, np.int64)
+    G = np.zeros(1, np.float32)
+    ab = None if amax_bits is None else np.array([amax_bits], np.uint32)
+    _check(lib().so_quantize_gen(_ptr(x), rows, cols, int(fmin), int(fmax), gm, _ptr(ab), ve, vm, se, sm,
+                                 bs, _ptr(codes), _ptr(scales), _ptr(offs), _ptr(err), _ptr(sums),
+                                 _ptr(neval), _ptr(G), int(threads)))
+    return QuantResult(codes, scales, offs, err, sums, int(neval[0]), float(G[0]))
+
+
+def dequantize_gen(codes, scales, rows: int, cols: int, fmt, G=1.0) -> np.ndarray:
+    ve, vm, se, sm, bs = fmt
+    codes = np.ascontiguousarray(codes, np.uint8)
+    scales = np.ascontiguousarray(scales, np.uint8)
+    out = np.empty((rows, cols), np.uint16)
+    _check(lib().so_dequantize_gen(_ptr(codes), _ptr(scales), rows, cols, ve, vm, se, sm, bs,
+                                   ctypes.c_float(G), _ptr(out)))
     return out

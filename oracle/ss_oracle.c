@@ -641,3 +641,271 @@ int so_dequantize_fmt(const uint8_t* codes, const uint8_t* scales, int64_t rows,
   }
   return 0;
 }
+
+
+/* ====================================================================== */
+/* Generic ExMy block formats (fig:nvfp-scale,            */
+/* fig:nvfp-val, fig:mxfp P:237-260, "hypothetical block quantization     */
+/* formats having different scale representation bits ... value           */
+/* representation bits" P:301-303).  Reading R21:          */
+/*  value format ExMy (e >= 1): sign bit above e+m magnitude bits, bias    */
+/*    2^(e-1)-1, E = 0 subnormal M * 2^(1-bias-m), else                    */
+/*    (2^m + M) * 2^(E-bias-m); every code finite (the OCP FP4/FP6 rule).   */
+/*  scale format UExMy (unsigned): the all-ones code is NaN (as E4M3 0x7F, */
+/*    E8M0 0xFF).  m >= 1: IEEE-like with subnormals, code 0 = the zero    */
+/*    scale (R3); c0 = nearest code, ties to the even code, satfinite (the */
+/*    UE4M3 rule, Alg. 1 line 2).  m = 0: pure powers of two 2^(c-bias),    */
+/*    no zero; c0 = the smallest power of two >= v (R19, the UE8M0 rule).  */
+/*  x_max -> v = RN(x_max * RN(1/vmax)) (R8); global scale numerator       */
+/*    vmax * smax (2688 for NVFP4, R9).                                     */
+/* Rounding is by enumerating the format's values (no bit tricks).         */
+/* ====================================================================== */
+
+/* magnitude of code c of an ExMy grid; m == 0 && pow2: 2^(c - bias) */
+static double gen_mag(int e, int m, int c, int pow2) {
+  const int bias = (1 << (e - 1)) - 1;
+  if (pow2) return ldexp(1.0, c - bias);
+  const int E = c >> m, M = c & ((1 << m) - 1);
+  if (E == 0) return ldexp((double)M, 1 - bias - m);
+  return ldexp((double)((1 << m) + M), E - bias - m);
+}
+
+static int gen_fmt_ok(int ve, int vm, int se, int sm) {
+  /* values: sign + e + m <= 8 bits; scales: e + m <= 8 bits and every finite
+   * scale, times vmax, inside binary32 */
+  if (ve < 1 || vm < 0 || ve + vm > 7) return 0;
+  if (se < 1 || sm < 0 || se + sm > 8) return 0;
+  if (sm > 0 && se > 7) return 0;
+  return 1;
+}
+
+double so_gen_value(int e, int m, int code) {
+  const int nmag = 1 << (e + m);
+  if (code < 0 || code >= 2 * nmag) return NAN;
+  const double v = gen_mag(e, m, code & (nmag - 1), 0);
+  return (code & nmag) ? -v : v;
+}
+
+/* nearest magnitude to |t| (ties to the even code), saturating at the
+ * largest value; sign bit from t (R10, R11). */
+int so_gen_encode(int e, int m, float t) {
+  const int nmag = 1 << (e + m);
+  const int sign = signbit(t) ? nmag : 0;
+  const double a = fabs((double)t);
+  const double vmax = gen_mag(e, m, nmag - 1, 0);
+  if (a >= vmax) return sign | (nmag - 1); /* satfinite (and +-inf) */
+  int best = 0;
+  double best_d = a;
+  for (int k = 1; k < nmag; k++) {
+    const double d = fabs(a - gen_mag(e, m, k, 0));
+    if (d < best_d || (d == best_d && (k % 2) == 0)) {
+      best = k;
+      best_d = d;
+    }
+  }
+  return sign | best;
+}
+
+double so_gen_scale_value(int e, int m, int code) {
+  const int ncode = 1 << (e + m);
+  if (code < 0 || code >= ncode - 1) return NAN; /* all ones: NaN */
+  return gen_mag(e, m, code, m == 0);
+}
+
+int so_gen_scale_encode(int e, int m, float v) {
+  const int maxc = (1 << (e + m)) - 2;
+  const double a = (double)v;
+  if (m == 0) { /* R19: smallest power of two >= v, saturating */
+    for (int c = 0; c <= maxc; c++)
+      if (gen_mag(e, m, c, 1) >= a) return c;
+    return maxc;
+  }
+  if (a >= gen_mag(e, m, maxc, 0)) return maxc; /* satfinite */
+  int best = 0;
+  double best_d = fabs(a);
+  for (int c = 1; c <= maxc; c++) {
+    const double d = fabs(a - gen_mag(e, m, c, 0));
+    if (d < best_d || (d == best_d && (c % 2) == 0)) {
+      best = c;
+      best_d = d;
+    }
+  }
+  return best;
+}
+
+/* RN(vmax * smax): the global-scale numerator of a format (R9, R21) */
+float so_gen_numer(int ve, int vm, int se, int sm) {
+  const float vmax = (float)gen_mag(ve, vm, (1 << (ve + vm)) - 1, 0);
+  const float smax = (float)gen_mag(se, sm, (1 << (se + sm)) - 2, sm == 0);
+  return vmax * smax;
+}
+
+/* One candidate (Alg. 1 lines 6-9) of a bs-element block in an ExMy value
+ * format: t = RN(y * rho) (R7), q = round(t), d = RN(y - q*s) (q*s exact),
+ * R12 chains per 16-element part, parts added as the R20 pairwise tree. */
+static float gen_candidate_loss(int ve, int vm, int bs, const float* y, float s, float rho,
+                                uint8_t* code) {
+  float part[16];
+  const int np = bs / 16;
+  for (int h = 0; h < np; h++) {
+    float d[16];
+    for (int i = 0; i < 16; i++) {
+      float t = y[16 * h + i] * rho;
+      code[16 * h + i] = (uint8_t)so_gen_encode(ve, vm, t);
+      float q = (float)so_gen_value(ve, vm, code[16 * h + i]);
+      d[i] = fmaf(-q, s, y[16 * h + i]);
+    }
+    float a = d[0] * d[0];
+    for (int i = 2; i < 16; i += 2) a = fmaf(d[i], d[i], a);
+    float b = d[1] * d[1];
+    for (int i = 3; i < 16; i += 2) b = fmaf(d[i], d[i], b);
+    part[h] = a + b;
+  }
+  for (int w = 1; w < np; w *= 2)
+    for (int h = 0; h < np; h += 2 * w) part[h] = part[h] + part[h + w];
+  return part[0];
+}
+
+/* Algorithm 1 for one block of a generic format: scan f
+ * ascending over valid codes (UExMy m >= 1: 1..maxc plus the zero scale at
+ * c0 = 0, f = 0; m = 0: 0..maxc), strict "<" (ties keep the smaller code). */
+int so_search_block_gen(int ve, int vm, int se, int sm, int bs, const float* y, int fmin,
+                        int fmax, so_block_result_fmt* out) {
+  if (fmin > 0 || fmax < 0 || !bs_ok(bs) || !gen_fmt_ok(ve, vm, se, sm)) return 1;
+  const int maxc = (1 << (se + sm)) - 2, cmin = sm == 0 ? 0 : 1;
+  const float vmax = (float)gen_mag(ve, vm, (1 << (ve + vm)) - 1, 0);
+  const float kinv = 1.0f / vmax; /* RN(1/vmax), R8 */
+  float xmax = 0.0f;
+  for (int i = 0; i < bs; i++)
+    if (fabsf(y[i]) > xmax) xmax = fabsf(y[i]);
+  const int c0 = so_gen_scale_encode(se, sm, xmax * kinv);
+  int have = 0, cstar = -1, n_eval = 0;
+  float best = INFINITY, base = NAN;
+  uint8_t code[256], best_code[256] = {0};
+  for (int f = fmin; f <= fmax; f++) {
+    const int c = c0 + f;
+    float s, rho;
+    if (sm > 0 && f == 0 && c0 == 0) {
+      s = 0.0f; /* R3 */
+      rho = 0.0f;
+    } else if (c < cmin || c > maxc) {
+      continue;
+    } else {
+      s = (float)so_gen_scale_value(se, sm, c);
+      rho = 1.0f / s;
+    }
+    const float loss = gen_candidate_loss(ve, vm, bs, y, s, rho, code);
+    n_eval++;
+    if (f == 0) base = loss;
+    if (!have || loss < best) {
+      have = 1;
+      best = loss;
+      cstar = c;
+      memcpy(best_code, code, (size_t)bs);
+    }
+  }
+  out->c0 = c0;
+  out->cstar = cstar;
+  out->fstar = cstar - c0;
+  out->n_evaluated = n_eval;
+  out->err_best = best;
+  out->err_base = base;
+  memcpy(out->code, best_code, (size_t)bs);
+  return 0;
+}
+
+/* Whole tensor in a generic format.  codes [rows][cols], one value code per
+ * byte; scales [rows][cols/bs]; gmode 0 NONE, 1 TENSOR, 2 GIVEN (amax bits),
+ * with G = RN(numer / A), numer = so_gen_numer. */
+int so_quantize_gen(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int fmax,
+                    int gmode, const uint32_t* amax_bits_in, int ve, int vm, int se, int sm,
+                    int bs, uint8_t* codes, uint8_t* scales, int8_t* offsets, float* err,
+                    double* sums, int64_t* n_eval, float* G_out, int threads) {
+  if (rows < 0 || cols < 0 || !bs_ok(bs) || cols % bs != 0 || fmin > 0 || fmax < 0 ||
+      !gen_fmt_ok(ve, vm, se, sm) || gmode < 0 || gmode > 2 || (gmode == 2 && !amax_bits_in))
+    return 1;
+  const int lim = (1 << (se + sm)) - 2;
+  if (fmin < -lim) fmin = -lim;
+  if (fmax > lim) fmax = lim;
+  const float numer = so_gen_numer(ve, vm, se, sm);
+  float G = 1.0f;
+  if (gmode != 0) {
+    uint32_t ab = 0;
+    int st = 0;
+    if (gmode == 1)
+      st = so_tensor_amax(x, rows * cols, &ab);
+    else
+      ab = *amax_bits_in;
+    if (st) return st;
+    const float A = bits_float(ab);
+    if (!(A >= 0.0f && isfinite(A))) return 4;
+    if (A > 0.0f) {
+      G = numer / A;
+      if (!isfinite(G)) return 5;
+    }
+  }
+  if (G_out) *G_out = G;
+  const int64_t nbr = cols / bs, nb = rows * nbr;
+  float* e = (float*)malloc(sizeof(float) * 2 * (nb > 0 ? nb : 1));
+  int32_t* ne = (int32_t*)malloc(sizeof(int32_t) * (nb > 0 ? nb : 1));
+  if (!e || !ne) {
+    free(e);
+    free(ne);
+    return 1;
+  }
+#ifdef _OPENMP
+  if (threads <= 0) threads = omp_get_num_procs();
+#pragma omp parallel for schedule(dynamic, 16) num_threads(threads)
+#endif
+  for (int64_t r = 0; r < rows; r++) {
+    for (int64_t bj = 0; bj < nbr; bj++) {
+      const int64_t blk = r * nbr + bj;
+      float y[256];
+      for (int i = 0; i < bs; i++) {
+        const float xv = bf16_to_float(x[r * cols + bj * bs + i]);
+        y[i] = gmode == 0 ? xv : xv * G;
+      }
+      so_block_result_fmt res;
+      so_search_block_gen(ve, vm, se, sm, bs, y, fmin, fmax, &res);
+      for (int j = 0; j < bs; j++) codes[r * cols + bj * bs + j] = res.code[j];
+      scales[blk] = (uint8_t)res.cstar;
+      if (offsets) offsets[blk] = (int8_t)(res.fstar < -128 ? -128 : (res.fstar > 127 ? 127 : res.fstar));
+      e[2 * blk] = res.err_best;
+      e[2 * blk + 1] = res.err_base;
+      ne[blk] = res.n_evaluated;
+    }
+  }
+  double sb = 0.0, s0 = 0.0;
+  int64_t total = 0;
+  for (int64_t b = 0; b < nb; b++) {
+    sb += (double)e[2 * b];
+    s0 += (double)e[2 * b + 1];
+    total += ne[b];
+  }
+  if (err) memcpy(err, e, sizeof(float) * 2 * nb);
+  if (sums) {
+    sums[0] = sb;
+    sums[1] = s0;
+  }
+  if (n_eval) *n_eval = total;
+  free(e);
+  free(ne);
+  return 0;
+}
+
+/* xhat = RNE_bf16(RN((q * s) / G)) for the code layout of so_quantize_gen. */
+int so_dequantize_gen(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols,
+                      int ve, int vm, int se, int sm, int bs, float G, uint16_t* out) {
+  if (rows < 0 || cols < 0 || !bs_ok(bs) || cols % bs != 0 || !gen_fmt_ok(ve, vm, se, sm) ||
+      !(G > 0.0f))
+    return 1;
+  const int64_t nbr = cols / bs;
+  for (int64_t r = 0; r < rows; r++)
+    for (int64_t k = 0; k < cols; k++) {
+      const float q = (float)so_gen_value(ve, vm, codes[r * cols + k]);
+      const int sc = scales[r * nbr + k / bs];
+      const float s = (sm > 0 && sc == 0) ? 0.0f : (float)so_gen_scale_value(se, sm, sc);
+      out[r * cols + k] = float_to_bf16_rne((q * s) / G);
+    }
+  return 0;
+}

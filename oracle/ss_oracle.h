@@ -91,6 +91,26 @@ int so_quantize_fmt(const uint16_t* x_bf16, int64_t rows, int64_t cols, int fmin
 int so_dequantize_fmt(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols,
                       int vfmt, int sfmt, int bs, const float* G, int per_row, uint16_t* out_bf16);
 
+/* Generic ExMy formats (fig:nvfp-scale / fig:nvfp-val /
+ * fig:mxfp P:237-260; reading R21): value ExMy (e >= 1, sign bit
+ * above the e+m magnitude bits, every code finite), unsigned scale UExMy
+ * (all-ones code NaN; m >= 1 with subnormals and a zero code, c0 by nearest
+ * ties-to-even satfinite; m == 0 pure powers of two, c0 rounded up, R19).
+ * Codes one per byte, scales one per block. */
+double so_gen_value(int e, int m, int code);
+int    so_gen_encode(int e, int m, float t);
+double so_gen_scale_value(int e, int m, int code);   /* NaN for the all-ones code */
+int    so_gen_scale_encode(int e, int m, float v);
+float  so_gen_numer(int ve, int vm, int se, int sm); /* RN(vmax * smax) */
+int so_search_block_gen(int ve, int vm, int se, int sm, int bs, const float* y, int fmin,
+                        int fmax, so_block_result_fmt* out);
+int so_quantize_gen(const uint16_t* x_bf16, int64_t rows, int64_t cols, int fmin, int fmax,
+                    int gmode, const uint32_t* amax_bits_in, int ve, int vm, int se, int sm,
+                    int bs, uint8_t* codes, uint8_t* scales, int8_t* offsets, float* err,
+                    double* sums, int64_t* n_eval, float* G_out, int threads);
+int so_dequantize_gen(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols,
+                      int ve, int vm, int se, int sm, int bs, float G, uint16_t* out_bf16);
+
 /* Dequantization: xhat = RNE_bf16(RN((q * s) / G)). */
 int so_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows,
                   int64_t cols, float G, uint16_t* out_bf16);

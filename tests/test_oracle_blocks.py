@@ -142,3 +142,30 @@ def test_maxabs_scale_for_every_bf16_block_max(oracle_lib):
         y[5] = -m[k] if k % 2 else m[k]
         r = oracle_lib.search_block(y, 0, 0)
         assert r.c0 == ref[k], (m[k], r.c0, ref[k])
+
+
+def test_r7_reciprocal_vs_division(oracle_lib):
+    import oracle
+    """R7 (DESIGN.md §3): t = RN(y * RN(1/s)) (vLLM, P:132-135) is not always the
+    E2M1 value nearest y/s (Alg. 1 writes x_i / s, P:190).  Pins the documented
+    example and bounds how often the two readings pick different values."""
+    s = np.float32(oracle.e4m3_value(38))
+    assert s == np.float32(0.21875)
+    y = np.nextafter(np.float32(1.75) * s, np.float32(0))  # 1 ulp below the 1.75 midpoint
+    t_rcp = np.float32(y * np.float32(np.float32(1) / s))
+    q_rcp = oracle.e2m1_value(int(oracle.e2m1_encode(np.array([t_rcp], np.float32))[0]))
+    q_div = oracle.e2m1_value(int(oracle.e2m1_encode(np.array([np.float32(y / s)], np.float32))[0]))
+    assert (q_rcp, q_div) == (2.0, 1.5)
+    # the nearer value is the division's: |y - 1.5 s| < |y - 2 s|
+    assert abs(float(y) - 1.5 * float(s)) < abs(float(y) - 2.0 * float(s))
+    # random bf16-representable y over every normal scale: differences are rare
+    rng = np.random.default_rng(7)
+    yy = (rng.standard_normal(1 << 16) * 3).astype(np.float32)
+    yy = (yy.view(np.uint32) & 0xFFFF0000).view(np.float32)
+    diff = 0
+    for c in range(8, 127, 3):
+        sc = np.float32(oracle.e4m3_value(c))
+        a = oracle.e2m1_encode((yy * sc * np.float32(np.float32(1) / sc)).astype(np.float32))
+        b = oracle.e2m1_encode(((yy * sc).astype(np.float32) / sc).astype(np.float32))
+        diff += int((a != b).sum())
+    assert diff < 1e-3 * len(yy) * len(range(8, 127, 3))
