@@ -293,6 +293,57 @@ SS_API ss_status ss_quantize_batched_fmt(const ss_tensor_io* tensors, int count,
                                   int f_max, int global_scale_mode, int format, void* stream);
 
 /*
+ * Generic ExMy block formats: the format sweeps of the paper's §4.1
+ * (fig:nvfp-scale: scale formats at E2M1 values; fig:nvfp-val: value formats
+ * at UE4M3 scales; fig:mxfp: value formats at UE8M0 scales; P:237-260,
+ * P:301-303 "hypothetical block quantization formats").  Reading R21
+ * (DESIGN.md §3):
+ *   value format ExMy   1 <= value_e, value_e + value_m <= 7; a sign bit above
+ *                       the magnitude bits; bias 2^(e-1)-1, subnormals at
+ *                       E = 0, every code finite (the OCP FP4/FP6 rule);
+ *                       rounding RNE, saturating, sign kept (R10, R11)
+ *   scale format UExMy  1 <= scale_e, scale_e + scale_m <= 8 (scale_e <= 7
+ *                       when scale_m > 0); the all-ones code is NaN and never
+ *                       used.  scale_m >= 1: subnormals, code 0 is the zero
+ *                       scale (R3), c0 = nearest code ties-to-even satfinite
+ *                       (Alg. 1 line 2); scale_m = 0: powers of two
+ *                       2^(c - bias), c0 = the smallest >= x_max/vmax (R19)
+ *   block               16 or 32 (a 32-block's loss: RN(low + high), R20)
+ * Everything else is the NVFP4 contract: t = RN(y * RN(1/s)) (R7), R12 loss,
+ * ascending strict-< scan (R4), f* = c* - c0, y = RN(x * G) with
+ * G = RN(vmax * smax / A) (SS_GLOBAL_TENSOR / SS_GLOBAL_DEVICE_AMAX) or 1.
+ * UE4M3 / E2M1 / 16 reproduces SS_FMT_NVFP4 bit for bit.
+ */
+typedef struct {
+  int value_e, value_m;         /* value format ExMy                                         */
+  int scale_e, scale_m;         /* scale format UExMy                                        */
+  int block;                    /* 16 or 32                                                  */
+} ss_gen_format;
+
+/*
+ * ScaleSearch over a generic format, one tensor (t->scale_layout must be
+ * linear; t->d_amax_bits is read in SS_GLOBAL_DEVICE_AMAX mode):
+ *   out_codes   DEVICE [rows][cols] u8, ONE value code per byte, 16-B aligned
+ *   out_scales  DEVICE [rows][cols/block] u8 scale codes
+ *   out_err     nullable float2 [nb] {err_best, err_base}; out_offset nullable
+ *               int8 [nb] f* clamped to [-128, 127]; d_err_sums nullable
+ *               double[2]; d_global_scale nullable float (G used)
+ *   f_min, f_max  window, clamped to +-(2^(scale_e+scale_m) - 2)
+ * Errors: SS_ERR_INVALID_ARG for a format outside the ranges above, cols %
+ * block != 0, or an inverted window; SS_ERR_ALIGNMENT as ss_quantize_nvfp4_ex.
+ * A study kernel (software rounding, one thread per block).
+ * Enqueued on `stream`, no host sync.
+ */
+SS_API ss_status ss_quantize_gen(const ss_tensor_io* t, int f_min, int f_max, int global_scale_mode,
+                                 const ss_gen_format* fmt, void* stream);
+
+/* a8 for a generic format: xhat = RNE_bf16(RN((q * s) / G)), codes and scales
+ * as written by ss_quantize_gen; d_global_scale nullable (G = 1). */
+SS_API ss_status ss_dequantize_gen(const uint8_t* codes, const uint8_t* scales, int64_t rows,
+                                   int64_t cols, const ss_gen_format* fmt, const float* d_global_scale,
+                                   void* out_bf16, void* stream);
+
+/*
  * FP32-input ScaleSearch NVFP4 through the one-thread block routine of
  * include/ss_device.cuh (the search a fused producer, e.g. attention's P
  * tile, runs in registers).  One thread per block.

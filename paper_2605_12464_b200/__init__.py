@@ -22,6 +22,8 @@ from ._binding import (  # noqa: F401
     quantize_batched,
     quantize_batched_next_amax,
     quantize_f32,
+    quantize_gen,
+    dequantize_gen,
     quantize_host,
     quantize_host_batched,
     quantize_simple,
@@ -32,7 +34,7 @@ from ._binding import (  # noqa: F401
 )
 
 __all__ = [
-    "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "quantize_batched_next_amax", "quantize_f32",
+    "lib", "tensor_amax", "tensor_amax_batched", "quantize_batched", "quantize_batched_next_amax", "quantize_f32", "quantize_gen", "dequantize_gen",
     "alloc_out", "quantize", "quantize_simple", "dequantize", "quantize_host", "quantize_host_batched",
     "device_status", "scale_bytes", "plan", "SCALE_LAYOUTS", "FORMATS", "status_string", "SSError", "QuantOut", "GMODES",
 ]

@@ -102,6 +102,17 @@ class Plan(ctypes.Structure):
     ]
 
 
+class GenFormat(ctypes.Structure):
+    """ss_gen_format: value ExMy, scale UExMy, block 16 or 32 (R21)."""
+    _fields_ = [
+        ("value_e", ctypes.c_int),
+        ("value_m", ctypes.c_int),
+        ("scale_e", ctypes.c_int),
+        ("scale_m", ctypes.c_int),
+        ("block", ctypes.c_int),
+    ]
+
+
 class DequantArgs(ctypes.Structure):
     _fields_ = [
         ("codes", ctypes.c_void_p),
@@ -163,6 +174,10 @@ def lib():
             L.ss_quantize_nvfp4_host_batched.argtypes = [ctypes.POINTER(HostTensorIO), I, I, I, I]
             L.ss_quantize_plan.restype = I
             L.ss_quantize_plan.argtypes = [ctypes.POINTER(TensorIO), I, I, I, I, I, ctypes.POINTER(Plan)]
+            L.ss_quantize_gen.restype = I
+            L.ss_quantize_gen.argtypes = [ctypes.POINTER(TensorIO), I, I, I, ctypes.POINTER(GenFormat), P]
+            L.ss_dequantize_gen.restype = I
+            L.ss_dequantize_gen.argtypes = [P, P, i64, i64, ctypes.POINTER(GenFormat), P, P, P]
             L.ss_get_device_status.restype = I
             L.ss_get_device_status.argtypes = [ctypes.POINTER(ctypes.c_int), P]
             _lib = L
@@ -422,4 +437,49 @@ def plan(shapes, radius=None, fmin=None, fmax=None, gmode: str = "tensor", fmt: 
                           dummy if gm == 3 else None, SCALE_LAYOUTS[scale_layout])
     out = Plan()
     _check(lib().ss_quantize_plan(arr, n, lo, hi, gm, FORMATS[fmt][0], ctypes.byref(out)), "ss_quantize_plan")
+    return out
+
+
+def quantize_gen(x, fmt, radius=None, fmin=None, fmax=None, gmode: str = "tensor", amax=None,
+                 want_err: bool = True, want_offsets: bool = True, want_sums: bool = True,
+                 want_g: bool = True, stream=None) -> QuantOut:
+    """ScaleSearch over a generic ExMy format ``fmt`` = (value_e, value_m,
+    scale_e, scale_m, block) (ss_quantize_gen).  Codes [rows][cols], one per byte."""
+    import torch
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+    rows, cols = x.shape
+    ve, vm, se, sm, bs = fmt
+    lim = (1 << (se + sm)) - 2
+    if fmin is None and fmax is None:
+        r = 8 if radius is None else int(radius)
+        lo, hi = -min(r, lim), min(r, lim)
+    else:
+        lo, hi = int(fmin), int(fmax)
+    gm = GMODES[gmode]
+    if gm == 2 and amax is None:
+        raise ValueError("gmode='device_amax' needs amax")
+    dev = x.device
+    nb = rows * cols // bs
+    out = QuantOut(torch.empty(rows, cols, dtype=torch.uint8, device=dev),
+                   torch.empty(rows, cols // bs, dtype=torch.uint8, device=dev),
+                   torch.empty(nb, 2, dtype=torch.float32, device=dev) if want_err else None,
+                   torch.empty(nb, dtype=torch.int8, device=dev) if want_offsets else None,
+                   torch.empty(2, dtype=torch.float64, device=dev) if want_sums else None,
+                   torch.empty(1, dtype=torch.float32, device=dev) if want_g else None)
+    t = TensorIO(_ptr(x), rows, cols, _ptr(amax) if gm == 2 else None, _ptr(out.codes), _ptr(out.scales),
+                 _ptr(out.err), _ptr(out.offsets), _ptr(out.sums), _ptr(out.G), 0)
+    f = GenFormat(ve, vm, se, sm, bs)
+    _check(lib().ss_quantize_gen(ctypes.byref(t), lo, hi, gm, ctypes.byref(f), _stream_ptr(stream)),
+           "ss_quantize_gen")
+    return out
+
+
+def dequantize_gen(codes, scales, rows: int, cols: int, fmt, G=None, out=None, stream=None):
+    """bf16 [rows][cols] from ss_quantize_gen outputs (ss_dequantize_gen)."""
+    import torch
+    if out is None:
+        out = torch.empty(rows, cols, dtype=torch.bfloat16, device=codes.device)
+    f = GenFormat(*fmt)
+    _check(lib().ss_dequantize_gen(_ptr(codes), _ptr(scales), rows, cols, ctypes.byref(f), _ptr(G),
+                                   _ptr(out), _stream_ptr(stream)), "ss_dequantize_gen")
     return out

@@ -399,9 +399,22 @@ inline bool row_fused(const ss_tensor_io& t, int gmode, bool wide) {
   return gmode == SS_GLOBAL_ROW && wide && t.rows > 0 && hpr >= ss::kTaskBlocks &&
          hpr <= 8 * ss::kTaskBlocks && SS_ROW_FUSION;
 }
-inline int64_t parts_of(const ss_tensor_io& t, int gmode, bool wide) {
+// Plain tensors: work items per scheduling unit (one ticket and one error-sum
+// partial per unit).  Units of several items amortise the per-unit work
+// (ticket, tensor lookup, the FP64 warp sums) when every warp gets many;
+// -DSS_IPU_MAX (tools-only builds) caps it.
+#ifndef SS_IPU_MAX
+#define SS_IPU_MAX 4
+#endif
+inline int items_per_unit(const ss_tensor_io* io, int count, int sms) {
+  int64_t items = 0;
+  for (int i = 0; i < count; i++) items += tasks_of(io[i].rows * io[i].cols / 16);
+  const int64_t warps = (int64_t)sms * 4 * ss::kWarps;  // ~ the persistent grid's warps
+  return (int)std::max<int64_t>(1, std::min<int64_t>(SS_IPU_MAX, items / (warps * 8)));
+}
+inline int64_t parts_of(const ss_tensor_io& t, int gmode, bool wide, int ipu) {
   const int64_t nb = t.rows * t.cols / 16;
-  if (!row_fused(t, gmode, wide)) return tasks_of(nb);
+  if (!row_fused(t, gmode, wide)) return (tasks_of(nb) + ipu - 1) / ipu;
   return t.rows * ((t.cols / 16 + ss::kTaskBlocks - 1) / ss::kTaskBlocks);
 }
 inline int64_t psegs_of(int64_t parts) { return (parts + ss::kSegTasks - 1) / ss::kSegTasks; }
@@ -578,6 +591,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   }
   const bool af = af_self || af_next;
 
+  const int ipu = items_per_unit(io, count, info.sms);
   // sizes of the largest launch (workspace grown once, before any launch)
   int64_t max_tasks = 0, max_segs = 0;
   bool any_sums = false;
@@ -593,8 +607,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         tk = gr = 0;
         in_batch = 0;
       }
-      tk += parts_of(io[i], gmode, wide);
-      gr += psegs_of(parts_of(io[i], gmode, wide));
+      tk += parts_of(io[i], gmode, wide, ipu);
+      gr += psegs_of(parts_of(io[i], gmode, wide, ipu));
       in_batch++;
       any_sums |= io[i].d_err_sums != nullptr;
     }
@@ -661,6 +675,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.fmax = fmax;
     b.gmode = gmode == SS_GLOBAL_NONE ? 0 : (gmode == SS_GLOBAL_ROW ? 2 : 1);
     b.g_numer = numer;
+    b.ipu = ipu;
     b.part1 = ws->part1;
     b.part2 = ws->part2;
     b.tick = ws->tick;
@@ -685,7 +700,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       }
       const bool rf = row_fused(t, gmode, wide);
       int hpr = 0, cpr = 0, upr = 0, cpu = 0;
-      int64_t units = tasks_of(nb);
+      int64_t units = (tasks_of(nb) + ipu - 1) / ipu;
       if (rf) {
         // units of `cpu` chunks: enough units for ~6 per warp of the grid, so
         // the dynamic schedule balances; each unit re-reads its row from L2
@@ -699,7 +714,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         upr = (cpr + cpu - 1) / cpu;
         units = t.rows * upr;
       }
-      const int64_t parts = parts_of(t, gmode, wide);
+      const int64_t parts = parts_of(t, gmode, wide, ipu);
       // the kernel indexes units, partials and amax units with 32 bits: close the batch before overflow
       const int64_t au = af_self ? amax_units(nb) : 0;
       if (b.n > 0 && (tk + units > (int64_t)INT32_MAX - ss::kCounters || pk + parts > (int64_t)INT32_MAX ||
@@ -823,6 +838,32 @@ struct HostRing {
 std::mutex g_ring_mu;
 std::map<int, HostRing> g_rings;
 
+// ---- generic ExMy block formats ----------------------
+bool gen_fmt(const ss_gen_format* g, ss::GenFmt* f) {
+  if (!g) return false;
+  const int ve = g->value_e, vm = g->value_m, se = g->scale_e, sm = g->scale_m;
+  if (ve < 1 || vm < 0 || ve + vm > 7 || se < 1 || sm < 0 || se + sm > 8 || (sm > 0 && se > 7))
+    return false;
+  if (g->block != 16 && g->block != 32) return false;
+  f->ve = ve;
+  f->vm = vm;
+  f->se = se;
+  f->sm = sm;
+  const int vbias = (1 << (ve - 1)) - 1;
+  f->vemin = 1 - vbias;
+  f->vmax = (float)std::ldexp((double)((2 << vm) - 1), (1 << ve) - 1 - vbias - vm);
+  f->kinv = 1.0f / f->vmax;  // RN(1/vmax), binary32 division (R8)
+  f->sbias = (1 << (se - 1)) - 1;
+  f->semin = 1 - f->sbias;
+  f->smaxc = (1 << (se + sm)) - 2;
+  if (sm == 0) {
+    f->smax = (float)std::ldexp(1.0, f->smaxc - f->sbias);
+  } else {
+    const int E = f->smaxc >> sm, M = f->smaxc & ((1 << sm) - 1);
+    f->smax = (float)std::ldexp((double)((1 << sm) + M), E - f->sbias - sm);
+  }
+  return true;
+}
 }  // namespace
 
 extern "C" {
@@ -1269,6 +1310,108 @@ ss_status ss_quantize_nvfp4_host_batched(const ss_host_tensor_io* t, int count, 
   cudaError_t e2 = cudaStreamSynchronize(R.s_comp);
   cudaError_t e3 = cudaStreamSynchronize(R.s_d2h);
   return (e1 || e2 || e3) ? SS_ERR_CUDA : SS_OK;
+}
+
+// ---- generic ExMy block formats ----------------------
+ss_status ss_quantize_gen(const ss_tensor_io* t, int f_min, int f_max, int global_scale_mode,
+                          const ss_gen_format* fmt, void* stream) {
+  ss::GenFmt f;
+  if (!t || !gen_fmt(fmt, &f)) return SS_ERR_INVALID_ARG;
+  const int bs = fmt->block;
+  if (t->rows < 0 || t->cols < 0 || t->cols % bs != 0 || f_min > 0 || f_max < 0) return SS_ERR_INVALID_ARG;
+  if (global_scale_mode != SS_GLOBAL_NONE && global_scale_mode != SS_GLOBAL_TENSOR &&
+      global_scale_mode != SS_GLOBAL_DEVICE_AMAX)
+    return SS_ERR_INVALID_ARG;
+  const int64_t nb = t->rows * t->cols / bs;
+  if (nb > 0 && (!t->in_bf16 || !t->out_codes || !t->out_scales)) return SS_ERR_INVALID_ARG;
+  if (global_scale_mode == SS_GLOBAL_DEVICE_AMAX && !t->d_amax_bits) return SS_ERR_INVALID_ARG;
+  if (!aligned(t->in_bf16, 16) || !aligned(t->out_codes, 16) || !aligned(t->out_err, 8) ||
+      !aligned(t->d_err_sums, 8) || !aligned(t->d_amax_bits, 4) || !aligned(t->d_global_scale, 4))
+    return SS_ERR_ALIGNMENT;
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (nb == 0) {
+    if (t->d_err_sums && cudaMemsetAsync(t->d_err_sums, 0, 16, cs) != cudaSuccess) return SS_ERR_CUDA;
+    return SS_OK;
+  }
+  Workspace* ws = nullptr;
+  if (ss_status s = get_ws(dev, stream, &ws)) return s;
+  std::lock_guard<std::mutex> wlk(ws->mu);
+  const int64_t chunks = (nb + 255) / 256;
+  if (t->d_err_sums) {
+    if (ss_status s = grow_dev(&ws->part1, &ws->part1_cap, chunks, false, cs)) return s;
+    if (ss_status s = grow_dev(&ws->part2, &ws->part2_cap, (chunks + ss::kSegTasks - 1) / ss::kSegTasks,
+                               false, cs))
+      return s;
+  }
+  const uint32_t* amax = nullptr;
+  if (global_scale_mode == SS_GLOBAL_TENSOR) {
+    if (ss_status s = grow_dev(&ws->amax, &ws->amax_cap, 1, false, cs)) return s;
+    const void* in = t->in_bf16;
+    const int64_t n = t->rows * t->cols;
+    if (ss_status s = amax_launch(&in, &n, ws->amax, 1, false, cs, info.sms)) return s;
+    amax = ws->amax;
+  } else if (global_scale_mode == SS_GLOBAL_DEVICE_AMAX) {
+    amax = t->d_amax_bits;
+  }
+  ss::GenParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.in = reinterpret_cast<const uint4*>(t->in_bf16);
+  p.nb = nb;
+  p.fmin = std::max(f_min, -f.smaxc);
+  p.fmax = std::min(f_max, f.smaxc);
+  p.gmode = amax ? 1 : 0;
+  p.amax = amax;
+  p.g_numer = f.vmax * f.smax;  // exact: both have few significant bits
+  p.codes = reinterpret_cast<uint4*>(t->out_codes);
+  p.scales = t->out_scales;
+  p.err = reinterpret_cast<float2*>(t->out_err);
+  p.offsets = t->out_offset;
+  p.g_out = t->d_global_scale;
+  p.part1 = t->d_err_sums ? ws->part1 : nullptr;
+  p.flags = ws->flags;
+  p.f = f;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)info.sms * 8));
+  ss_status st = bs == 16 ? launch_pdl(ss::quant_gen_kernel<16>, grid, 256, cs, p)
+                          : launch_pdl(ss::quant_gen_kernel<32>, grid, 256, cs, p);
+  if (st) return st;
+  if (t->d_err_sums) {  // reduce the per-chunk partials (fixed order) into the tensor's sums
+    QuantBatch b;
+    std::memset(&b, 0, sizeof(b));
+    b.n = 1;
+    b.part1 = ws->part1;
+    b.part2 = ws->part2;
+    b.tick = ws->tick;
+    b.t[0].sums = t->d_err_sums;
+    b.t[0].part0 = 0;
+    b.t[0].npart = (int32_t)chunks;
+    b.t[0].seg0 = 0;
+    b.nsegs = (chunks + ss::kSegTasks - 1) / ss::kSegTasks;
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(b.nsegs, sums_grid(info.sms)));
+    if (ss_status s = launch_pdl(ss::sums_kernel, g2, ss::kThreads, cs, b)) return s;
+  }
+  return SS_OK;
+}
+
+ss_status ss_dequantize_gen(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols,
+                            const ss_gen_format* fmt, const float* d_global_scale, void* out_bf16,
+                            void* stream) {
+  ss::GenFmt f;
+  if (!gen_fmt(fmt, &f)) return SS_ERR_INVALID_ARG;
+  if (rows < 0 || cols < 0 || cols % fmt->block != 0) return SS_ERR_INVALID_ARG;
+  const int64_t n = rows * cols;
+  if (n > 0 && (!codes || !scales || !out_bf16)) return SS_ERR_INVALID_ARG;
+  if (!aligned(out_bf16, 2) || !aligned(d_global_scale, 4)) return SS_ERR_ALIGNMENT;
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  if (n == 0) return SS_OK;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)info.sms * 8));
+  ss::dequant_gen_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      codes, scales, n, fmt->block, d_global_scale, f, reinterpret_cast<__nv_bfloat16*>(out_bf16));
+  return launch_status();
 }
 
 #ifdef SS_COUNT_EVALS

@@ -44,3 +44,4 @@
 #include "ss_quant_kernel.cuh"
 #include "ss_aux_kernels.cuh"
 #include "ss_block.cuh"
+#include "ss_gen_kernel.cuh"

@@ -63,28 +63,26 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 
   const float kinv = __uint_as_float(F::kInvVmaxBits);  // RN(1 / vmax) (R8)
   // A work item is up to kTaskBlocks half-blocks of one tensor, named by its
-  // error-sum partial index (global over the batch).  Plain tensor: item
-  // part0 + k covers half-blocks [64k, 64k + 64).  Row-fused tensor (T.hpr >
-  // 0): item part0 + r * cpr + c is chunk c of row r; its G_r rides along in
-  // shared memory (q_g).
+  // tensor and local index li.  Plain tensor: item li covers half-blocks
+  // [64 li, 64 li + 64); its items are handed out in scheduling units of
+  // p.ipu consecutive items (one ticket and one error-sum partial per unit).
+  // Row-fused tensor (T.hpr > 0): item li = r * cpr + c is chunk c of row r,
+  // one partial per chunk; its G_r rides along in shared memory (q_g).
   struct Item {
     int b0;  // < 2^31 half-blocks per tensor (validate_io)
     int nblk;
     uint32_t row;
   };
-  // first item of a tensor (part0; equal to task0 unless the launch has row-fused tensors)
-  auto first_item = [&](const QTensor& T) -> int { return RI == 2 ? (int)T.part0 : (int)T.task0; };
-  auto item_of = [&](const QTensor& T, int it) -> Item {
-    const int local = it - first_item(T);
+  auto item_of = [&](const QTensor& T, int li) -> Item {
     Item x;
     if (RI == 2 && T.hpr) {
-      x.row = (uint32_t)(local / T.cpr);
-      const int c = local - (int)x.row * T.cpr;
+      x.row = (uint32_t)(li / T.cpr);
+      const int c = li - (int)x.row * T.cpr;
       x.b0 = (int)x.row * T.hpr + c * kTaskBlocks;
       x.nblk = min(kTaskBlocks, T.hpr - c * kTaskBlocks);
     } else {
       x.row = 0;
-      x.b0 = local * kTaskBlocks;
+      x.b0 = li * kTaskBlocks;
       x.nblk = (int)min((int64_t)kTaskBlocks, T.nb - x.b0);
     }
     return x;
@@ -93,9 +91,9 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   // l, l+32, ... (2 x 16-B LDGSTS each) and later reads back only what it
   // copied, so no cross-lane sync is needed; one commit group per stage
   // (empty groups past the end keep the group count uniform).
-  auto issue = [&](int it, int ti, int s) {
+  auto issue = [&](int li, int ti, int s) {
     const QTensor& T = p.t[ti];
-    const Item x = item_of(T, it);
+    const Item x = item_of(T, li);
     const uint8_t* src = T.in + (int64_t)x.b0 * 32;
 #pragma unroll
     for (int u = 0; u < kBPL; u++) {
@@ -112,16 +110,21 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   };
   // Dynamic scheduling: counter c hands out units c, c + kCounters, ... ; warp
   // gw draws from counter gw % kCounters, so warps the arbiter favours simply
-  // take more units and every warp finishes at about the same time.  A unit is
-  // one item (plain tensor) or, for a row-fused tensor, `cpu` consecutive
-  // chunks of one row, whose global scale the warp first computes from the
-  // whole row (one coalesced pass; the chunks' own reads then hit L2).  Each
-  // warp's units increase, so the tensor lookup only moves forward.  Unit and
-  // item indices are 32-bit (the host splits batches before 2^31).
+  // take more units and every warp finishes at about the same time.  Lane 0
+  // draws each ticket one unit ahead (`pend`), so the atomic's latency hides
+  // under the current unit.  A plain unit is p.ipu items; a row-fused unit is
+  // `cpu` consecutive chunks of one row, whose global scale the warp first
+  // computes from the whole row (one coalesced pass; the chunks' own reads
+  // then hit L2).  Each warp's units increase, so the tensor lookup only
+  // moves forward.  Unit and item indices are 32-bit (the host splits
+  // batches before 2^31).
   const int cidx = gw % kCounters;
   bool exhausted = false;
   const int nunits = (int)p.ntasks;
   int tj = 0;
+  int un_li = 0, un_end = 0, un_pt = 0;  // current plain unit: items [un_li, un_end), its partial
+  uint32_t pend = 0;
+  if (lane == 0) pend = atomicAdd(p.ctr + cidx, 1u);
   // RI == 2 kernels: the current row-fused unit (chunks [c, ce) of row `row`, scale
   // g still to hand out) lives in shared memory, off the register budget
   struct RowUnit {
@@ -135,9 +138,9 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     if (lane == 0) ru[w] = RowUnit{0, 0, 0u, 1.0f};
     __syncwarp();
   }
-  // next item (its partial index; its tensor in tj), -1 when exhausted.  In a
-  // launch without row-fused tensors (RI < 2) part0 == task0: item == unit.
-  auto grab = [&](int s) -> int {
+  // next item: its local index (-1 when exhausted), tensor (gti) and the
+  // partial to flush after it (gpt, -1 if the unit continues)
+  auto grab = [&](int s, int& gti, int& gpt) -> int {
     if constexpr (RI == 2) {
       __syncwarp();
       const RowUnit cur = ru[w];
@@ -148,22 +151,31 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
           ru[w].c = cur.c + 1;
           q_g[w][s] = cur.g;
         }
-        return (int)(T.part0 + (int64_t)cur.row * T.cpr + cur.c);
+        const int li = (int)cur.row * T.cpr + cur.c;
+        gti = tj;
+        gpt = T.part0 + li;
+        return li;
       }
     }
+    if (un_li < un_end) {  // next item of the current plain unit
+      gti = tj;
+      const int li = un_li++;
+      gpt = un_li == un_end ? un_pt : -1;
+      return li;
+    }
     if (exhausted) return -1;
-    uint32_t idx = 0;
-    if (lane == 0) idx = atomicAdd(p.ctr + cidx, 1u);
-    idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
+    const uint32_t idx = __shfl_sync(0xFFFFFFFFu, pend, 0);
     const int64_t u = cidx + (int64_t)idx * kCounters;
     if (u >= nunits) {
       exhausted = true;
       return -1;
     }
+    if (lane == 0) pend = atomicAdd(p.ctr + cidx, 1u);  // the ticket after this one
+    tj = locate_task(p, u, tj);
+    const QTensor& T = p.t[tj];
+    const int k = (int)(u - T.task0);
+    gti = tj;
     if constexpr (RI == 2) {
-      tj = locate_task(p, u, tj);
-      const QTensor& T = p.t[tj];
-      const int k = (int)(u - T.task0);
       if (T.hpr) {  // row-fused unit: row k / upr, chunk group k % upr
         const uint32_t row = (uint32_t)(k / T.upr);
         const int c = (k - (int)row * T.upr) * T.cpu;
@@ -174,25 +186,30 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
           ru[w] = RowUnit{c + 1, min(c + T.cpu, T.cpr), row, g};
           q_g[w][s] = g;
         }
-        return (int)(T.part0 + (int64_t)row * T.cpr + c);
+        const int li = (int)row * T.cpr + c;
+        gpt = T.part0 + li;
+        return li;
       }
-      return (int)T.part0 + k;
     }
-    return (int)u;  // the caller locates its tensor
+    const int items = (int)((T.nb + kTaskBlocks - 1) / kTaskBlocks);
+    const int li = k * p.ipu;
+    un_end = min(li + p.ipu, items);
+    un_li = li + 1;
+    un_pt = T.part0 + k;
+    gpt = un_li == un_end ? un_pt : -1;
+    return li;
   };
 
   // prologue: kStages items in flight
-  int q_it[kStages];
-  int q_ti[kStages];
+  int q_li[kStages], q_ti[kStages], q_pt[kStages];
 #pragma unroll
   for (int k = 0; k < kStages; k++) {
-    const int t = grab(k);
-    if (t >= 0) {
-      if (RI != 2) tj = locate_task(p, t, tj);
-      issue(t, tj, k);
-    }
-    q_it[k] = t;
-    q_ti[k] = tj;
+    int gti = tj, gpt = -1;
+    const int li = grab(k, gti, gpt);
+    if (li >= 0) issue(li, gti, k);
+    q_li[k] = li;
+    q_ti[k] = gti;
+    q_pt[k] = gpt;
     cp_async_commit();
   }
   int s = 0;
@@ -202,18 +219,20 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   // global scale of the current item's tensor, recomputed when the tensor changes
   int cur_ti = -1;
   float G = 1.0f;
-  while (q_it[0] >= 0) {
-    const int it = q_it[0];
+  double sb = 0.0, sc = 0.0;  // this lane's error sums over the current unit
+  while (q_li[0] >= 0) {
+    const int li = q_li[0];
     const int ti = q_ti[0];
+    const int pt = q_pt[0];
     const QTensor& T = p.t[ti];
-    const Item x = item_of(T, it);
+    const Item x = item_of(T, li);
     const int b0 = x.b0;  // first half-block of the item
     const int nblk = x.nblk;
     if (RI == 2 && T.hpr) {  // row-fused: this item's G_r (the next plain item reloads G)
       __syncwarp();
       G = q_g[w][s];
       cur_ti = -1;
-    } else if (ti != cur_ti) {  // warp-uniform
+    } else if (ti != cur_ti) {  // warp-uniform; a tensor's item 0 always lands here
       cur_ti = ti;
       if constexpr (AF) {  // wait until every amax unit of the tensor has been folded in
 #ifdef SS_AF_TRACE
@@ -230,16 +249,16 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 #ifdef SS_AF_TRACE
         if (lane == 0) atomicAdd(p.evals + 2, gtime() - t0);
 #endif
-        G = global_scale(ld_relaxed_gpu(T.amax), p.flags, it == first_item(T) && lane == 0, p.g_numer);
+        G = global_scale(ld_relaxed_gpu(T.amax), p.flags, li == 0 && lane == 0, p.g_numer);
       } else {
-        G = gscale(ti, it == first_item(T) && lane == 0);
+        G = gscale(ti, li == 0 && lane == 0);
       }
+      if (li == 0 && lane == 0 && T.g_out && p.gmode != 2) *T.g_out = G;
     }
 
     cp_async_wait<kStages - 1>();  // this lane's copies of stage s have landed
     int8_t* offsets = T.offsets ? T.offsets + b0 / kHalves : nullptr;
     float2* err = T.err ? T.err + b0 / kHalves : nullptr;
-    double sb = 0.0, sc = 0.0;
     const uint64_t GG = pack2(G, G);
 
 #pragma unroll 1
@@ -278,9 +297,10 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       const int c0 = F::SF ? (int)ue8m0_code(v) : (int)e4m3_code(v);
       const uint4* base = F::SF ? tab + Pad + c0 : tab + (c0 ? TabW : 0) + Pad + c0;
 
-      // a5 + a6: candidate search (Alg. 1 lines 5-10)
+      // a5 + a6: candidate search (Alg. 1 lines 5-10).  bidx = the winner's
+      // offset into base (its table entry gives code and rho at emit time).
       float best, loss0;
-      uint32_t bsel;
+      int bidx;
       if constexpr (NEG >= 0) {
         // f = 0, 1, ..., POS in chunks of CI interleaved candidates (the
         // selection updates applied in scan order), then the negative side
@@ -306,11 +326,11 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
             if (i == 0) {
               best = l[c];
               loss0 = l[c];  // err_base: the max-abs scale (f = 0)
-              bsel = e[c].z;
+              bidx = 0;
             } else {
               const bool t_ = l[c] < best;
               best = t_ ? l[c] : best;
-              bsel = t_ ? e[c].z : bsel;
+              bidx = t_ ? i : bidx;
             }
           }
         }
@@ -326,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         best = block_loss<FMT>(y2, y, base[0]);
         SS_COUNT(1);
         loss0 = best;  // err_base: the max-abs scale (f = 0)
-        bsel = base[0].z;
+        bidx = 0;
         // runtime window; skip offsets that are clamped duplicates for every lane
         const int lo = __reduce_min_sync(0xFFFFFFFFu, F::SF ? -c0 : (c0 ? 1 : 0) - c0);
         const int hi = __reduce_max_sync(0xFFFFFFFFu, F::kMaxCode - c0);
@@ -344,10 +364,9 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       }
 
       // a7: emit the winner: codes of t = y * rho*, scale byte, offset, errors
-      const uint32_t code = bsel >> 16;
-      const float rs = __uint_as_float(
-          (F::SF ? tab[Pad + code] : tab[(code ? TabW : 0) + Pad + code]).x);
-      const uint64_t rr = pack2(rs, rs);
+      const uint4 eb = base[bidx];
+      const uint32_t code = eb.z >> 16;
+      const uint64_t rr = pack2u(eb.x, eb.x);
       float t[16];
 #pragma unroll
       for (int k = 0; k < 8; k++) unpack2(fmul2(y2[k], rr), t[2 * k], t[2 * k + 1]);
@@ -380,26 +399,29 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       }
     }
     {  // refill stage s with the next item drawn (always commit: uniform group count)
-      const int t = grab(s);
-      if (t >= 0) {
-        if (RI != 2) tj = locate_task(p, t, tj);
-        issue(t, tj, s);
-      }
+      int gti = tj, gpt = -1;
+      const int nl = grab(s, gti, gpt);
+      if (nl >= 0) issue(nl, gti, s);
       cp_async_commit();
 #pragma unroll
       for (int k = 0; k + 1 < kStages; k++) {
-        q_it[k] = q_it[k + 1];
+        q_li[k] = q_li[k + 1];
         q_ti[k] = q_ti[k + 1];
+        q_pt[k] = q_pt[k + 1];
       }
-      q_it[kStages - 1] = t;
-      q_ti[kStages - 1] = tj;
+      q_li[kStages - 1] = nl;
+      q_ti[kStages - 1] = gti;
+      q_pt[kStages - 1] = gpt;
     }
-    if (T.sums) {  // per-item partial (fixed lane tree); reduced by sums_kernel
-      sb = warp_sum(sb);
-      sc = warp_sum(sc);
-      if (lane == 0) p.part1[it] = make_double2(sb, sc);
+    if (pt >= 0) {  // the unit's last item: its partial (fixed lane tree); reduced by sums_kernel
+      if (T.sums) {
+        sb = warp_sum(sb);
+        sc = warp_sum(sc);
+        if (lane == 0) p.part1[pt] = make_double2(sb, sc);
+      }
+      sb = 0.0;
+      sc = 0.0;
     }
-    if (T.g_out && b0 == 0 && lane == 0 && p.gmode != 2) *T.g_out = G;
 
     s = s + 1 == kStages ? 0 : s + 1;
   }

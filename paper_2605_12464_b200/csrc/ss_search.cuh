@@ -135,7 +135,8 @@ struct QuantBatch {
   int fmin, fmax;           // window (runtime loop variant only)
   int gmode;                // 0: G = 1; 1: G from t[i].amax; 2: per-row G from t[i].g_row
   float g_numer;            // vmax * 448 (2688 for E2M1, 3360 for E2M3 values)
-  int64_t ntasks;           // total tasks of the batch
+  int64_t ntasks;           // total scheduling units of the batch
+  int32_t ipu;              // plain tensors: work items per scheduling unit (and per error-sum partial)
   int64_t nsegs;            // total error-sum segments of the batch
   double2* part1;           // per task {sum best, sum base}   (when any sums wanted)
   double2* part2;           // per segment
@@ -351,7 +352,7 @@ __device__ __forceinline__ float cand_lb(float m, const uint4 e, bool& sat) {
       const float l_ = block_loss<FMT>(y2, y, e_);                       \
       const bool t_ = l_ <= best;                                        \
       best = t_ ? l_ : best;                                             \
-      bsel = t_ ? e_.z : bsel;                                           \
+      bidx = t_ ? (F) : bidx;                                            \
     }                                                                    \
   }
 #else
@@ -366,7 +367,7 @@ __device__ __forceinline__ float cand_lb(float m, const uint4 e, bool& sat) {
     const float l_ = block_loss<FMT>(y2, y, e_);             \
     const bool t_ = l_ CMP best;                             \
     best = t_ ? l_ : best;                                   \
-    bsel = t_ ? e_.z : bsel;                                 \
+    bidx = t_ ? (F) : bidx;                                  \
   }
 
 // NEG/POS >= 0: compile-time window [-NEG, POS]; NEG < 0: runtime [fmin, fmax].
