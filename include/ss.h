@@ -330,7 +330,8 @@ typedef struct {
  *               double[2]; d_global_scale nullable float (G used)
  *   f_min, f_max  window, clamped to +-(2^(scale_e+scale_m) - 2)
  * Errors: SS_ERR_INVALID_ARG for a format outside the ranges above, cols %
- * block != 0, or an inverted window; SS_ERR_ALIGNMENT as ss_quantize_nvfp4_ex.
+ * block != 0, an inverted window, or a global-scale mode whose numerator
+ * vmax * smax is not finite in binary32 (UE8M0 scales: use SS_GLOBAL_NONE); SS_ERR_ALIGNMENT as ss_quantize_nvfp4_ex.
  * A study kernel (software rounding, one thread per block).
  * Enqueued on `stream`, no host sync.
  */

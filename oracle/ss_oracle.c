@@ -828,6 +828,7 @@ int so_quantize_gen(const uint16_t* x, int64_t rows, int64_t cols, int fmin, int
   if (fmin < -lim) fmin = -lim;
   if (fmax > lim) fmax = lim;
   const float numer = so_gen_numer(ve, vm, se, sm);
+  if (gmode != 0 && !isfinite(numer)) return 1; /* vmax * smax beyond binary32 (e.g. UE8M0) */
   float G = 1.0f;
   if (gmode != 0) {
     uint32_t ab = 0;

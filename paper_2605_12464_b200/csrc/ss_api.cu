@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -1325,6 +1326,8 @@ ss_status ss_quantize_gen(const ss_tensor_io* t, int f_min, int f_max, int globa
   const int64_t nb = t->rows * t->cols / bs;
   if (nb > 0 && (!t->in_bf16 || !t->out_codes || !t->out_scales)) return SS_ERR_INVALID_ARG;
   if (global_scale_mode == SS_GLOBAL_DEVICE_AMAX && !t->d_amax_bits) return SS_ERR_INVALID_ARG;
+  // a global scale needs a finite numerator vmax * smax (not UE8M0, whose range needs none)
+  if (global_scale_mode != SS_GLOBAL_NONE && !std::isfinite(f.vmax * f.smax)) return SS_ERR_INVALID_ARG;
   if (!aligned(t->in_bf16, 16) || !aligned(t->out_codes, 16) || !aligned(t->out_err, 8) ||
       !aligned(t->d_err_sums, 8) || !aligned(t->d_amax_bits, 4) || !aligned(t->d_global_scale, 4))
     return SS_ERR_ALIGNMENT;

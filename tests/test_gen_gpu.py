@@ -57,7 +57,8 @@ def test_gen_parity(ss, oracle_lib, fmt):
             continue
         x = _data(shape, 41)
         xc = x.cuda()
-        for gmode in ("tensor", "none"):
+        gmodes = ("none",) if not np.isfinite(oracle_lib.gen_numer(*fmt[:4])) else ("tensor", "none")
+        for gmode in gmodes:
             for w in [(0, 0), (-1, 1), (-3, 5), (-8, 8), (-lim, lim)]:
                 g = ss.quantize_gen(xc, fmt, fmin=w[0], fmax=w[1], gmode=gmode)
                 torch.cuda.synchronize()
@@ -108,3 +109,13 @@ def test_gen_sampled_large(ss, oracle_lib):
     torch.cuda.synchronize()
     ref = oracle_lib.quantize_gen(x, 64, 8192, -16, 16, fmt, "tensor")
     _cmp(g, ref)
+
+
+def test_gen_argument_errors(ss):
+    """Synchronous argument checks (no launch): bad formats, a global scale for UE8M0."""
+    x = torch.zeros(16, 64, dtype=torch.bfloat16, device="cuda")
+    for fmt in ((0, 3, 4, 3, 16), (2, 6, 4, 3, 16), (2, 1, 8, 1, 16), (2, 1, 4, 3, 48), (2, 1, 9, 0, 16)):
+        with pytest.raises(ss.SSError):
+            ss.quantize_gen(x, fmt, radius=2, gmode="none")
+    with pytest.raises(ss.SSError):
+        ss.quantize_gen(x, (2, 1, 8, 0, 32), radius=2, gmode="tensor")

@@ -38,6 +38,9 @@ VARIANTS = {
     "rowupr2": ["SS_ROW_UPR=2"],
     "rowupr4": ["SS_ROW_UPR=4"],
     "nosmall": ["SS_SMALL_MAX_BLOCKS=0"],
+    "ipu1": ["SS_IPU_MAX=1"],
+    "ipu2": ["SS_IPU_MAX=2"],
+    "ipu8": ["SS_IPU_MAX=8"],
 }
 WINDOWS = [(0, 0), (-1, 1), (-2, 2), (-4, 4), (-2, 6), (-8, 8), (-16, 16), (-126, 126)]
 
