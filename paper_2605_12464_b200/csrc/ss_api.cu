@@ -109,7 +109,7 @@ ss_status get_ws(int dev, void* stream, Workspace** out) {
   Workspace& w = g_ws[std::make_pair(dev, stream)];
   if (!w.flags) {
     void* p = nullptr;
-    const size_t bytes = sizeof(uint32_t) * (1 + ss::kMaxTensors + ss::kCounters + 1 + ss::kMaxTensors + 1);
+    const size_t bytes = sizeof(uint32_t) * (1 + ss::kMaxTensors + ss::kCounters + 1 + ss::kMaxTensors + 2);
     if (cudaMalloc(&p, bytes) != cudaSuccess) return SS_ERR_CUDA;
     if (cudaMemset(p, 0, bytes) != cudaSuccess) return SS_ERR_CUDA;
     w.flags = reinterpret_cast<uint32_t*>(p);
@@ -296,6 +296,25 @@ int sums_grid(int sms) {
   return sms * occ;
 }
 
+// The kernels index a tensor's 16-element half-blocks with 32 bits.  Larger
+// tensors run as row pieces of at most kPieceMax half-blocks (quantize_core);
+// -DSS_MAX_PIECE_BLOCKS (tools / test builds) shrinks the limit so the piece
+// path can be checked against the oracle at small sizes.
+#ifndef SS_MAX_PIECE_BLOCKS
+#define SS_MAX_PIECE_BLOCKS ((1LL << 31) - (1LL << 16))
+#endif
+constexpr int64_t kPieceMax = SS_MAX_PIECE_BLOCKS;
+
+// Rows per piece of a tensor (0: the tensor cannot be split this way).
+int64_t piece_rows(const ss_tensor_io& t) {
+  const int64_t hpr = t.cols / 16;
+  if (hpr <= 0) return t.rows;
+  if (t.rows * hpr <= kPieceMax) return t.rows;
+  int64_t r = kPieceMax / hpr;
+  if (t.scale_layout == SS_SCALE_SWIZZLED) r -= r % 128;  // pieces start on a 128-row tile band
+  return r;
+}
+
 ss_status validate_io(const ss_tensor_io& t, int gmode, const FmtInfo& f) {
   if (t.rows < 0 || t.cols < 0 || (t.cols % f.bs) != 0) return SS_ERR_INVALID_ARG;
   const int64_t nb = t.rows * t.cols / 16;
@@ -304,7 +323,7 @@ ss_status validate_io(const ss_tensor_io& t, int gmode, const FmtInfo& f) {
   if (gmode == SS_GLOBAL_ROW && nb > 0 && !t.d_global_scale) return SS_ERR_INVALID_ARG;
   if (t.scale_layout != SS_SCALE_LINEAR && t.scale_layout != SS_SCALE_SWIZZLED)
     return SS_ERR_INVALID_ARG;
-  if (nb >= ((int64_t)1 << 31)) return SS_ERR_INVALID_ARG;  // 32-bit block index per tensor
+  if (nb > 0 && piece_rows(t) <= 0) return SS_ERR_INVALID_ARG;  // a row (or 128-row band) over the piece limit
   // E2M1 codes are stored as one 8-B word per 16-element part, E2M3 codes
   // (one byte each) as one 16-B vector
   if (!aligned(t.in_bf16, 16) || !aligned(t.out_codes, f.vf ? 16 : 8) || !aligned(t.out_err, 8) ||
@@ -577,8 +596,48 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   if (ss_status s = get_ws(dev, stream, &ws)) return s;
   std::lock_guard<std::mutex> wlk(ws->mu);
 
+  // Row pieces of tensors over the 32-bit half-block index (kPieceMax): each
+  // piece is a tensor of its own for the launches, with its tensor's amax
+  // slot, G output and window; the first piece also reduces every later
+  // piece's error-sum partials (prole 1), the others only write theirs
+  // (prole 2).  All pieces of a tensor go into one launch.
+  const ss_tensor_io* io0 = io;
+  const int count0 = count;
+  std::vector<ss_tensor_io> pio;
+  std::vector<int> psrc, prole, pnum;
+  bool split = false;
+  for (int i = 0; i < count0; i++) split |= io0[i].rows * io0[i].cols / 16 > kPieceMax;
+  if (split) {
+    for (int i = 0; i < count0; i++) {
+      const ss_tensor_io& t = io0[i];
+      const int64_t pr = piece_rows(t);
+      const int np = t.rows * t.cols / 16 > kPieceMax ? (int)((t.rows + pr - 1) / pr) : 1;
+      const int64_t nbr = t.cols / fi.bs;
+      for (int k = 0; k < np; k++) {
+        ss_tensor_io q = t;
+        const int64_t r0 = k * pr;
+        q.rows = std::min(pr, t.rows - r0);
+        if (np > 1) {
+          q.in_bf16 = static_cast<const uint8_t*>(t.in_bf16) + r0 * t.cols * 2;
+          q.out_codes = t.out_codes + r0 * t.cols / (fi.vf ? 1 : 2);
+          q.out_scales = t.out_scales + (t.scale_layout == SS_SCALE_SWIZZLED
+                                             ? (r0 / 128) * ((nbr + 3) / 4) * 512 : r0 * nbr);
+          if (t.out_err) q.out_err = t.out_err + 2 * r0 * nbr;
+          if (t.out_offset) q.out_offset = t.out_offset + r0 * nbr;
+          if (gmode == SS_GLOBAL_ROW && t.d_global_scale) q.d_global_scale = t.d_global_scale + r0;
+        }
+        pio.push_back(q);
+        psrc.push_back(i);
+        prole.push_back(np == 1 ? 0 : (k == 0 ? 1 : 2));
+        pnum.push_back(k == 0 ? np : 0);
+      }
+    }
+    io = pio.data();
+    count = (int)pio.size();
+  }
+
   const Plan pl = make_plan(io, count, fmin, fmax, gmode, format, next);
-  const bool wide = pl.wide, af_self = pl.af_self, af_next = pl.af_next;
+  const bool wide = pl.wide, af_self = pl.af_self && !split, af_next = pl.af_next && !split;
   const int ri = pl.ri;
   if (next && next->count > 0) {
     if (af_next) {
@@ -602,7 +661,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     for (int i = 0; i < count; i++) {
       const int64_t nb = io[i].rows * io[i].cols / 16;
       if (nb == 0) continue;
-      if (in_batch == ss::kMaxTensors) {
+      if (in_batch == ss::kMaxTensors && !split) {  // split: launches keep pieces together, size for all
         max_tasks = std::max(max_tasks, tk);
         max_segs = std::max(max_segs, gr);
         tk = gr = 0;
@@ -624,17 +683,17 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   // SS_GLOBAL_TENSOR: the amax pass of every tensor first (a2)
   std::vector<const uint32_t*> amax(count, nullptr);
   if (gmode == SS_GLOBAL_TENSOR) {
-    if (ss_status s = grow_dev(&ws->amax, &ws->amax_cap, count, false, cs)) return s;
-    std::vector<const void*> ins(count);
-    std::vector<int64_t> ns(count);
-    for (int i = 0; i < count; i++) {
-      ins[i] = io[i].in_bf16;
-      ns[i] = io[i].rows * io[i].cols;
-      amax[i] = ws->amax + i;
+    if (ss_status s = grow_dev(&ws->amax, &ws->amax_cap, std::max(count, count0), false, cs)) return s;
+    std::vector<const void*> ins(count0);
+    std::vector<int64_t> ns(count0);
+    for (int i = 0; i < count0; i++) {  // the whole tensors (a piece uses its tensor's slot)
+      ins[i] = io0[i].in_bf16;
+      ns[i] = io0[i].rows * io0[i].cols;
     }
+    for (int i = 0; i < count; i++) amax[i] = ws->amax + (split ? psrc[i] : i);
     if (af) {  // the quantize launches fold their amax units into zeroed slots
       if (cudaMemsetAsync(ws->amax, 0, 4 * (size_t)count, cs) != cudaSuccess) return SS_ERR_CUDA;
-    } else if (ss_status s = amax_launch(ins.data(), ns.data(), ws->amax, count, false, cs, info.sms)) {
+    } else if (ss_status s = amax_launch(ins.data(), ns.data(), ws->amax, count0, false, cs, info.sms)) {
       return s;
     }
   } else if (gmode == SS_GLOBAL_DEVICE_AMAX) {
@@ -716,10 +775,22 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         units = t.rows * upr;
       }
       const int64_t parts = parts_of(t, gmode, wide, ipu);
+      // a split tensor's pieces: all in this launch, the first reduces all partials
+      const int role = split ? prole[i] : 0;
+      int64_t all_units = units, all_parts = parts;
+      if (role == 1) {
+        all_units = all_parts = 0;
+        for (int k = 0; k < pnum[i]; k++) {
+          all_units += (tasks_of(io[i + k].rows * io[i + k].cols / 16) + ipu - 1) / ipu;
+          all_parts += parts_of(io[i + k], gmode, wide, ipu);
+        }
+      }
       // the kernel indexes units, partials and amax units with 32 bits: close the batch before overflow
       const int64_t au = af_self ? amax_units(nb) : 0;
-      if (b.n > 0 && (tk + units > (int64_t)INT32_MAX - ss::kCounters || pk + parts > (int64_t)INT32_MAX ||
-                      b.namax + au > (int64_t)INT32_MAX - ss::kWarps * 65536))
+      if (role != 2 && b.n > 0 &&
+          (tk + all_units > (int64_t)INT32_MAX - ss::kCounters || pk + all_parts > (int64_t)INT32_MAX ||
+           b.namax + au > (int64_t)INT32_MAX - ss::kWarps * 65536 ||
+           (role == 1 && b.n + pnum[i] > ss::kMaxTensors)))
         break;
       QTensor& q = b.t[b.n++];
       q.in = reinterpret_cast<const uint8_t*>(t.in_bf16);
@@ -741,7 +812,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       q.cpu = (int16_t)cpu;
       q.task0 = tk;
       q.part0 = (int32_t)pk;
-      q.npart = (int32_t)parts;
+      q.npart = (int32_t)(role == 0 ? parts : (role == 1 ? all_parts : 0));
       q.seg0 = gr;
       if (af_self) {  // this tensor's own amax, counted into done[b.n - 1]
         ss::AmaxTask& a = b.am[b.nam++];
@@ -755,7 +826,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       b.namax += (int32_t)au;
       tk += units;
       pk += parts;
-      gr += psegs_of(parts);
+      gr += psegs_of(q.npart);
       sums |= t.d_err_sums != nullptr;
     }
     if (b.n == 0) break;
@@ -1011,7 +1082,9 @@ ss_status ss_quantize_plan(const ss_tensor_io* tensors, int count, int f_min, in
     }
     if (k) launches += 1 + (sums ? 1 : 0);
   }
-  out->amax_fused = pl.af_self ? 1 : 0;
+  bool split = false;  // tensors over the piece limit run as row pieces, never with the fused amax
+  for (int i = 0; i < count; i++) split |= tensors[i].rows * tensors[i].cols / 16 > kPieceMax;
+  out->amax_fused = pl.af_self && !split ? 1 : 0;
   out->small_path = pl.small >= 0 ? 1 : 0;
   out->row_fused = pl.n_rowfused;
   out->launches = launches;
@@ -1028,35 +1101,46 @@ ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* a) {
   const int64_t nb = a->rows * a->cols / 16;
   if (nb > 0 && (!a->codes || !a->scales || !a->out_bf16)) return SS_ERR_INVALID_ARG;
   if (a->g_per_row && nb > 0 && !a->d_global_scale) return SS_ERR_INVALID_ARG;
-  if (nb >= ((int64_t)1 << 31)) return SS_ERR_INVALID_ARG;
+  ss_tensor_io shape;
+  std::memset(&shape, 0, sizeof(shape));
+  shape.rows = a->rows;
+  shape.cols = a->cols;
+  shape.scale_layout = a->scale_layout;
+  const int64_t pr = piece_rows(shape);  // row pieces over the 32-bit half-block index
+  if (nb > 0 && pr <= 0) return SS_ERR_INVALID_ARG;
   if (!aligned(a->codes, fi.vf ? 16 : 8) || !aligned(a->out_bf16, 16)) return SS_ERR_ALIGNMENT;
   int dev;
   DeviceInfo info;
   if (ss_status s = device_check(&dev, &info)) return s;
   if (nb == 0) return SS_OK;
-  ss::DequantParams p;
-  p.codes = a->codes;
-  p.scales = a->scales;
-  p.nb = nb;
-  p.g = a->d_global_scale;
-  p.g_per_row = a->g_per_row;
-  row_geometry(a->cols, &p.nbr, &p.nbr_magic, &p.nkt, fi.bs);
-  p.swz = a->scale_layout == SS_SCALE_SWIZZLED;
-  p.out = reinterpret_cast<uint4*>(a->out_bf16);
-  int64_t want = (nb + 255) / 256;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)info.sms * 8));
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(a->stream);
-  switch (a->format) {
-    case SS_FMT_MXFP4: ss::dequant_kernel<ss::kFmtMXFP4><<<grid, 256, 0, cs>>>(p); break;
-    case SS_FMT_MXFP6_E2M3: ss::dequant_kernel<ss::kFmtMXFP6E2M3><<<grid, 256, 0, cs>>>(p); break;
-    case SS_FMT_NVFP6_E2M3: ss::dequant_kernel<ss::kFmtNVFP6E2M3><<<grid, 256, 0, cs>>>(p); break;
-    case SS_FMT_NVFP4_B32: ss::dequant_kernel<ss::kFmtNVFP4B32><<<grid, 256, 0, cs>>>(p); break;
-    case SS_FMT_NVFP4_B64: ss::dequant_kernel<ss::kFmtNVFP4B64><<<grid, 256, 0, cs>>>(p); break;
-    case SS_FMT_NVFP4_B128: ss::dequant_kernel<ss::kFmtNVFP4B128><<<grid, 256, 0, cs>>>(p); break;
-    case SS_FMT_NVFP4_B256: ss::dequant_kernel<ss::kFmtNVFP4B256><<<grid, 256, 0, cs>>>(p); break;
-    default: ss::dequant_kernel<ss::kFmtNVFP4><<<grid, 256, 0, cs>>>(p); break;
+  const int64_t nbr = a->cols / fi.bs;
+  for (int64_t r0 = 0; r0 < a->rows; r0 += pr) {
+    const int64_t rows = std::min(pr, a->rows - r0);
+    ss::DequantParams p;
+    p.codes = a->codes + r0 * a->cols / (fi.vf ? 1 : 2);
+    p.scales = a->scales + (a->scale_layout == SS_SCALE_SWIZZLED ? (r0 / 128) * ((nbr + 3) / 4) * 512 : r0 * nbr);
+    p.nb = rows * a->cols / 16;
+    p.g = a->d_global_scale && a->g_per_row ? a->d_global_scale + r0 : a->d_global_scale;
+    p.g_per_row = a->g_per_row;
+    row_geometry(a->cols, &p.nbr, &p.nbr_magic, &p.nkt, fi.bs);
+    p.swz = a->scale_layout == SS_SCALE_SWIZZLED;
+    p.out = reinterpret_cast<uint4*>(static_cast<uint8_t*>(a->out_bf16) + r0 * a->cols * 2);
+    const int64_t want = (p.nb + 255) / 256;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)info.sms * 8));
+    switch (a->format) {
+      case SS_FMT_MXFP4: ss::dequant_kernel<ss::kFmtMXFP4><<<grid, 256, 0, cs>>>(p); break;
+      case SS_FMT_MXFP6_E2M3: ss::dequant_kernel<ss::kFmtMXFP6E2M3><<<grid, 256, 0, cs>>>(p); break;
+      case SS_FMT_NVFP6_E2M3: ss::dequant_kernel<ss::kFmtNVFP6E2M3><<<grid, 256, 0, cs>>>(p); break;
+      case SS_FMT_NVFP4_B32: ss::dequant_kernel<ss::kFmtNVFP4B32><<<grid, 256, 0, cs>>>(p); break;
+      case SS_FMT_NVFP4_B64: ss::dequant_kernel<ss::kFmtNVFP4B64><<<grid, 256, 0, cs>>>(p); break;
+      case SS_FMT_NVFP4_B128: ss::dequant_kernel<ss::kFmtNVFP4B128><<<grid, 256, 0, cs>>>(p); break;
+      case SS_FMT_NVFP4_B256: ss::dequant_kernel<ss::kFmtNVFP4B256><<<grid, 256, 0, cs>>>(p); break;
+      default: ss::dequant_kernel<ss::kFmtNVFP4><<<grid, 256, 0, cs>>>(p); break;
+    }
+    if (ss_status s = launch_status()) return s;
   }
-  return launch_status();
+  return SS_OK;
 }
 
 ss_status ss_quantize_nvfp4_f32(const float* in, int64_t rows, int64_t cols, int f_min, int f_max,

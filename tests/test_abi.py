@@ -178,3 +178,18 @@ def test_e2m3_codes_need_16_byte_alignment(L):
     io = (B.TensorIO * 1)(B.TensorIO(base, 2, 32, None, base + 1024 + 8, base + 2048, None, None, None,
                                      None, 0))
     assert L.ss_quantize_batched_fmt(io, 1, -1, 1, 0, B.FORMATS["mxfp4"][0], None) != B.SS_ERR_ALIGNMENT
+
+
+def test_piece_limit_plan(L):
+    """Tensors over the kernels' 32-bit half-block index are accepted (they run
+    as row pieces, never with the fused amax); a single row (or, swizzled, a
+    128-row band) over the piece limit is rejected synchronously."""
+    from paper_2605_12464_b200 import _binding as B
+    big = (1 << 20) + 1024, 32768                      # 2^31 + 2^21 half-blocks
+    p = B.plan([(4096, 4096), big], radius=8)       # would fuse without the split
+    assert p.amax_fused == 0
+    assert B.plan([(4096, 4096), (4096, 4096)], radius=8).amax_fused == 1
+    with pytest.raises(B.SSError):
+        B.plan([(2, 1 << 36)], radius=8)                # one row of 2^32 half-blocks
+    with pytest.raises(B.SSError):                      # 128 rows of 2^25 half-blocks: no swizzled piece
+        B.plan([(256, 1 << 29)], radius=8, scale_layout="swizzled")
