@@ -272,6 +272,74 @@ SS_API ss_status ss_quantize_nvfp4_batched_next_amax(const ss_tensor_io* tensors
                                                      uint32_t* next_amax_bits, void* stream);
 
 /*
+ * Peer-memory amax exchange for row-sharded steps (the one
+ * exchange of the method: G needs the whole tensor's amax).  Instead
+ * of a host-issued NCCL all-reduce between the amax and quantize launches,
+ * every rank owns an exchange buffer that every other rank maps (CUDA IPC,
+ * over NVLink/NVSwitch).  The quantize launch of tensor group g reads the
+ * ranks' shard amaxes of g from its own buffer once each rank's flag word
+ * for g carries the step's epoch; the same launch computes the LOCAL amaxes
+ * of group g+1 (the fused amax warps) and the warp that finishes the last of
+ * them stores them into every rank's buffer and releases its flags there.
+ * No host round trip and no collective kernel sit on the step's critical path.
+ *
+ * Buffer (ss_exchange_bytes): u32 words [2][max_tensors][8] amax slots (step
+ * parity, tensor slot, rank) + [max_groups][8] flag words, zeroed once by
+ * ss_exchange_init.  Epochs: the caller numbers steps 1, 2, ... identically
+ * on every rank; slots alternate by epoch parity, so a rank one step ahead
+ * never overwrites values a peer still reads.  A rank that never publishes
+ * trips a ~10 s watchdog (SS_FLAG_EXCHANGE_TIMEOUT, G = 1) instead of a hang.
+ */
+#define SS_FLAG_EXCHANGE_TIMEOUT 8
+#define SS_MAX_PEERS 8
+#define SS_IPC_HANDLE_BYTES 64
+typedef struct {
+  int world;                    /* ranks, 1..8                                              */
+  int rank;                     /* this rank                                                */
+  uint32_t* buf[SS_MAX_PEERS];  /* DEVICE: every rank's exchange buffer as mapped in this   */
+                                /* process (buf[rank] = own, the others via ss_ipc_open)    */
+  int max_tensors;              /* geometry, identical on every rank                        */
+  int max_groups;
+} ss_exchange;
+typedef struct {
+  int slot0;                    /* first tensor slot of the group within a step             */
+  int count;                    /* tensors of the group (= the call's count)                */
+  int group;                    /* flag word index, < max_groups                            */
+  uint32_t epoch;               /* step number >= 1, the same on every rank                 */
+} ss_exchange_group;
+
+SS_API int64_t ss_exchange_bytes(int max_tensors, int max_groups);
+/* Zero a (new) exchange buffer of ss_exchange_bytes bytes on `stream`. */
+SS_API ss_status ss_exchange_init(void* d_buf, int max_tensors, int max_groups, void* stream);
+/* A zeroed exchange buffer in its own cudaMalloc allocation (so that
+ * ss_ipc_handle exports exactly it; a sub-allocation of a caching allocator
+ * would export its whole segment), and its release. */
+SS_API ss_status ss_exchange_alloc(int max_tensors, int max_groups, void** d_buf);
+SS_API ss_status ss_exchange_free(void* d_buf);
+/* CUDA IPC: export a device allocation (SS_IPC_HANDLE_BYTES written to
+ * `handle`), map a peer's (LAZY peer access), unmap.  Plain host calls. */
+SS_API ss_status ss_ipc_handle(const void* d_ptr, void* handle);
+SS_API ss_status ss_ipc_open(const void* handle, void** d_ptr);
+SS_API ss_status ss_ipc_close(void* d_ptr);
+/* Publish `g->count` local amaxes (DEVICE u32, FP32 bits) of a group to every
+ * rank (one warp; used for the first group of a step, after
+ * ss_tensor_amax_batched). */
+SS_API ss_status ss_exchange_publish(const ss_exchange* x, const ss_exchange_group* g,
+                                     const uint32_t* d_local_amax, void* stream);
+/* Quantize group g_in (NVFP4, linear scales; per-tensor G from the ranks'
+ * amaxes in the exchange, d_amax_bits ignored) and, in the same launch, the
+ * local amaxes of the next group's shards (next_in / next_n as in
+ * ss_quantize_nvfp4_batched_next_amax, into next_local_amax, overwritten),
+ * published to every rank as group g_next.  next_count = 0: consume only.
+ * Bit-identical to ss_tensor_amax_batched + all-reduce(max) +
+ * ss_quantize_nvfp4_batched in SS_GLOBAL_DEVICE_AMAX mode. */
+SS_API ss_status ss_quantize_nvfp4_exchange(const ss_tensor_io* tensors, int count, int f_min, int f_max,
+                                            const ss_exchange* x, const ss_exchange_group* g_in,
+                                            const void* const* next_in, const int64_t* next_n,
+                                            int next_count, uint32_t* next_local_amax,
+                                            const ss_exchange_group* g_next, void* stream);
+
+/*
  * The launch plan of a batched call, without enqueueing anything (no device
  * needed; pointers are validated for null / alignment but never read):
  * which kernels ss_quantize_batched_fmt / ss_quantize_nvfp4_batched would
@@ -429,7 +497,9 @@ SS_API ss_status ss_dequantize_nvfp4_ex(const ss_dequant_args* args);
  * (device, stream) workspace: bit 0 = non-finite input seen (SS_ERR_NONFINITE),
  * bit 1 = global scale out of range (SS_ERR_RANGE), bit 2 = a fused-amax
  * search warp gave up waiting for its tensor's amax after ~10 s (a
- * watchdog against a stalled GPU; that tensor's outputs are meaningless). */
+ * watchdog against a stalled GPU; that tensor's outputs are meaningless),
+ * bit 3 = a peer-exchange wait gave up after ~10 s (a rank never published;
+ * SS_FLAG_EXCHANGE_TIMEOUT, that group's outputs are meaningless). */
 SS_API ss_status ss_get_device_status(int* flags, void* stream);
 
 #ifdef __cplusplus

@@ -113,6 +113,29 @@ class GenFormat(ctypes.Structure):
     ]
 
 
+MAX_PEERS, IPC_HANDLE_BYTES = 8, 64
+
+
+class Exchange(ctypes.Structure):
+    """ss_exchange: every rank's exchange buffer as mapped in this process."""
+    _fields_ = [
+        ("world", ctypes.c_int),
+        ("rank", ctypes.c_int),
+        ("buf", ctypes.c_void_p * MAX_PEERS),
+        ("max_tensors", ctypes.c_int),
+        ("max_groups", ctypes.c_int),
+    ]
+
+
+class ExchangeGroup(ctypes.Structure):
+    _fields_ = [
+        ("slot0", ctypes.c_int),
+        ("count", ctypes.c_int),
+        ("group", ctypes.c_int),
+        ("epoch", ctypes.c_uint32),
+    ]
+
+
 class DequantArgs(ctypes.Structure):
     _fields_ = [
         ("codes", ctypes.c_void_p),
@@ -178,6 +201,26 @@ def lib():
             L.ss_quantize_gen.argtypes = [ctypes.POINTER(TensorIO), I, I, I, ctypes.POINTER(GenFormat), P]
             L.ss_dequantize_gen.restype = I
             L.ss_dequantize_gen.argtypes = [P, P, i64, i64, ctypes.POINTER(GenFormat), P, P, P]
+            L.ss_exchange_bytes.restype = i64
+            L.ss_exchange_bytes.argtypes = [I, I]
+            L.ss_exchange_init.restype = I
+            L.ss_exchange_init.argtypes = [P, I, I, P]
+            L.ss_exchange_alloc.restype = I
+            L.ss_exchange_alloc.argtypes = [I, I, ctypes.POINTER(ctypes.c_void_p)]
+            L.ss_exchange_free.restype = I
+            L.ss_exchange_free.argtypes = [P]
+            L.ss_ipc_handle.restype = I
+            L.ss_ipc_handle.argtypes = [P, P]
+            L.ss_ipc_open.restype = I
+            L.ss_ipc_open.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
+            L.ss_ipc_close.restype = I
+            L.ss_ipc_close.argtypes = [P]
+            L.ss_exchange_publish.restype = I
+            L.ss_exchange_publish.argtypes = [ctypes.POINTER(Exchange), ctypes.POINTER(ExchangeGroup), P, P]
+            L.ss_quantize_nvfp4_exchange.restype = I
+            L.ss_quantize_nvfp4_exchange.argtypes = [ctypes.POINTER(TensorIO), I, I, I, ctypes.POINTER(Exchange),
+                                                     ctypes.POINTER(ExchangeGroup), P, P, I, P,
+                                                     ctypes.POINTER(ExchangeGroup), P]
             L.ss_get_device_status.restype = I
             L.ss_get_device_status.argtypes = [ctypes.POINTER(ctypes.c_int), P]
             _lib = L
@@ -483,3 +526,78 @@ def dequantize_gen(codes, scales, rows: int, cols: int, fmt, G=None, out=None, s
     _check(lib().ss_dequantize_gen(_ptr(codes), _ptr(scales), rows, cols, ctypes.byref(f), _ptr(G),
                                    _ptr(out), _stream_ptr(stream)), "ss_dequantize_gen")
     return out
+
+
+# ---------------------------------------------------------------------------
+# Peer-memory amax exchange (include/ss.h)
+# ---------------------------------------------------------------------------
+def exchange_bytes(max_tensors: int, max_groups: int) -> int:
+    return int(lib().ss_exchange_bytes(int(max_tensors), int(max_groups)))
+
+
+def exchange_alloc(max_tensors: int, max_groups: int) -> int:
+    """A zeroed exchange buffer in its own cudaMalloc allocation (device pointer;
+    the current device); free with exchange_free."""
+    out = ctypes.c_void_p()
+    _check(lib().ss_exchange_alloc(int(max_tensors), int(max_groups), ctypes.byref(out)), "ss_exchange_alloc")
+    return int(out.value)
+
+
+def exchange_free(ptr: int) -> None:
+    _check(lib().ss_exchange_free(ctypes.c_void_p(ptr)), "ss_exchange_free")
+
+
+def ipc_handle(ptr: int) -> bytes:
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(lib().ss_ipc_handle(ctypes.c_void_p(ptr), h), "ss_ipc_handle")
+    return h.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    out = ctypes.c_void_p()
+    _check(lib().ss_ipc_open(ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES), ctypes.byref(out)),
+           "ss_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib().ss_ipc_close(ctypes.c_void_p(ptr)), "ss_ipc_close")
+
+
+def make_exchange(world: int, rank: int, ptrs, max_tensors: int, max_groups: int) -> Exchange:
+    x = Exchange()
+    x.world, x.rank, x.max_tensors, x.max_groups = world, rank, max_tensors, max_groups
+    for r, p_ in enumerate(ptrs):
+        x.buf[r] = p_
+    return x
+
+
+def exchange_publish(x: Exchange, slot0: int, group: int, epoch: int, local_amax, stream=None):
+    g = ExchangeGroup(slot0, local_amax.numel(), group, epoch)
+    _check(lib().ss_exchange_publish(ctypes.byref(x), ctypes.byref(g), _ptr(local_amax), _stream_ptr(stream)),
+           "ss_exchange_publish")
+
+
+def quantize_exchange(xs, outs, x: Exchange, slot0: int, group: int, epoch: int, next_xs=None,
+                      next_amax=None, next_slot0: int = 0, radius=None, fmin=None, fmax=None, stream=None):
+    """Quantize ``xs`` (a group of row shards; zero-row shards included) with G
+    from the ranks' amaxes in the exchange, and publish the local amaxes of
+    ``next_xs`` (computed in the same launch into ``next_amax``) as group
+    ``group + 1`` (ss_quantize_nvfp4_exchange)."""
+    lo, hi = _window(radius, fmin, fmax)
+    n = len(xs)
+    arr = (TensorIO * max(n, 1))()
+    for i, (t, o) in enumerate(zip(xs, outs)):
+        rows, cols = t.shape
+        arr[i] = TensorIO(_ptr(t) if t.numel() else None, rows, cols, None, _ptr(o.codes) if t.numel() else None,
+                          _ptr(o.scales) if t.numel() else None, _ptr(o.err) if t.numel() else None,
+                          _ptr(o.offsets) if t.numel() else None, _ptr(o.sums), _ptr(o.G), 0)
+    gin = ExchangeGroup(slot0, n, group, epoch)
+    nn = len(next_xs) if next_xs else 0
+    ptrs = (ctypes.c_void_p * max(nn, 1))(*[t.data_ptr() if t.numel() else None for t in (next_xs or [])])
+    ns = (ctypes.c_int64 * max(nn, 1))(*[t.numel() for t in (next_xs or [])])
+    gout = ExchangeGroup(next_slot0, nn, group + 1, epoch)
+    _check(lib().ss_quantize_nvfp4_exchange(arr, n, lo, hi, ctypes.byref(x), ctypes.byref(gin), ptrs, ns, nn,
+                                            _ptr(next_amax) if nn else None, ctypes.byref(gout) if nn else None,
+                                            _stream_ptr(stream)), "ss_quantize_nvfp4_exchange")
+    return outs

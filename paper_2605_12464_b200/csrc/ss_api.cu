@@ -518,12 +518,42 @@ ss_status small_launch(const ss_tensor_io& t, int fmin, int fmax, int gmode, con
 // The one quantization path behind every entry point.
 // The next group's tensors whose local amaxes a sharded step wants while this
 // call searches (ss_quantize_nvfp4_batched_next_amax).
+// Peer-memory amax exchange of a sharded step.
+struct XIn {                  // consumer: G from every rank's slot of this group
+  const uint32_t* slots;      // own buffer: the group's first slot (stride kMaxPeers)
+  const uint32_t* flags;      // own buffer: the group's flag words [world]
+  int world;
+  uint32_t epoch;
+};
+struct XOut {                 // producer: the next group's local amaxes to every rank
+  uint32_t* slots[ss::kMaxPeers];  // rank p's buffer: the next group's first slot + this rank
+  uint32_t* flags[ss::kMaxPeers];  // rank p's flag word [next group][this rank]
+  int world;
+  uint32_t epoch;
+};
+
 struct NextAmax {
   const void* const* in;
   const int64_t* n;
   int count;
   uint32_t* out;
+  const XOut* xo = nullptr;   // also publish them (exchange)
 };
+
+ss_status publish_launch(const NextAmax* next, cudaStream_t cs) {
+  ss::XPub x;
+  std::memset(&x, 0, sizeof(x));
+  x.local = next->out;
+  x.count = next->count;
+  x.world = next->xo->world;
+  x.epoch = next->xo->epoch;
+  for (int r = 0; r < x.world; r++) {
+    x.slots[r] = next->xo->slots[r];
+    x.flags[r] = next->xo->flags[r];
+  }
+  ss::exchange_publish_kernel<<<1, 32, 0, cs>>>(x);
+  return launch_status();
+}
 
 // Launch decisions of one call (shared by quantize_core and ss_quantize_plan).
 struct Plan {
@@ -574,15 +604,17 @@ Plan make_plan(const ss_tensor_io* io, int count, int fmin, int fmax, int gmode,
 }
 
 ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
-                        void* stream, int format = SS_FMT_NVFP4, const NextAmax* next = nullptr) {
+                        void* stream, int format = SS_FMT_NVFP4, const NextAmax* next = nullptr,
+                        const XIn* xi = nullptr) {
   FmtInfo fi;
   if (!fmt_info(format, &fi)) return SS_ERR_INVALID_ARG;
   if (count < 0 || (count > 0 && !io)) return SS_ERR_INVALID_ARG;
   if (f_min > 0 || f_max < 0) return SS_ERR_INVALID_ARG;
   if (gmode < SS_GLOBAL_NONE || gmode > SS_GLOBAL_ROW) return SS_ERR_INVALID_ARG;
   if (fi.sf == 1 && gmode != SS_GLOBAL_NONE) return SS_ERR_INVALID_ARG;  // UE8M0: no global scale
-  for (int i = 0; i < count; i++)
-    if (ss_status s = validate_io(io[i], gmode, fi)) return s;
+  if (xi && (gmode != SS_GLOBAL_DEVICE_AMAX || format != SS_FMT_NVFP4)) return SS_ERR_INVALID_ARG;
+  for (int i = 0; i < count; i++)  // exchange: G comes from the buffer, no d_amax_bits needed
+    if (ss_status s = validate_io(io[i], xi ? SS_GLOBAL_NONE : gmode, fi)) return s;
   int dev;
   DeviceInfo info;
   if (ss_status s = device_check(&dev, &info)) return s;
@@ -636,7 +668,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     count = (int)pio.size();
   }
 
-  const Plan pl = make_plan(io, count, fmin, fmax, gmode, format, next);
+  Plan pl = make_plan(io, count, fmin, fmax, gmode, format, next);
+  if (xi) pl.small = -1;  // the exchange reads G from the buffer: persistent kernel only
   const bool wide = pl.wide, af_self = pl.af_self && !split, af_next = pl.af_next && !split;
   const int ri = pl.ri;
   if (next && next->count > 0) {
@@ -644,9 +677,12 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       if (cudaMemsetAsync(next->out, 0, 4 * (size_t)next->count, reinterpret_cast<cudaStream_t>(stream)) !=
           cudaSuccess)
         return SS_ERR_CUDA;
-    } else if (ss_status s = amax_launch(next->in, next->n, next->out, next->count, false,
-                                         reinterpret_cast<cudaStream_t>(stream), info.sms)) {
-      return s;  // not fusable here: a plain amax launch first
+    } else {  // not fusable here: a plain amax launch first (and its publication)
+      if (ss_status s = amax_launch(next->in, next->n, next->out, next->count, false,
+                                    reinterpret_cast<cudaStream_t>(stream), info.sms))
+        return s;
+      if (next->xo)
+        if (ss_status s = publish_launch(next, reinterpret_cast<cudaStream_t>(stream))) return s;
     }
   }
   const bool af = af_self || af_next;
@@ -733,7 +769,13 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     std::memset(&b, 0, sizeof(b));
     b.fmin = fmin;
     b.fmax = fmax;
-    b.gmode = gmode == SS_GLOBAL_NONE ? 0 : (gmode == SS_GLOBAL_ROW ? 2 : 1);
+    b.gmode = xi ? 3 : (gmode == SS_GLOBAL_NONE ? 0 : (gmode == SS_GLOBAL_ROW ? 2 : 1));
+    if (xi) {
+      b.xw = xi->world;
+      b.xin = xi->slots;
+      b.xin_flag = xi->flags;
+      b.xepoch_in = xi->epoch;
+    }
     b.g_numer = numer;
     b.ipu = ipu;
     b.part1 = ws->part1;
@@ -823,6 +865,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         a.done = b.n - 1;
       }
       q.na = (int32_t)au;
+      q.xslot = split ? psrc[i] : i;
       b.namax += (int32_t)au;
       tk += units;
       pk += parts;
@@ -830,7 +873,9 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       sums |= t.d_err_sums != nullptr;
     }
     if (b.n == 0) break;
+    bool publish_after = false;
     if (af_next && !next_done) {  // the next group's shards: local amaxes, nobody waits
+      const int32_t a_first = b.namax;
       for (int j = 0; j < next->count; j++) {
         const int64_t nv = next->n[j] / 8;
         if (nv == 0) continue;
@@ -842,6 +887,18 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         a.done = -1;
         b.namax += (int32_t)((nv + ss::kAmaxUnitVecs - 1) / ss::kAmaxUnitVecs);
       }
+      if (next->xo) {  // exchange: the warp finishing the last next-group unit publishes
+        b.xunits_out = b.namax - a_first;
+        b.xcount_out = next->count;
+        b.xlocal = next->out;
+        b.xw = next->xo->world;
+        b.xepoch_out = next->xo->epoch;
+        for (int r = 0; r < next->xo->world; r++) {
+          b.xout[r] = next->xo->slots[r];
+          b.xout_flag[r] = next->xo->flags[r];
+        }
+        publish_after = b.xunits_out == 0;  // no local next-group elements: publish the zeros after
+      }
       next_done = true;
     }
     b.ntasks = tk;
@@ -850,6 +907,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, slots));
     // later launches of a next-amax call carry no amax tasks: the plain kernel
     if (ss_status s = launch_pdl(b.nam ? k : (af_self ? k : k_plain), grid, ss::kThreads, cs, b)) return s;
+    if (publish_after)
+      if (ss_status s = publish_launch(next, cs)) return s;
     if (sums) {
       const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(gr, sums_grid(info.sms)));
       if (ss_status s = launch_pdl(ss::sums_kernel, g2, ss::kThreads, cs, b)) return s;
@@ -1041,6 +1100,137 @@ ss_status ss_quantize_nvfp4_batched_next_amax(const ss_tensor_io* tensors, int c
   if (!aligned(next_amax_bits, 4)) return SS_ERR_ALIGNMENT;
   NextAmax nx{next_in, next_n, next_count, next_amax_bits};
   return quantize_core(tensors, count, f_min, f_max, SS_GLOBAL_DEVICE_AMAX, stream, SS_FMT_NVFP4, &nx);
+}
+
+int64_t ss_exchange_bytes(int max_tensors, int max_groups) {
+  if (max_tensors < 1 || max_groups < 1) return 0;
+  return 4 * (2 * (int64_t)max_tensors * ss::kMaxPeers + (int64_t)max_groups * ss::kMaxPeers);
+}
+
+ss_status ss_exchange_init(void* d_buf, int max_tensors, int max_groups, void* stream) {
+  const int64_t bytes = ss_exchange_bytes(max_tensors, max_groups);
+  if (!d_buf || bytes <= 0 || !aligned(d_buf, 4)) return SS_ERR_INVALID_ARG;
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  return cudaMemsetAsync(d_buf, 0, (size_t)bytes, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SS_OK : SS_ERR_CUDA;
+}
+
+ss_status ss_exchange_alloc(int max_tensors, int max_groups, void** d_buf) {
+  const int64_t bytes = ss_exchange_bytes(max_tensors, max_groups);
+  if (!d_buf || bytes <= 0) return SS_ERR_INVALID_ARG;
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  *d_buf = nullptr;
+  if (cudaMalloc(d_buf, (size_t)bytes) != cudaSuccess) return SS_ERR_CUDA;
+  if (cudaMemset(*d_buf, 0, (size_t)bytes) != cudaSuccess) return SS_ERR_CUDA;  // synchronous: ready for peers
+  return SS_OK;
+}
+
+ss_status ss_exchange_free(void* d_buf) {
+  if (!d_buf) return SS_ERR_INVALID_ARG;
+  return cudaFree(d_buf) == cudaSuccess ? SS_OK : SS_ERR_CUDA;
+}
+
+ss_status ss_ipc_handle(const void* d_ptr, void* handle) {
+  if (!d_ptr || !handle) return SS_ERR_INVALID_ARG;
+  static_assert(sizeof(cudaIpcMemHandle_t) == SS_IPC_HANDLE_BYTES, "IPC handle size");
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)) != cudaSuccess) return SS_ERR_CUDA;
+  std::memcpy(handle, &h, sizeof(h));
+  return SS_OK;
+}
+
+ss_status ss_ipc_open(const void* handle, void** d_ptr) {
+  if (!handle || !d_ptr) return SS_ERR_INVALID_ARG;
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  if (cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return SS_ERR_CUDA;
+  return SS_OK;
+}
+
+ss_status ss_ipc_close(void* d_ptr) {
+  if (!d_ptr) return SS_ERR_INVALID_ARG;
+  return cudaIpcCloseMemHandle(d_ptr) == cudaSuccess ? SS_OK : SS_ERR_CUDA;
+}
+
+}  // extern "C"
+
+namespace {
+// Buffer geometry (ss.h): words [2][max_tensors][kMaxPeers] of amax slots
+// (step parity, group tensor, rank), then [max_groups][kMaxPeers] flags.
+bool exchange_ok(const ss_exchange* x, const ss_exchange_group* g, int count) {
+  if (!x || !g || x->world < 1 || x->world > ss::kMaxPeers || x->rank < 0 || x->rank >= x->world) return false;
+  if (x->max_tensors < 1 || x->max_groups < 1 || g->epoch == 0) return false;
+  if (g->group < 0 || g->group >= x->max_groups || g->slot0 < 0 || g->count != count ||
+      g->slot0 + count > x->max_tensors)
+    return false;
+  for (int r = 0; r < x->world; r++)
+    if (!x->buf[r] || !aligned(x->buf[r], 4)) return false;
+  return true;
+}
+uint32_t* ex_slots(const ss_exchange* x, int r, const ss_exchange_group* g) {
+  return x->buf[r] + ((int64_t)(g->epoch & 1u) * x->max_tensors + g->slot0) * ss::kMaxPeers;
+}
+uint32_t* ex_flags(const ss_exchange* x, int r, int group) {
+  return x->buf[r] + 2 * (int64_t)x->max_tensors * ss::kMaxPeers + (int64_t)group * ss::kMaxPeers;
+}
+void make_xout(const ss_exchange* x, const ss_exchange_group* g, XOut* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->world = x->world;
+  o->epoch = g->epoch;
+  for (int r = 0; r < x->world; r++) {
+    o->slots[r] = ex_slots(x, r, g) + x->rank;
+    o->flags[r] = ex_flags(x, r, g->group) + x->rank;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+ss_status ss_exchange_publish(const ss_exchange* x, const ss_exchange_group* g, const uint32_t* d_local_amax,
+                              void* stream) {
+  if (!x || !g || !exchange_ok(x, g, g->count) || (g->count > 0 && !d_local_amax)) return SS_ERR_INVALID_ARG;
+  int dev;
+  DeviceInfo info;
+  if (ss_status s = device_check(&dev, &info)) return s;
+  XOut o;
+  make_xout(x, g, &o);
+  NextAmax nx{nullptr, nullptr, g->count, const_cast<uint32_t*>(d_local_amax), &o};
+  return publish_launch(&nx, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ss_status ss_quantize_nvfp4_exchange(const ss_tensor_io* tensors, int count, int f_min, int f_max,
+                                     const ss_exchange* x, const ss_exchange_group* g_in,
+                                     const void* const* next_in, const int64_t* next_n, int next_count,
+                                     uint32_t* next_local_amax, const ss_exchange_group* g_next,
+                                     void* stream) {
+  if (!exchange_ok(x, g_in, count)) return SS_ERR_INVALID_ARG;
+  if (next_count < 0 || (next_count > 0 && (!next_in || !next_n || !next_local_amax || !g_next)) ||
+      next_count > ss::kMaxTensors)
+    return SS_ERR_INVALID_ARG;
+  if (next_count > 0 && !exchange_ok(x, g_next, next_count)) return SS_ERR_INVALID_ARG;
+  for (int j = 0; j < next_count; j++)
+    if (next_n[j] < 0 || next_n[j] % 8 != 0 || (next_n[j] > 0 && !aligned(next_in[j], 16)))
+      return SS_ERR_INVALID_ARG;
+  XIn xi;
+  xi.slots = ex_slots(x, x->rank, g_in);
+  xi.flags = ex_flags(x, x->rank, g_in->group);
+  xi.world = x->world;
+  xi.epoch = g_in->epoch;
+  XOut o;
+  if (next_count > 0) make_xout(x, g_next, &o);
+  NextAmax nx{next_in, next_n, next_count, next_local_amax, next_count > 0 ? &o : nullptr};
+  return quantize_core(tensors, count, f_min, f_max, SS_GLOBAL_DEVICE_AMAX, stream, SS_FMT_NVFP4,
+                       next_count > 0 ? &nx : nullptr, &xi);
 }
 
 ss_status ss_quantize_plan(const ss_tensor_io* tensors, int count, int f_min, int f_max,

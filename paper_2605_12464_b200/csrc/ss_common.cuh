@@ -73,6 +73,7 @@ struct Fmt {
 };
 __host__ __device__ constexpr float global_numer(int vf) { return vf ? 3360.0f : kGlobalNumer; }
 
-enum : uint32_t { kFlagNonFinite = 1u, kFlagRange = 2u, kFlagAmaxTimeout = 4u };
+enum : uint32_t { kFlagNonFinite = 1u, kFlagRange = 2u, kFlagAmaxTimeout = 4u, kFlagExchangeTimeout = 8u };
+constexpr int kMaxPeers = 8;  // ranks of a peer-memory amax exchange (one NVLink domain)
 
 }  // namespace ss

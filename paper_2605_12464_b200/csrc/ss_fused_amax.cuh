@@ -30,14 +30,51 @@ __device__ __forceinline__ uint32_t hmax_abs_vec(uint32_t m, const uint4& a) {
 }
 
 // Fold a unit's per-lane magnitude maxima into task ta's amax, then count the unit.
+// Peer-memory exchange, producer side: `count` local amaxes
+// are complete; one warp stores them into every rank's exchange buffer
+// (lanes stride tensors x ranks), makes the stores visible system-wide, then
+// releases each rank's flag word for this rank with `epoch`.
+__device__ __forceinline__ void exchange_store(const uint32_t* local, int count, int world, uint32_t epoch,
+                                               uint32_t* const* slots, uint32_t* const* flags, int lane) {
+  const int n = count * world;
+  for (int k = lane; k < n; k += 32) {
+    const int j = k / world, r = k - j * world;
+    st_relaxed_sys(slots[r] + j * kMaxPeers, ld_relaxed_gpu(local + j));
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (lane < world) st_release_sys(flags[lane], epoch);
+}
+__device__ __forceinline__ void exchange_out(const QuantBatch& p, int lane) {
+  exchange_store(p.xlocal, p.xcount_out, p.xw, p.xepoch_out, p.xout, p.xout_flag, lane);
+}
+
+// The same from its own one-warp launch, after a separate amax pass (stream order).
+struct XPub {
+  const uint32_t* local;
+  int count, world;
+  uint32_t epoch;
+  uint32_t* slots[kMaxPeers];
+  uint32_t* flags[kMaxPeers];
+};
+__global__ void __launch_bounds__(32) exchange_publish_kernel(const __grid_constant__ XPub x) {
+  exchange_store(x.local, x.count, x.world, x.epoch, x.slots, x.flags, threadIdx.x);
+}
+
 __device__ __forceinline__ void amax_publish(const QuantBatch& p, int ta, uint32_t m, int lane) {
   m &= 0x7FFF7FFFu;
   const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, max(m & 0xFFFFu, m >> 16));
+  uint32_t last = 0;
   if (lane == 0) {
     const AmaxTask& A = p.am[ta];
     if (r && (r << 16) > ld_relaxed_gpu(A.slot)) atomicMax(A.slot, r << 16);
-    if (A.done >= 0) red_release_add_gpu(p.done + A.done, 1u);
+    if (A.done >= 0) {
+      red_release_add_gpu(p.done + A.done, 1u);
+    } else if (p.xunits_out > 0) {  // a next-group unit of an exchanging launch
+      last = atom_add_acq_rel_gpu(p.done + kMaxTensors + 1, 1u) == (uint32_t)p.xunits_out - 1;
+    }
   }
+  if (__shfl_sync(0xFFFFFFFFu, last, 0)) exchange_out(p, lane);  // warp-uniform
 }
 
 __device__ __forceinline__ uint32_t amax_draw(const QuantBatch& p, int lane) {

@@ -4,8 +4,8 @@
 //
 // No conversion instruction exists for most of these formats, so both
 // roundings are software RNE: |t| is scaled onto its binade's quantum grid
-// with an exact power-of-two ldexp in FP64 and rounded with rint (ties to the
-// even quantum count = the even code).  The candidate arithmetic is the FP32
+// with an exact power-of-two ldexp in FP64 and rounded to nearest, ties to
+// the even code (R10).  The candidate arithmetic is the FP32
 // contract of the NVFP4 path: t = RN(y * RN(1/s)) (R7), d = RN(y - q*s) with
 // q*s exact (at most vm + sm + 2 <= 24 significant bits), R12 chains, R20
 // tree for 32-element blocks.  One thread per block; a study kernel, not a
@@ -52,8 +52,12 @@ struct GenParams {
 __device__ __forceinline__ int gen_rne_code(double a, int m, int emin) {
   if (a == 0.0) return 0;
   const int e = max(ilogb(a), emin);
-  const double r = rint(ldexp(a, m - e));  // exact scaling; RNE
-  return ((e - emin) << m) + (int)r;       // r == 2^(m+1) carries into the next binade
+  const double x = ldexp(a, m - e);  // exact scaling onto the quantum grid
+  const double fl = floor(x);
+  const int lo = ((e - emin) << m) + (int)fl;  // fl == 2^(m+1) - 1 + 1 carries into the next binade
+  // nearest; a tie goes to the even CODE (R10) -- for m = 0 the code's parity
+  // is the exponent's, not the quantum count's, so rint alone is not enough
+  return x - fl > 0.5 ? lo + 1 : (x - fl < 0.5 ? lo : lo + (lo & 1));
 }
 // Value of magnitude code c on that grid (exact).
 __device__ __forceinline__ float gen_mag_value(int c, int m, int emin) {

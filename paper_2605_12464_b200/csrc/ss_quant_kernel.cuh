@@ -105,6 +105,19 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     }
   };
   auto gscale = [&](int ti, bool report) -> float {
+    if (p.gmode == 3) {  // peer-memory exchange (§5b): wait for every rank, then the max
+      for (uint32_t spins = 0;; spins++) {
+        const bool ok = lane >= p.xw || ld_acquire_sys(p.xin_flag + lane) == p.xepoch_in;
+        if (__all_sync(0xFFFFFFFFu, ok)) break;
+        if (spins == (1u << 25)) {  // ~10 s: a rank never published (watchdog, not a hang)
+          if (lane == 0) atomicOr(p.flags, kFlagExchangeTimeout);
+          break;
+        }
+        __nanosleep(256);
+      }
+      const uint32_t v = lane < p.xw ? ld_relaxed_sys(p.xin + p.t[ti].xslot * kMaxPeers + lane) : 0u;
+      return global_scale(__reduce_max_sync(0xFFFFFFFFu, v), p.flags, report, p.g_numer);
+    }
     if (p.gmode != 1) return 1.0f;  // 0: G = 1; 2: per-row G, read per block
     return global_scale(__ldg(p.t[ti].amax), p.flags, report, p.g_numer);
   };
@@ -249,7 +262,8 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
 #ifdef SS_AF_TRACE
         if (lane == 0) atomicAdd(p.evals + 2, gtime() - t0);
 #endif
-        G = global_scale(ld_relaxed_gpu(T.amax), p.flags, li == 0 && lane == 0, p.g_numer);
+        G = p.gmode == 3 ? gscale(ti, li == 0 && lane == 0)  // exchange: the ranks' amaxes
+                         : global_scale(ld_relaxed_gpu(T.amax), p.flags, li == 0 && lane == 0, p.g_numer);
       } else {
         G = gscale(ti, li == 0 && lane == 0);
       }
@@ -302,16 +316,21 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       float best, loss0;
       int bidx;
       if constexpr (NEG >= 0) {
-        // f = 0, 1, ..., POS in chunks of CI interleaved candidates (the
-        // selection updates applied in scan order), then the negative side
-        constexpr int NC = 1 + POS;
+        // f = 0, 1, ..., POS, then -1, ..., -(kPruneFrom - 1): the
+        // unconditional candidates, in chunks of CI whose loss loops are
+        // interleaved (the selection updates applied in scan order: "<" on
+        // the positive side, "<=" on the negative side, R4); then the pruned
+        // negative side
+        constexpr int NN = NEG < kPruneFrom - 1 ? NEG : kPruneFrom - 1;
+        constexpr int NC = 1 + POS + NN;
         constexpr int CI = SS_CILP < NC ? SS_CILP : NC;
+        auto off = [](int i) { return i <= POS ? i : POS - i; };  // candidate i -> offset f
 #pragma unroll
         for (int i0 = 0; i0 < NC; i0 += CI) {
           uint4 e[CI];
           float l[CI];
 #pragma unroll
-          for (int c = 0; c < CI; c++) e[c] = base[i0 + c < NC ? i0 + c : NC - 1];
+          for (int c = 0; c < CI; c++) e[c] = base[off(i0 + c < NC ? i0 + c : NC - 1)];
           if constexpr (FMT == kFmtNVFP4) {
             cand_loss_n<CI>(y2, y, e, l);
           } else {
@@ -328,20 +347,14 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
               loss0 = l[c];  // err_base: the max-abs scale (f = 0)
               bidx = 0;
             } else {
-              const bool t_ = l[c] < best;
+              const bool t_ = i <= POS ? l[c] < best : l[c] <= best;
               best = t_ ? l[c] : best;
-              bidx = t_ ? i : bidx;
+              bidx = t_ ? off(i) : bidx;
             }
           }
         }
 #pragma unroll
-        for (int f = 1; f <= NEG; f++) {
-          if (f < kPruneFrom) {  // near offsets almost never prune for a whole warp
-            SS_TAKE(-f, <=)
-          } else {
-            SS_TAKE_NEG(-f)
-          }
-        }
+        for (int f = NN + 1; f <= NEG; f++) SS_TAKE_NEG(-f)
       } else {
         best = block_loss<FMT>(y2, y, base[0]);
         SS_COUNT(1);
@@ -439,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       if (AF) {
         for (int i = 0; i < p.n; i++) p.done[i] = 0u;
         p.done[kMaxTensors] = 0u;
+        p.done[kMaxTensors + 1] = 0u;
       }
       p.ctr[kCounters] = 0u;
     }

@@ -117,6 +117,7 @@ struct QTensor {
   // fused amax (AF launches): the search of this tensor waits until
   // QuantBatch::done[i] == na (0: G needs no in-launch amax)
   int32_t na;
+  int32_t xslot;            // gmode 3: the tensor's slot in QuantBatch::xin
 };
 
 // A tensor whose amax the AF amax warps compute: units [a0, next a0) of
@@ -149,6 +150,21 @@ struct QuantBatch {
   int32_t nam;              // AF launches: amax tasks (am[0..nam))
   AmaxTask am[kMaxTensors];
   unsigned long long* evals;  // SS_COUNT_EVALS builds: block-candidate evaluations executed
+  // Peer-memory amax exchange.  Consumer, gmode 3: G of
+  // tensor i from max_r xin[xslot_i * kMaxPeers + r] once every rank's flag
+  // xin_flag[r] == xepoch_in.  Producer: when the launch's xunits_out
+  // next-group amax units are done (counted in done[kMaxTensors + 1]), the
+  // finishing warp stores the xcount_out local amaxes (xlocal) into every
+  // rank's buffer (xout[p] + j * kMaxPeers) and releases xout_flag[p] =
+  // xepoch_out.
+  int32_t xw;               // ranks
+  uint32_t xepoch_in, xepoch_out;
+  int32_t xcount_out, xunits_out;
+  const uint32_t* xin;
+  const uint32_t* xin_flag;
+  const uint32_t* xlocal;
+  uint32_t* xout[kMaxPeers];
+  uint32_t* xout_flag[kMaxPeers];
   QTensor t[kMaxTensors];
 };
 

@@ -112,6 +112,41 @@ class CudaOps:
         return launches * (2 if self.want_sums else 1)  # quant_kernel (+ sums_kernel)
 
 
+class PeerExchange:
+    """Every rank's amax exchange buffer mapped into this process (CUDA IPC
+    over NVLink/NVSwitch).  The handles travel once through
+    ``group`` (any backend); after that no step uses the host or a collective."""
+
+    def __init__(self, group, rank: int, world: int, max_tensors: int, max_groups: int):
+        from . import _binding as B
+        self.B = B
+        self.own = B.exchange_alloc(max_tensors, max_groups)
+        ptrs, self.opened = [0] * world, []
+        ptrs[rank] = self.own
+        if world > 1:
+            import torch.distributed as dist
+            hs = [None] * world
+            dist.all_gather_object(hs, B.ipc_handle(self.own), group=group)
+            for r in range(world):
+                if r != rank:
+                    ptrs[r] = B.ipc_open(hs[r])
+                    self.opened.append(ptrs[r])
+            dist.barrier(group=group)
+        self.x = B.make_exchange(world, rank, ptrs, max_tensors, max_groups)
+        self.epoch = 0
+
+    def close(self, group=None):
+        for p in self.opened:
+            self.B.ipc_close(p)
+        if self.opened:  # no rank frees its buffer while a peer may still map it
+            import torch.distributed as dist
+            dist.barrier(group=group)
+        self.opened = []
+        if self.own:
+            self.B.exchange_free(self.own)
+            self.own = 0
+
+
 @dataclass
 class ShardPlan:
     shapes: Sequence[tuple]          # full (rows, cols) of every tensor
@@ -129,7 +164,7 @@ class ShardPlan:
 class RowShardQuantizer:
     """Quantize a list of tensors whose rows are sharded over ``world`` ranks."""
 
-    EXCHANGES = ("grouped", "single")
+    EXCHANGES = ("grouped", "single", "peer")
 
     def __init__(self, plan: ShardPlan, ops, group=None, device=None, pipeline_groups: int = 1,
                  collective: bool | None = None, exchange: str = "grouped"):
@@ -138,6 +173,10 @@ class RowShardQuantizer:
         quantize launch); "grouped" = the same exchange cut into tensor groups
         so that each group's amax runs inside the previous group's quantize
         launch (a few all-reduces per step, only the first amax exposed).
+        "peer" = the grouped step with the all-reduces replaced by the
+        peer-memory exchange (CUDA IPC buffers; each quantize launch reads
+        its group's amaxes from every rank and publishes the next group's,
+        DESIGN.md §5b): no host round trip or collective per group.
         Outputs are bit-identical either way."""
         if exchange not in self.EXCHANGES:
             raise ValueError("exchange must be one of %s" % (self.EXCHANGES,))
@@ -150,6 +189,15 @@ class RowShardQuantizer:
         self.pipeline_groups = pipeline_groups
         self._side = None
         self.groups = amax_groups([r * c for r, c in plan.shapes])
+        self.peer = None
+        if exchange == "peer" and self.collective:
+            self.peer = PeerExchange(group, plan.rank, plan.world, max(len(plan.shapes), 1),
+                                     max(len(self.groups), 1))
+
+    def close(self):
+        if self.peer is not None:
+            self.peer.close(self.group)
+            self.peer = None
 
     def step(self, shards: List[torch.Tensor], outs: List, hooks=None) -> int:
         """One pass over every tensor; returns the number of kernels launched.
@@ -180,6 +228,8 @@ class RowShardQuantizer:
         if not self.collective and self.pipeline_groups > 1 and torch.cuda.is_available() \
                 and len(shards) > 1 and shards[0].is_cuda:
             return self._pipelined(shards, outs, hooks)
+        if self.collective and self.exchange == "peer":
+            return self._peer(shards, outs, hooks)
         if self.collective and self.exchange == "grouped" and len(self.groups) > 1 and \
                 hasattr(self.ops, "quantize_next_amax"):
             return self._grouped(shards, outs, hooks)
@@ -217,6 +267,30 @@ class RowShardQuantizer:
                 hooks.after()
             if k + 1 < len(gs):
                 dist.all_reduce(buf[nlo:nhi], op=dist.ReduceOp.MAX, group=self.group)
+        return n
+
+    def _peer(self, shards, outs, hooks) -> int:
+        """Grouped step over the peer-memory exchange: amax(g0) -> publish(g0)
+        -> [quantize(g_k) reading every rank's g_k amaxes, computing and
+        publishing the local g_{k+1} amaxes in the same launch]*.  The host
+        only enqueues; ranks synchronise through flag words in device memory."""
+        B, P, buf, gs = self.ops.B, self.peer, self.amax_buf, self.groups
+        P.epoch += 1
+        lo, hi = gs[0]
+        n = self.ops.amax_all(shards[lo:hi], buf[lo:hi])
+        B.exchange_publish(P.x, lo, 0, P.epoch, buf[lo:hi])
+        n += 1
+        for k, (lo, hi) in enumerate(gs):
+            if hooks is not None:
+                hooks.before()
+            nxt = gs[k + 1] if k + 1 < len(gs) else None
+            B.quantize_exchange(shards[lo:hi], outs[lo:hi], P.x, lo, k, P.epoch,
+                                next_xs=shards[nxt[0]:nxt[1]] if nxt else None,
+                                next_amax=buf[nxt[0]:nxt[1]] if nxt else None,
+                                next_slot0=nxt[0] if nxt else 0, fmin=self.ops.fmin, fmax=self.ops.fmax)
+            if hooks is not None:
+                hooks.after()
+            n += (1 + (1 if self.ops.want_sums else 0)) * ((hi - lo + 127) // 128)
         return n
 
     def _pipelined(self, shards, outs, hooks) -> int:

@@ -1,5 +1,7 @@
 """Row-shard driver on the CUDA path: world_size 2 on one B200 (gloo carries the
-amax all-reduce so two ranks can share the device; the product uses NCCL).
+amax all-reduce so two ranks can share the device; the product uses NCCL), and
+the peer-memory exchange (CUDA IPC between the ranks' processes; gloo only
+carries the IPC handles once).
 
 Both ranks quantize their row shards of a list of tensors with CudaOps
 (batched libss launches); the concatenated shards must be bitwise the CPU
@@ -42,8 +44,10 @@ def _worker(rank, world, port, q, exchange="grouped", nan_at=None):
         ops = CudaOps(-8, 8, want_err=True, want_sums=True)
         outs = [ops.alloc_out(x) for x in shards]
         qz = RowShardQuantizer(plan, ops, group=None, device="cuda", exchange=exchange)
-        n = qz.step(shards, outs)
+        for _ in range(3 if exchange == "peer" else 1):  # peer: epochs 1..3 (both slot parities)
+            n = qz.step(shards, outs)
         torch.cuda.synchronize()
+        qz.close()
         res = [None if o.codes.numel() == 0 else
                (o.codes.cpu().numpy(), o.scales.cpu().numpy(), o.err.cpu().numpy(), float(o.G.item()))
                for o in outs]
@@ -77,7 +81,8 @@ def _run(world, exchange="grouped", nan_at=None):
     return n, gathered
 
 
-@pytest.mark.parametrize("world,exchange", [(2, "grouped"), (3, "grouped"), (2, "single")])
+@pytest.mark.parametrize("world,exchange", [(2, "grouped"), (3, "grouped"), (2, "single"), (2, "peer"),
+                                            (3, "peer")])
 def test_sharded_cuda_equals_oracle(oracle_lib, world, exchange):
     n, gathered = _run(world, exchange)
     assert n >= 2  # one batched amax + one batched quantize launch at least
@@ -94,7 +99,7 @@ def test_sharded_cuda_equals_oracle(oracle_lib, world, exchange):
         assert all(np.float32(p[3]) == np.float32(whole.G) for p in parts)
 
 
-@pytest.mark.parametrize("exchange", ["grouped", "single"])
+@pytest.mark.parametrize("exchange", ["grouped", "single", "peer"])
 def test_nan_on_one_rank_flags_every_rank(oracle_lib, exchange):
     # rank 1 of 2 holds rows 150..299 of tensor 0: poison its local row 10
     n, gathered = _run(2, exchange, nan_at=(1, 0, 10, 3))
@@ -108,3 +113,35 @@ def test_nan_on_one_rank_flags_every_rank(oracle_lib, exchange):
         parts = [g[0][k] for g in gathered if g[0][k] is not None]
         assert np.array_equal(np.concatenate([p[0] for p in parts]), whole.codes), k
         assert all(np.float32(p[3]) == np.float32(whole.G) for p in parts), k
+
+
+def test_peer_exchange_world1_equals_oracle(oracle_lib):
+    """The peer-memory exchange at world size 1 (own buffer only, no process
+    group): several steps (both slot parities), every output against the
+    oracle; the C2 layer-0 shapes make several groups."""
+    import paper_2605_12464_b200 as ss
+    from paper_2605_12464_b200.dist import CudaOps, RowShardQuantizer, ShardPlan
+    specs = ssgen.workload("c2_qwen3_8b_weights")[:7]
+    xs = [ssgen.generate(s.kind, s.rows // 8, s.cols, seed=ssgen.workloads.BASE_SEED, tid=s.tid) for s in specs]
+    shapes = [tuple(x.shape) for x in xs] + [(0, 64), (3, 32)]
+    xs += [torch.zeros(0, 64, dtype=torch.bfloat16), ssgen.generate("gaussian", 3, 32, seed=4, tid=4)]
+    plan = ShardPlan(shapes, 0, 1)
+    ops = CudaOps(-2, 6, want_err=True, want_sums=True)
+    shards = [x.cuda() for x in xs]
+    outs = [ops.alloc_out(x) for x in shards]
+    qz = RowShardQuantizer(plan, ops, device="cuda", collective=True, exchange="peer")
+    assert len(qz.groups) > 1
+    for _ in range(3):
+        qz.step(shards, outs)
+    torch.cuda.synchronize()
+    qz.close()
+    assert ss.device_status() == 0
+    for x, o in zip(xs, outs):
+        if x.numel() == 0:
+            continue
+        r = oracle_lib.quantize(x, x.shape[0], x.shape[1], -2, 6, "tensor")
+        assert np.array_equal(o.codes.cpu().numpy(), r.codes)
+        assert np.array_equal(o.scales.cpu().numpy(), r.scales)
+        assert np.array_equal(o.err.cpu().numpy().view(np.uint32), r.err.view(np.uint32))
+        assert np.float32(o.G.item()) == np.float32(r.G)
+        np.testing.assert_allclose(o.sums.cpu().numpy(), r.sums, rtol=1e-9)
