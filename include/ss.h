@@ -286,8 +286,11 @@ SS_API ss_status ss_quantize_nvfp4_batched_next_amax(const ss_tensor_io* tensors
  * Buffer (ss_exchange_bytes): u32 words [2][max_tensors][8] amax slots (step
  * parity, tensor slot, rank) + [max_groups][8] flag words, zeroed once by
  * ss_exchange_init.  Epochs: the caller numbers steps 1, 2, ... identically
- * on every rank; slots alternate by epoch parity, so a rank one step ahead
- * never overwrites values a peer still reads.  A rank that never publishes
+ * on every rank.  A consumer accepts a flag >= its epoch (a rank may run one
+ * step ahead: it needs nothing from a peer's consumption to publish the next
+ * step), and slots alternate by epoch parity, so that rank never overwrites
+ * values a peer still reads (two steps ahead it would need the peer's next
+ * publication, which is stream-ordered after the peer's reads).  A rank that never publishes
  * trips a ~10 s watchdog (SS_FLAG_EXCHANGE_TIMEOUT, G = 1) instead of a hang.
  */
 #define SS_FLAG_EXCHANGE_TIMEOUT 8

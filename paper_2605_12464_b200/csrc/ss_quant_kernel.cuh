@@ -107,7 +107,10 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   auto gscale = [&](int ti, bool report) -> float {
     if (p.gmode == 3) {  // peer-memory exchange (§5b): wait for every rank, then the max
       for (uint32_t spins = 0;; spins++) {
-        const bool ok = lane >= p.xw || ld_acquire_sys(p.xin_flag + lane) == p.xepoch_in;
+        // >= (mod 2^32): a rank may already have published the NEXT step's
+        // flag (it needs nothing from this launch to get there); its slots for
+        // this step stay intact in the other parity
+        const bool ok = lane >= p.xw || (int32_t)(ld_acquire_sys(p.xin_flag + lane) - p.xepoch_in) >= 0;
         if (__all_sync(0xFFFFFFFFu, ok)) break;
         if (spins == (1u << 25)) {  // ~10 s: a rank never published (watchdog, not a hang)
           if (lane == 0) atomicOr(p.flags, kFlagExchangeTimeout);

@@ -152,7 +152,7 @@ struct QuantBatch {
   unsigned long long* evals;  // SS_COUNT_EVALS builds: block-candidate evaluations executed
   // Peer-memory amax exchange.  Consumer, gmode 3: G of
   // tensor i from max_r xin[xslot_i * kMaxPeers + r] once every rank's flag
-  // xin_flag[r] == xepoch_in.  Producer: when the launch's xunits_out
+  // xin_flag[r] >= xepoch_in (mod 2^32).  Producer: when the launch's xunits_out
   // next-group amax units are done (counted in done[kMaxTensors + 1]), the
   // finishing warp stores the xcount_out local amaxes (xlocal) into every
   // rank's buffer (xout[p] + j * kMaxPeers) and releases xout_flag[p] =

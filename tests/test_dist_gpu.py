@@ -44,8 +44,8 @@ def _worker(rank, world, port, q, exchange="grouped", nan_at=None):
         ops = CudaOps(-8, 8, want_err=True, want_sums=True)
         outs = [ops.alloc_out(x) for x in shards]
         qz = RowShardQuantizer(plan, ops, group=None, device="cuda", exchange=exchange)
-        for _ in range(3 if exchange == "peer" else 1):  # peer: epochs 1..3 (both slot parities)
-            n = qz.step(shards, outs)
+        for _ in range(3 if exchange == "peer" else 1):  # peer: epochs 1..3 (both slot parities),
+            n = qz.step(shards, outs)                    # enqueued back to back (ranks may run ahead)
         torch.cuda.synchronize()
         qz.close()
         res = [None if o.codes.numel() == 0 else
@@ -145,3 +145,48 @@ def test_peer_exchange_world1_equals_oracle(oracle_lib):
         assert np.array_equal(o.err.cpu().numpy().view(np.uint32), r.err.view(np.uint32))
         assert np.float32(o.G.item()) == np.float32(r.G)
         np.testing.assert_allclose(o.sums.cpu().numpy(), r.sums, rtol=1e-9)
+
+
+def _worker_one_group(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2605_12464_b200 as ss
+        from paper_2605_12464_b200.dist import CudaOps, RowShardQuantizer, ShardPlan
+        x = ssgen.generate("gaussian", 2048, 4096, seed=5, tid=1)
+        plan = ShardPlan([tuple(x.shape)], rank, world)
+        shard = x[slice(*plan.rows(0))].contiguous().cuda()
+        ops = CudaOps(-8, 8)
+        outs = [ops.alloc_out(shard)]
+        qz = RowShardQuantizer(plan, ops, device="cuda", exchange="peer")
+        assert len(qz.groups) == 1
+        for _ in range(8):   # one group: a rank can publish step e+1 before its peer consumed step e
+            qz.step([shard], outs)
+        torch.cuda.synchronize()
+        qz.close()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (outs[0].codes.cpu().numpy(), float(outs[0].G.item()),
+                                          ss.device_status()))
+        if rank == 0:
+            q.put(gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_one_group_back_to_back(oracle_lib):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_one_group, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    x = ssgen.generate("gaussian", 2048, 4096, seed=5, tid=1)
+    whole = oracle_lib.quantize(x, 2048, 4096, -8, 8, "tensor")
+    assert all(st == 0 for _, _, st in gathered)
+    assert np.array_equal(np.concatenate([g[0] for g in gathered]), whole.codes)
+    assert all(np.float32(g[1]) == np.float32(whole.G) for g in gathered)

@@ -25,7 +25,7 @@ import sys
 import threading
 import time
 
-ROOT = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 METRIC = "scalesearch_nvfp4_quantize_gbs_bf16_in"
@@ -388,7 +388,11 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.synchronize()
 
     for i in range(a.warmup):
+        t0 = time.time()
         q.step(shard_sets[i % copies], outs)
+        torch.cuda.synchronize()
+        sys.stderr.write("[dbg] rank %d warmup %d %.3f s status %d epoch %s\n" % (
+            rank, i, time.time() - t0, ss.device_status(), getattr(q.peer, "epoch", None)))
     torch.cuda.synchronize()
     if dist_on:
         dist.barrier()
