@@ -10,8 +10,10 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2
 for rep in 1 2; do
   for v in ${VARS//,/ }; do
     timeout 600 python tools/kbench.py one --variants $v --layers 4 --reps 10 --windows=0:0,-1:1,-2:2,-2:6,-8:8 >> gpurun_out/kbench_$TAG.jsonl 2>> gpurun_out/kbench_$TAG.err
-    for w in 0:0 -1:1 -2:2 -8:8; do
-      timeout 300 python tools/qone.py --workload c5_gauss_1gib --window=$w --reps 6 --variant $v 2>>gpurun_out/qone_$TAG.err | tail -1 | sed "s/^{/{\"variant\": \"$v\", /" >> gpurun_out/qone_$TAG.jsonl
+    for wl in c5_gauss_1gib c1_gauss4096; do
+      for w in 0:0 -1:1 -2:2 -8:8; do
+        timeout 300 python tools/qone.py --workload $wl --window=$w --reps 20 --variant $v 2>>gpurun_out/qone_$TAG.err | sort -t: -k5 | python -c "import sys,json; L=[json.loads(l) for l in sys.stdin]; L.sort(key=lambda d: d['ms']); print(json.dumps(L[len(L)//2]))" | sed "s/^{/{\"variant\": \"$v\", /" >> gpurun_out/qone_$TAG.jsonl
+      done
     done
   done
 done

@@ -15,7 +15,8 @@ def main(tag):
                 r = json.loads(ln)
                 if r.get("kernel", "quant") != "quant":
                     continue
-                d[(kind, tuple(r["window"]), r["variant"])].append(r["ms"])
+                d[(r.get("workload", kind) if kind != "c2x4" else kind, tuple(r["window"]), r["variant"])].append(
+                    r["ms"])
         except FileNotFoundError:
             pass
     variants = sorted({k[2] for k in d}, key=lambda v: (v != "prev", v != "base", v))
