@@ -150,6 +150,14 @@ def report(cfg, fmin, fmax, res, n, ceff, s_best, s_base, hist, hbm, mhz, extra=
         ev = res["evaluated_per_block"]
         line["executed_c_per_block"] = ev
         line["executed_alu_frac"] = (4.0 * ev + 2.0) * n / alu_peak / tq
+        line["executed_frac_3op"] = (3.0 * ev + 2.0) * n / alu_peak / tq
+    # the algorithmic (4-op, every valid candidate) fraction is
+    # the headline while it is <= 1; past 1 (pruning skips work) the executed
+    # 3-op fraction is, when a counting run measured it
+    if line["roofline_frac"] <= 1.0 or "executed_frac_3op" not in line:
+        line["headline_frac"], line["headline_basis"] = line["roofline_frac"], "algorithmic"
+    else:
+        line["headline_frac"], line["headline_basis"] = line["executed_frac_3op"], "executed 3-op"
     if extra:
         line.update(extra)
     print(json.dumps(line), flush=True)
