@@ -278,7 +278,11 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     float2* err = T.err ? T.err + b0 / kHalves : nullptr;
     const uint64_t GG = pack2(G, G);
 
-#pragma unroll 1
+    // both blocks of a lane in one unrolled body for the windows where that
+    // measured faster (r = 2: -2 %, [-2, 6]: -1.4 %; r = 1 and r >= 3 slower,
+    // profiles/r02/ab4_unroll.md)
+    constexpr int kUnrollU = (NEG == 2 && (POS == 2 || POS == 6)) ? kBPL : 1;
+#pragma unroll kUnrollU
     for (int u = 0; u < kBPL; u++) {
       const int j = u * 32 + lane;          // half-block within the item
       const bool active = j < nblk;
