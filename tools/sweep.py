@@ -169,7 +169,7 @@ def main():
     import ssgen
     import paper_2605_12464_b200 as ss
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,oracle,c2,c3,c4,f32,paper_tab,c5,formats")
+    ap.add_argument("--configs", default="c1,oracle,oracle_samples,c2,c3,c4,f32,paper_tab,c5,formats")
     ap.add_argument("--c5-gib", default="1,8")
     ap.add_argument("--out", default=None)
     ap.add_argument("--variant", default="base", help="tools build libss_<variant>.so (e.g. count)")
@@ -218,6 +218,37 @@ def main():
             lines.append(line)
         del x, xc, o
         torch.cuda.empty_cache()
+    if "oracle_samples" in cfgs:   # a fixed 2^24-element sample per config and radius,
+        import time               # all host cores, with the extrapolated full-workload oracle time
+        import oracle
+        oracle.build()
+        for name, windows in (("c2_qwen3_8b_weights", [(0, 0), (-2, 6), (-8, 8)]),
+                              ("c3_act_student_t", [(0, 0), (-1, 1), (-2, 2), (-8, 8), (-16, 16)]),
+                              ("c4_llama70b_kv", [(-8, 8)]),
+                              ("c5_gauss_1gib", [(0, 0), (-1, 1), (-8, 8), (-126, 126)])):
+            specs = ssgen.workload(name)
+            full = sum(sp.numel for sp in specs)
+            sample, need = [], 1 << 24   # leading rows of the leading tensors, 2^24 elements
+            for sp in specs:
+                rows = min(sp.rows, -(-need // sp.cols))
+                sample.append(ssgen.generate(sp.kind, sp.rows, sp.cols, seed=seed, tid=sp.tid, row_start=0,
+                                             row_end=rows))
+                need -= rows * sp.cols
+                if need <= 0:
+                    break
+            n = sum(x.numel() for x in sample)
+            for w in windows:
+                t0 = time.perf_counter()
+                for x in sample:
+                    oracle.quantize(x, x.shape[0], x.shape[1], w[0], w[1], "tensor", threads=0)
+                dt = time.perf_counter() - t0
+                line = {"config": "oracle_sample_" + name, "window": list(w), "elements": n,
+                        "cpu": os.cpu_count(), "threads": os.cpu_count(), "oracle_s": dt,
+                        "oracle_gelem_s": n / dt / 1e9, "oracle_gbs_bf16": 2 * n / dt / 1e9,
+                        "extrapolated_full_s": dt * full / n,
+                        "note": "G from each sample tensor's own amax (timing only)"}
+                print(json.dumps(line), flush=True)
+                lines.append(line)
     if "c2" in cfgs:
         xs = gen(ssgen.workload("c2_qwen3_8b_weights"))
         for w in [(-8, 8), (-2, 6), (0, 0)]:
