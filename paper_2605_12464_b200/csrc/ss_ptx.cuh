@@ -30,6 +30,18 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
+// bf16 pair word -> (lo as f32 bits, hi as f32 bits): exact widening.  The
+// low half moves up with a byte permute (integer ALU pipe) instead of a
+// shift the compiler may place on the FMA pipe as IMAD.
+__device__ __forceinline__ uint64_t bf16x2_to_f32x2(uint32_t w) {
+#ifdef SS_PRMT_WIDEN
+  uint32_t lo;
+  asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(lo) : "r"(w));
+  return pack2u(lo, w & 0xFFFF0000u);
+#else
+  return pack2u(w << 16, w & 0xFFFF0000u);
+#endif
+}
 // E2M1 nibbles of (lo, hi) -> f16x2 (q_lo, q_hi).
 __device__ __forceinline__ uint32_t e2m1_round_f16x2(float lo, float hi) {
   uint32_t h;

@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       uint64_t y2[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        y2[k] = fmul2(pack2u(wd[k] << 16, wd[k] & 0xFFFF0000u), Gb);
+        y2[k] = fmul2(bf16x2_to_f32x2(wd[k]), Gb);
         unpack2(y2[k], y[2 * k], y[2 * k + 1]);
       }
       // a4: block max-abs scale code c0 (Alg. 1 lines 1-2)

@@ -39,6 +39,7 @@ VARIANTS = {
     "rowupr4": ["SS_ROW_UPR=4"],
     "nosmall": ["SS_SMALL_MAX_BLOCKS=0"],
     "unrollu": ["SS_UNROLL_U=1"],
+    "prmt": ["SS_PRMT_WIDEN=1"],
     "ipu1": ["SS_IPU_MAX=1"],
     "ipu2": ["SS_IPU_MAX=2"],
     "ipu8": ["SS_IPU_MAX=8"],
