@@ -15,7 +15,7 @@ if has bench; then
   timeout 900 python bench.py --steps 10 --warmup 3 --out gpurun_out/bench_$TAG.json > gpurun_out/bench_$TAG.log 2>&1
 fi
 if has ncu; then
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"quant_kernel|amax_kernel|sums_kernel|rowscale_kernel|dequant" -c 400 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --profile --steps 2 --warmup 1 > gpurun_out/ncu_launch_$TAG.log 2>&1
   python tools/ncu_summary.py launches gpurun_out/launches_$TAG.csv > gpurun_out/launches_$TAG.md 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:quant_kernel -s 2 -c 1 \

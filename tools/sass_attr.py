@@ -72,10 +72,11 @@ def main():
     kname = rows[0][1]
     head = rows[1]
     ia, ie, iss = head.index("Address"), head.index("Instructions Executed"), head.index("# Samples")
+    stall_cols = [(k, c) for k, c in enumerate(head) if c.startswith("stall_") and "(Not Issued)" not in c]
     data = [r for r in rows[2:] if len(r) > ie and r[ia].startswith("0x")]
     base = int(data[0][ia], 16)
     table = line_table(a.lib, mangled(kname))
-    agg = defaultdict(lambda: [0, 0, set()])
+    agg = defaultdict(lambda: [0, 0, set(), defaultdict(int)])
     total = 0
     for r in data:
         off = int(r[ia], 16) - base
@@ -86,6 +87,9 @@ def main():
         e[0] += n
         e[1] += int(r[iss] or 0)
         e[2].add(ins.split()[0] if not ins.startswith("@") else ins.split()[1])
+        for k, c in stall_cols:
+            if k < len(r) and r[k] not in ("", "0"):
+                e[3][c[6:]] += int(float(r[k]))
     srcs = {}
     for d in ("paper_2605_12464_b200/csrc",):
         for f in os.listdir(os.path.join(ROOT, d)):
@@ -93,13 +97,16 @@ def main():
     print("kernel:", kname)
     print("warp instructions executed: %d%s" % (total, "  (%.1f per half-block per lane)" % (
         total * 32 / a.halfblocks) if a.halfblocks else ""))
-    print("\n| file:line | warp inst | share | per hb | samples | opcodes | source |\n|---|---|---|---|---|---|---|")
-    for loc, (n, smp, ops) in sorted(agg.items(), key=lambda kv: -kv[1][0])[: a.top]:
+    tot_smp = sum(v[1] for v in agg.values()) or 1
+    print("\n| file:line | warp inst | share | per hb | stall samples (share) | top stall reasons | opcodes | source |")
+    print("|---|---|---|---|---|---|---|---|")
+    for loc, (n, smp, ops, st) in sorted(agg.items(), key=lambda kv: -kv[1][0])[: a.top]:
         txt = srcs.get(loc[0], [""] * (loc[1] + 1))[loc[1] - 1].strip() if loc else ""
-        print("| %s | %d | %.1f%% | %s | %d | %s | `%s` |" % (
+        top = ", ".join("%s %d" % kv for kv in sorted(st.items(), key=lambda kv: -kv[1])[:3])
+        print("| %s | %d | %.1f%% | %s | %d (%.1f%%) | %s | %s | `%s` |" % (
             "%s:%d" % loc if loc else "?", n, 100.0 * n / total,
-            "%.1f" % (n * 32 / a.halfblocks) if a.halfblocks else "-", smp,
-            " ".join(sorted(ops))[:60], txt[:70].replace("|", "\\|")))
+            "%.1f" % (n * 32 / a.halfblocks) if a.halfblocks else "-", smp, 100.0 * smp / tot_smp, top,
+            " ".join(sorted(ops))[:50], txt[:60].replace("|", "\\|")))
 
 
 if __name__ == "__main__":
