@@ -11,7 +11,7 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2
 for c in $CASES; do
   IFS=: read -r wl lo hi <<< "$c"
   name=${wl}_${lo}_${hi}_$TAG
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:quant_kernel -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"quant_kernel|quant_narrow" -s 1 -c 1 \
     -o gpurun_out/$name python tools/qone.py --workload $wl --window=$lo:$hi --reps 2 --variant $VAR > gpurun_out/$name.log 2>&1
   if [ -f gpurun_out/$name.ncu-rep ]; then
     python tools/ncu_summary.py full gpurun_out/$name.ncu-rep > gpurun_out/$name.md 2>&1

@@ -26,7 +26,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def mangled(name: str) -> str:
     # void ss::quant_kernel<(int)0, (int)0, (int)0, (int)0, (bool)0>(ss::QuantBatch)
-    m = re.search(r"quant_kernel<(.*)>\(", name)
+    kn = re.search(r"ss::(quant_\w+)<", name).group(1)
+    m = re.search(r"%s<(.*)>\(" % kn, name)
     args = [a.strip() for a in m.group(1).split(",")]
     enc = ""
     for a in args:
@@ -36,7 +37,7 @@ def mangled(name: str) -> str:
         else:
             iv = int(v)
             enc += "Li%sE" % (str(iv) if iv >= 0 else "n%d" % -iv)
-    return "_ZN2ss12quant_kernelI%sEEvNS_10QuantBatchE" % enc
+    return "_ZN2ss%d%sI%sEEvNS_10QuantBatchE" % (len(kn), kn, enc)
 
 
 def line_table(lib: str, fn: str):
