@@ -193,3 +193,42 @@ def test_piece_limit_plan(L):
         B.plan([(2, 1 << 36)], radius=8)                # one row of 2^32 half-blocks
     with pytest.raises(B.SSError):                      # 128 rows of 2^25 half-blocks: no swizzled piece
         B.plan([(256, 1 << 29)], radius=8, scale_layout="swizzled")
+
+
+def test_generic_and_exchange_argument_errors(L):
+    """ss_quantize_gen / ss_dequantize_gen and the peer-exchange entry points
+    reject bad arguments synchronously (no device needed)."""
+    from paper_2605_12464_b200 import _binding as B
+    P = ctypes.c_void_p
+    buf = ctypes.create_string_buffer(4096 + 64)
+    base = (ctypes.addressof(buf) + 63) // 64 * 64
+    io = B.TensorIO(base, 4, 64, None, base, base, None, None, None, None, 0)
+    for fmt in ((0, 3, 4, 3, 16), (2, 6, 4, 3, 16), (2, 1, 8, 1, 16), (2, 1, 4, 3, 48), (2, 1, 9, 0, 16)):
+        f = B.GenFormat(*fmt)
+        assert L.ss_quantize_gen(ctypes.byref(io), -2, 2, 0, ctypes.byref(f), None) == B.SS_ERR_INVALID_ARG
+    f = B.GenFormat(2, 1, 8, 0, 32)     # UE8M0: no global scale (vmax * smax overflows binary32)
+    assert L.ss_quantize_gen(ctypes.byref(io), -2, 2, 1, ctypes.byref(f), None) == B.SS_ERR_INVALID_ARG
+    f = B.GenFormat(2, 1, 4, 3, 16)
+    assert L.ss_quantize_gen(ctypes.byref(io), 1, 2, 0, ctypes.byref(f), None) == B.SS_ERR_INVALID_ARG
+    bad = B.TensorIO(base, 4, 64, None, base + 8, base, None, None, None, None, 0)  # codes not 16-B aligned
+    assert L.ss_quantize_gen(ctypes.byref(bad), -2, 2, 0, ctypes.byref(f), None) == B.SS_ERR_ALIGNMENT
+    assert L.ss_dequantize_gen(P(base), P(base), 4, 40, ctypes.byref(f), None, P(base), None) == B.SS_ERR_INVALID_ARG
+    # exchange geometry and descriptors
+    assert L.ss_exchange_bytes(0, 1) == 0
+    assert L.ss_exchange_bytes(252, 8) == 4 * (2 * 252 * 8 + 8 * 8)
+    assert L.ss_exchange_init(None, 4, 2, None) == B.SS_ERR_INVALID_ARG
+    x = B.make_exchange(2, 0, [base, base + 1024], 4, 2)
+    g = B.ExchangeGroup(0, 2, 0, 1)
+    assert L.ss_exchange_publish(ctypes.byref(x), ctypes.byref(g), None, None) == B.SS_ERR_INVALID_ARG
+    g0 = B.ExchangeGroup(3, 2, 0, 1)    # slot0 + count > max_tensors
+    assert L.ss_exchange_publish(ctypes.byref(x), ctypes.byref(g0), P(base), None) == B.SS_ERR_INVALID_ARG
+    g0 = B.ExchangeGroup(0, 2, 0, 0)    # epoch 0 is reserved (a zeroed buffer)
+    assert L.ss_exchange_publish(ctypes.byref(x), ctypes.byref(g0), P(base), None) == B.SS_ERR_INVALID_ARG
+    x9 = B.make_exchange(9, 0, [base] * 8, 4, 2)
+    assert L.ss_exchange_publish(ctypes.byref(x9), ctypes.byref(g), P(base), None) == B.SS_ERR_INVALID_ARG
+    ios = (B.TensorIO * 2)(io, io)
+    gin = B.ExchangeGroup(0, 3, 0, 1)   # count differs from the call's
+    assert L.ss_quantize_nvfp4_exchange(ios, 2, -8, 8, ctypes.byref(x), ctypes.byref(gin), None, None, 0, None,
+                                        None, None) == B.SS_ERR_INVALID_ARG
+    assert L.ss_ipc_handle(None, P(base)) == B.SS_ERR_INVALID_ARG
+    assert L.ss_ipc_open(None, ctypes.byref(ctypes.c_void_p())) == B.SS_ERR_INVALID_ARG
