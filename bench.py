@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: several ranks may share one GPU (testing the sharded path on a "
                          "1-GPU box); the product uses nccl")
+    ap.add_argument("--probe-shared-gpu", action="store_true",
+                    help="test only: let --exchange auto probe the peer exchange even when ranks share a GPU")
     ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "grouped", "single"],
                     help="sharded steps: the amax exchange over peer memory inside the quantize "
                          "launches (peer, DESIGN.md §5b), as NCCL all-reduces per tensor group "
@@ -302,19 +304,24 @@ def c_eff_of(torch, outs, shards, fmin, fmax, max_tensors=8):
     return tot / max(cnt, 1)
 
 
-def pick_exchange(torch, dist, ss, plan, ops, shards, dist_on, world, dev_idx):
+def pick_exchange(torch, dist, ss, plan, ops, shards, dist_on, world, dev_idx, shared_ok=False):
     """--exchange auto: the peer-memory exchange when every rank
     has its own GPU with peer access to every other, and one warm-up step of it
     reproduces the NCCL grouped step bit for bit on every rank; else grouped."""
     from paper_2605_12464_b200.dist import RowShardQuantizer
     if not dist_on or world < 2:
         return "grouped", "one rank: no exchange"
+    try:
+        props = torch.cuda.get_device_properties(dev_idx)
+        mine = (str(getattr(props, "uuid", dev_idx)),
+                all(torch.cuda.can_device_access_peer(dev_idx, j)
+                    for j in range(torch.cuda.device_count()) if j != dev_idx))
+    except Exception as e:  # noqa: BLE001 -- reported; every rank then takes the NCCL path
+        sys.stderr.write("[bench] device query failed: %s\n" % e)
+        mine = ("?%d" % dev_idx, False)
     devs = [None] * world
-    dist.all_gather_object(devs, (torch.cuda.get_device_properties(dev_idx).uuid.hex
-                                  if hasattr(torch.cuda.get_device_properties(dev_idx), "uuid") else str(dev_idx),
-                                  [torch.cuda.can_device_access_peer(dev_idx, j) if j != dev_idx else True
-                                   for j in range(torch.cuda.device_count())]))
-    ok = len({d[0] for d in devs}) == world and all(all(d[1]) for d in devs)
+    dist.all_gather_object(devs, mine)
+    ok = (len({d[0] for d in devs}) == world or shared_ok) and all(d[1] for d in devs)
     if ok:
         try:
             outs_a = [ops.alloc_out(x) for x in shards]
@@ -379,7 +386,8 @@ def run_ours(a, rank, world, local_rank):
     outs = [ops.alloc_out(x) for x in shards]
     exchange, why = a.exchange, None
     if exchange == "auto":
-        exchange, why = pick_exchange(torch, dist, ss, plan, ops, shards, dist_on, world, dev_idx)
+        exchange, why = pick_exchange(torch, dist, ss, plan, ops, shards, dist_on, world, dev_idx,
+                                      a.probe_shared_gpu)
     a.exchange_used, a.exchange_note = exchange, why
     q = RowShardQuantizer(plan, ops, group=None, device=dev, collective=dist_on, exchange=exchange)
     hooks = QuantEvents(torch)
