@@ -20,7 +20,10 @@ constexpr int kBPL = SS_BPL;                  // 16-element blocks per lane per 
 constexpr int kTaskBlocks = 32 * kBPL;        // NVFP4 blocks per warp task
 constexpr int kTaskBytes = kTaskBlocks * 32;  // bf16 input bytes per task
 constexpr int kStages = kBPL >= 4 ? 2 : 4 / kBPL;  // per-warp smem buffers (tasks in flight)
-constexpr int kSegTasks = 4096;               // tasks per CTA of the error-sum kernel
+#ifndef SS_SEG_TASKS
+#define SS_SEG_TASKS 512  // C1 call 58.5 -> 56.3 us, C3 -2 % (4096 before; profiles/r02/c1ab_seg.md)
+#endif
+constexpr int kSegTasks = SS_SEG_TASKS;       // partials per CTA of the error-sum kernel
 constexpr int kCounters = 256;                // task counters of the dynamic scheduler
 #ifndef SS_PRUNE_FROM
 #define SS_PRUNE_FROM 3

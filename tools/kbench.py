@@ -40,6 +40,8 @@ VARIANTS = {
     "nosmall": ["SS_SMALL_MAX_BLOCKS=0"],
     "unrollu": ["SS_UNROLL_U=1"],
     "prmt": ["SS_PRMT_WIDEN=1"],
+    "seg512": ["SS_SEG_TASKS=512"],
+    "seg256": ["SS_SEG_TASKS=256"],
     "ipu1": ["SS_IPU_MAX=1"],
     "ipu2": ["SS_IPU_MAX=2"],
     "ipu8": ["SS_IPU_MAX=8"],
