@@ -276,6 +276,9 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
     cp_async_wait<kStages - 1>();  // this lane's copies of stage s have landed
     int8_t* offsets = T.offsets ? T.offsets + b0 / kHalves : nullptr;
     float2* err = T.err ? T.err + b0 / kHalves : nullptr;
+    // the item's output streams, so a block's stores index them with 32-bit j
+    uint2* codes_it = T.codes + b0;
+    uint8_t* scales_it = T.scales + b0 / kHalves;
     const uint64_t GG = pack2(G, G);
 
     // both blocks of a lane in one unrolled body for the windows where that
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       const bool active = j < nblk;
       const bool writer = (lane & (kHalves - 1)) == 0;  // owns the scale block
       // scale-block index within the tensor; its row (per-row G, swizzled layout)
-      const uint32_t sbk = (uint32_t)(b0 + min(j, nblk - 1)) / kHalves;
+      const uint32_t sbk = RI ? (uint32_t)(b0 + min(j, nblk - 1)) / kHalves : (uint32_t)(b0 + j) / kHalves;
       uint32_t row = x.row;
       uint64_t Gb = GG;
       if (RI && !(RI == 2 && T.hpr) && (T.g_row || T.swz)) {  // warp-uniform
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
           uint2 cw;
           cw.x = e2m1_pack8(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
           cw.y = e2m1_pack8(t[8], t[9], t[10], t[11], t[12], t[13], t[14], t[15]);
-          __stcs(T.codes + hb, cw);
+          __stcs(codes_it + j, cw);
         } else {  // E2M3: one code per byte
           uint32_t cw[4];
 #pragma unroll
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
         }
         if (writer) {
           if (!RI || !T.swz) {
-            T.scales[sbk] = (uint8_t)code;
+            scales_it[j / kHalves] = (uint8_t)code;
           } else {
             T.scales[swizzled_scale_offset(row, sbk - row * T.nbr, T.nkt)] = (uint8_t)code;
           }
