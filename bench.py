@@ -454,8 +454,10 @@ def run_ours(a, rank, world, local_rank):
     # >= 4 offsets (ss_api.cu): that kernel reads the input twice
     # the library's own launch plan (ss_quantize_plan): whether the amax ran
     # inside the quantize launch (it then reads the input twice)
-    fused = not dist_on and bool(ss.plan([tuple(x.shape) for x in shards if x.shape[0]],
-                                         fmin=a.fmin, fmax=a.fmax, gmode="tensor").amax_fused)
+    qplan = ss.plan([tuple(x.shape) for x in shards if x.shape[0]], fmin=a.fmin, fmax=a.fmax, gmode="tensor")
+    fused = not dist_on and bool(qplan.amax_fused)
+    # quantize launches per step: one per trailing-amax batch, else per 128 tensors
+    qlaunches = qplan.trail_batches if (fused and qplan.trail_batches) else (len(shards) + 127) // 128
     bytes_q = n_local * ((2.0 if fused else 0.0) + 2.0 + 0.5 + 0.0625 + 0.5)  # [amax] + in + codes + scales + err
     hbm_achieved = bytes_q / (quant_ms * 1e-3) / 1e9
     traffic, traffic_src = None, None
@@ -465,7 +467,7 @@ def run_ours(a, rank, world, local_rank):
             with open(tf) as f:
                 tj = json.load(f)
             tk = tj["fused" if fused else "plain"]
-            traffic = tk["dram_bytes_per_elem"] * n_local / ((len(shards) + 127) // 128)
+            traffic = tk["dram_bytes_per_elem"] * n_local / qlaunches
             traffic_src = "not measured in this run: DRAM bytes/element of %s scaled to this launch" % (
                 tk.get("source", "profiles/quant_traffic.json"))
         except Exception:
@@ -477,7 +479,7 @@ def run_ours(a, rank, world, local_rank):
             "ops_per_elem": ops_per_elem, "c_eff": ceff,
             "peak_source": "148 SMs x 128 FP32 lanes x %.0f MHz (%s)" % (pk["sm_max_mhz"], pk["source"]),
             "quant_ms_per_step": quant_ms, "quant_share_of_step": quant_ms / ms,
-            "quant_launches_per_step": (len(shards) + 127) // 128,
+            "quant_launches_per_step": qlaunches,
             "hbm_gbs_achieved": hbm_achieved, "hbm_peak_gbs": pk["hbm_gbs"],
             "hbm_frac": hbm_achieved / pk["hbm_gbs"]}
     if clk and clk.get("sm_mhz"):

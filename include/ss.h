@@ -354,6 +354,8 @@ typedef struct {
   int small_path;   /* 1: one small tensor through the one-thread-per-block kernel (§4.8)      */
   int row_fused;    /* tensors whose per-row amax runs inside the quantize pass (§4.4)         */
   int launches;     /* kernels the call enqueues (amax, row-scale, quantize, error-sum)        */
+  int trail_batches; /* > 1: a fused-amax call run as this many quantize launches, each
+                        folding the next one's amax (trailing amax); else 0  */
 } ss_plan;
 SS_API ss_status ss_quantize_plan(const ss_tensor_io* tensors, int count, int f_min, int f_max,
                                   int global_scale_mode, int format, ss_plan* out);

@@ -99,6 +99,7 @@ class Plan(ctypes.Structure):
         ("small_path", ctypes.c_int),
         ("row_fused", ctypes.c_int),
         ("launches", ctypes.c_int),
+        ("trail_batches", ctypes.c_int),
     ]
 
 

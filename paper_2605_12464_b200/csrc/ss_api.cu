@@ -448,6 +448,12 @@ inline int64_t psegs_of(int64_t parts) { return (parts + ss::kSegTasks - 1) / ss
 #define SS_SMALL_MAX_BLOCKS (1 << 19)
 #endif
 constexpr int64_t kSmallMaxBlocks = SS_SMALL_MAX_BLOCKS;
+// Trailing amax (§4.2c) for per-tensor-G calls of at least this many elements
+// (smaller calls keep the single fused launch); 0 disables it (tools-only A/B)
+#ifndef SS_TRAIL_MIN_ELEMS
+#define SS_TRAIL_MIN_ELEMS (int64_t(1) << 26)
+#endif
+constexpr int64_t kTrailMinElems = SS_TRAIL_MIN_ELEMS;
 
 typedef void (*SmallKernel)(ss::SmallParams);
 SmallKernel pick_small(int fmin, int fmax) {
@@ -601,6 +607,37 @@ Plan make_plan(const ss_tensor_io* io, int count, int fmin, int fmax, int gmode,
                 ? live
                 : -1;
   return p;
+}
+
+// Launch batches of a trailing-amax call (§4.2c): exclusive tensor end index
+// per launch.  Batch 0 holds about 1/64 of the elements (its amax is the only
+// one a search waits for); each later batch at most doubles its predecessor's
+// elements (its amax is folded by the predecessor's search warps at up to
+// 4 KiB per 2 KiB work item); at most kMaxTensors / 2 tensors per batch, so a
+// launch's own and next-batch amax tasks fit QuantBatch::am.  A single batch
+// (empty result) means no trailing amax.
+std::vector<int> trail_batches(const ss_tensor_io* io, int count) {
+  int64_t n_all = 0;
+  for (int i = 0; i < count; i++) n_all += io[i].rows * io[i].cols;
+  std::vector<int> bend;
+  if (count < 2 || kTrailMinElems <= 0 || n_all < kTrailMinElems) return bend;
+  int64_t lim = std::max<int64_t>(n_all / 64, 1);
+  int i = 0;
+  while (i < count) {
+    int64_t el = 0;
+    int nt = 0;
+    while (i < count && nt < ss::kMaxTensors / 2) {
+      const int64_t n = io[i].rows * io[i].cols;
+      if (nt > 0 && (el + n > lim || el + n > (int64_t(1) << 36))) break;  // 32-bit unit indices
+      el += n;
+      nt += n > 0;
+      i++;
+    }
+    bend.push_back(i);
+    lim = 2 * std::max<int64_t>(el, 1);
+  }
+  if (bend.size() < 2) bend.clear();
+  return bend;
 }
 
 ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
@@ -762,6 +799,14 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   QuantKernel k = pick_kernel(fmin, fmax, ri, format, af);
   const int64_t slots = (int64_t)info.sms * occupancy(k);
   const QuantKernel k_plain = af_next ? pick_kernel(fmin, fmax, ri, format, false) : k;
+  // Trailing amax (§4.2c): a per-tensor-G call of several tensors runs as a
+  // chain of launches whose batches grow geometrically; launch 0 computes its
+  // own (small) batch's amax with the amax warps, and every launch's search
+  // warps also fold the NEXT batch's amax after each scheduling unit, so no
+  // later launch waits for an amax and the amax reads spread over the search.
+  const std::vector<int> bend = af_self && !xi ? trail_batches(io, count) : std::vector<int>();
+  const bool trail = bend.size() > 1;
+  size_t launch_idx = 0;
   bool next_done = false;
   int i = 0;
   while (i < count) {
@@ -793,7 +838,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.done = ws->done;
     bool sums = false;
     int64_t tk = 0, gr = 0, pk = 0;
-    for (; i < count && b.n < ss::kMaxTensors; i++) {
+    const bool self_amax = af_self && (!trail || launch_idx == 0);
+    for (; i < count && b.n < ss::kMaxTensors && (!trail || i < bend[launch_idx]); i++) {
       const ss_tensor_io& t = io[i];
       const int64_t nb = t.rows * t.cols / 16;
       if (nb == 0) {
@@ -828,7 +874,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
         }
       }
       // the kernel indexes units, partials and amax units with 32 bits: close the batch before overflow
-      const int64_t au = af_self ? amax_units(nb) : 0;
+      const int64_t au = self_amax ? amax_units(nb) : 0;
       if (role != 2 && b.n > 0 &&
           (tk + all_units > (int64_t)INT32_MAX - ss::kCounters || pk + all_parts > (int64_t)INT32_MAX ||
            b.namax + au > (int64_t)INT32_MAX - ss::kWarps * 65536 ||
@@ -856,7 +902,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       q.part0 = (int32_t)pk;
       q.npart = (int32_t)(role == 0 ? parts : (role == 1 ? all_parts : 0));
       q.seg0 = gr;
-      if (af_self) {  // this tensor's own amax, counted into done[b.n - 1]
+      if (self_amax) {  // this tensor's own amax, counted into done[b.n - 1]
         ss::AmaxTask& a = b.am[b.nam++];
         a.in = reinterpret_cast<const uint4*>(t.in_bf16);
         a.nvec = 2 * nb;
@@ -901,6 +947,22 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       }
       next_done = true;
     }
+    if (trail && launch_idx + 1 < bend.size()) {  // the next batch's amax, folded by the search warps
+      b.tr0 = b.nam;
+      for (int j = bend[launch_idx]; j < bend[launch_idx + 1]; j++) {
+        const int64_t nv = 2 * (io[j].rows * io[j].cols / 16);
+        if (nv == 0) continue;
+        ss::AmaxTask& a = b.am[b.nam++];
+        a.in = reinterpret_cast<const uint4*>(io[j].in_bf16);
+        a.nvec = nv;
+        a.slot = const_cast<uint32_t*>(amax[j]);
+        a.a0 = b.ntrail;
+        a.done = -1;
+        b.ntrail += (int32_t)((nv + ss::kTrailVecs - 1) / ss::kTrailVecs);
+      }
+      b.tpu = (int32_t)((b.ntrail + tk - 1) / tk);
+    }
+    launch_idx++;
     b.ntasks = tk;
     b.nsegs = gr;
     const int64_t want = (tk + ss::kWarps - 1) / ss::kWarps;
@@ -1256,8 +1318,22 @@ ss_status ss_quantize_plan(const ss_tensor_io* tensors, int count, int f_min, in
   int launches = 0;
   if (global_scale_mode == SS_GLOBAL_TENSOR && !pl.af_self) launches += (live + per - 1) / per;  // amax_kernel
   if (global_scale_mode == SS_GLOBAL_ROW) launches += (plain_rows + per - 1) / per;              // rowscale_kernel
+  bool split = false;  // tensors over the piece limit run as row pieces, never with the fused amax
+  for (int i = 0; i < count; i++) split |= tensors[i].rows * tensors[i].cols / 16 > kPieceMax;
+  const std::vector<int> bend = pl.af_self && !split ? trail_batches(tensors, count) : std::vector<int>();
   if (pl.small >= 0) {
     launches += 1 + (tensors[pl.small].d_err_sums ? 1 : 0);  // quant_small_kernel (+ sums_kernel)
+  } else if (bend.size() > 1) {  // trailing amax: one quantize launch (+ sums_kernel) per batch
+    int i0 = 0;
+    for (const int e : bend) {
+      bool live_b = false, sums = false;
+      for (int i = i0; i < e; i++) {
+        live_b |= tensors[i].rows * tensors[i].cols > 0;
+        sums |= tensors[i].rows * tensors[i].cols > 0 && tensors[i].d_err_sums != nullptr;
+      }
+      if (live_b) launches += 1 + (sums ? 1 : 0);
+      i0 = e;
+    }
   } else {
     int k = 0;
     bool sums = false;
@@ -1272,9 +1348,8 @@ ss_status ss_quantize_plan(const ss_tensor_io* tensors, int count, int f_min, in
     }
     if (k) launches += 1 + (sums ? 1 : 0);
   }
-  bool split = false;  // tensors over the piece limit run as row pieces, never with the fused amax
-  for (int i = 0; i < count; i++) split |= tensors[i].rows * tensors[i].cols / 16 > kPieceMax;
   out->amax_fused = pl.af_self && !split ? 1 : 0;
+  out->trail_batches = bend.size() > 1 ? (int)bend.size() : 0;
   out->small_path = pl.small >= 0 ? 1 : 0;
   out->row_fused = pl.n_rowfused;
   out->launches = launches;

@@ -22,7 +22,9 @@ namespace ss {
 // units run out they join the search.  A search warp waits (acquire) for
 // done[i] == na before its first item of tensor i.  The amax warps never
 // wait, so the HBM-bound amax runs ahead under the ALU-bound search and no
-// schedule can deadlock.
+// schedule can deadlock.  Trailing amax (p.ntrail > 0, §4.2c): the search
+// warps also fold the NEXT launch's tensors' amax, a share per scheduling
+// unit; nobody in this launch waits for it.
 template <int NEG, int POS, int RI, int FMT, bool AF = false>
 __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __grid_constant__ QuantBatch p) {
   static_assert(!AF || RI == 0, "fused amax: per-tensor G, plain layout");
@@ -236,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
   int cur_ti = -1;
   float G = 1.0f;
   double sb = 0.0, sc = 0.0;  // this lane's error sums over the current unit
+  int tt = 0;                 // trailing amax: the fold's task cursor (warp-uniform, moves forward)
   while (q_li[0] >= 0) {
     const int li = q_li[0];
     const int ti = q_ti[0];
@@ -343,6 +346,23 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
           for (int c = 0; c < CI; c++) e[c] = base[off(i0 + c < NC ? i0 + c : NC - 1)];
           if constexpr (FMT == kFmtNVFP4) {
             cand_loss_n<CI>(y2, y, e, l);
+#ifdef SS_CORE_REPEAT  // tools only: evaluate the unconditional candidates twice (marginal cost per pair)
+            {
+              uint4 e2[CI];
+              float l2[CI];
+              uint32_t one;
+              asm volatile("mov.b32 %0, 0x3f800000;" : "=r"(one));
+#pragma unroll
+              for (int c = 0; c < CI; c++) {
+                e2[c] = e[c];
+                e2[c].x = __float_as_uint(__fmul_rn(__uint_as_float(e[c].x), __uint_as_float(one)));
+                e2[c].y = e2[c].x;
+              }
+              cand_loss_n<CI>(y2, y, e2, l2);
+#pragma unroll
+              for (int c = 0; c < CI; c++) l[c] = fminf(l[c], l2[c]);
+            }
+#endif
           } else {
 #pragma unroll
             for (int c = 0; c < CI; c++) l[c] = block_loss<FMT>(y2, y, e[c]);
@@ -437,6 +457,8 @@ __global__ void __launch_bounds__(kThreads, SS_MIN_BLOCKS) quant_kernel(const __
       q_pt[kStages - 1] = gpt;
     }
     if (pt >= 0) {  // the unit's last item: its partial (fixed lane tree); reduced by sums_kernel
+      // trailing amax (§4.2c): the unit's share of the next batch's amax
+      if (AF && p.ntrail) trail_fold(p, T.task0 + (pt - T.part0), tt, lane);
       if (T.sums) {
         sb = warp_sum(sb);
         sc = warp_sum(sc);

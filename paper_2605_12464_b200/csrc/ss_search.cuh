@@ -148,6 +148,13 @@ struct QuantBatch {
                             // amax unit counter (zero, re-armed)
   int32_t namax;            // AF launches: amax units of the batch
   int32_t nam;              // AF launches: amax tasks (am[0..nam))
+  // Trailing amax (AF launches of a pipelined per-tensor-G call, DESIGN.md
+  // §4.2c): the NEXT launch's tensors are am[tr0..nam), cut into ntrail
+  // units of kTrailVecs 16-B vectors numbered by AmaxTask::a0 from 0; the
+  // search warp finishing scheduling unit u folds trail units
+  // [u * tpu, u * tpu + tpu) into their tensors' slots.  Nobody waits on them
+  // in this launch; the next launch reads the slots (stream order).
+  int32_t tr0, ntrail, tpu;
   AmaxTask am[kMaxTensors];
   unsigned long long* evals;  // SS_COUNT_EVALS builds: block-candidate evaluations executed
   // Peer-memory amax exchange.  Consumer, gmode 3: G of

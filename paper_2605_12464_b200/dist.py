@@ -218,7 +218,8 @@ class RowShardQuantizer:
         import torch.distributed as dist
         self.allreduces = 0
         if not self.collective and self.pipeline_groups <= 1 and hasattr(self.ops, "quantize_local"):
-            # unsharded: amax and quantize in one launch per 128 tensors
+            # unsharded: the amax inside the quantize launches (one per 128 tensors,
+            # or the trailing-amax chain of DESIGN.md §4.2c)
             if hooks is not None:
                 hooks.before()
             n = self.ops.quantize_local(shards, outs)

@@ -8,6 +8,7 @@ Per config and window, one JSON line with the median time (CUDA events, 3
 warm-ups, `--reps` timed calls; inputs rotated over copies when the workload
 fits in L2) of
   sep    ss_tensor_amax_batched + ss_quantize_nvfp4_batched(DEVICE_AMAX)
+  search ss_quantize_nvfp4_batched(DEVICE_AMAX) alone (workloads over L2 only)
   fused  ss_quantize_nvfp4_batched(TENSOR)   (amax units inside the launch)
 and whether the fused outputs (codes, scales, errors, sums, G) equal the
 separate path's bit for bit.  --variant noamaxfusion (a build with
@@ -70,8 +71,12 @@ def main():
             def fused(s):
                 ss.quantize_batched(s, outs_b, fmin=fmin, fmax=fmax, gmode="tensor")
 
+            def search(s):  # the quantize launches alone (amax precomputed by sep)
+                ss.quantize_batched(s, outs_a, fmin=fmin, fmax=fmax, gmode="device_amax", amax=amax)
+
             t_sep = timed(sep)
             t_fused = timed(fused)
+            t_search = timed(search) if copies == 1 else None
             sep(xs)
             fused(xs)
             torch.cuda.synchronize()
@@ -81,7 +86,7 @@ def main():
                        if getattr(oa, f) is not None)
             print(json.dumps({"config": cfg, "window": [fmin, fmax], "tensors": len(xs), "elements": n,
                               "variant": a.variant,
-                              "sep_ms": t_sep, "fused_ms": t_fused, "speedup": t_sep / t_fused,
+                              "sep_ms": t_sep, "fused_ms": t_fused, "search_only_ms": t_search, "speedup": t_sep / t_fused,
                               "sep_gbs": 2 * n / t_sep / 1e6, "fused_gbs": 2 * n / t_fused / 1e6,
                               "bit_identical": bool(same),
                               "status": ss.device_status()}), flush=True)

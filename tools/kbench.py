@@ -41,6 +41,8 @@ VARIANTS = {
     "unrollu": ["SS_UNROLL_U=1"],
     "prmt": ["SS_PRMT_WIDEN=1"],
     "seg512": ["SS_SEG_TASKS=512"],
+    "corex2": ["SS_CORE_REPEAT=1"],
+    "notrail": ["SS_TRAIL_MIN_ELEMS=0"],
     "seg256": ["SS_SEG_TASKS=256"],
     "ipu1": ["SS_IPU_MAX=1"],
     "ipu2": ["SS_IPU_MAX=2"],
