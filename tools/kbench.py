@@ -44,6 +44,8 @@ VARIANTS = {
     "corex2": ["SS_CORE_REPEAT=1"],
     "notrail": ["SS_TRAIL_MIN_ELEMS=0"],
     "seg256": ["SS_SEG_TASKS=256"],
+    "seg128": ["SS_SEG_TASKS=128"],
+    "seg64": ["SS_SEG_TASKS=64"],
     "ipu1": ["SS_IPU_MAX=1"],
     "ipu2": ["SS_IPU_MAX=2"],
     "ipu8": ["SS_IPU_MAX=8"],
