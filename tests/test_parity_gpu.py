@@ -346,7 +346,7 @@ def test_cuda_graph_capture_and_replay(ss, oracle_lib):
 def test_bench_launch_configuration_c2_sampled(ss, oracle_lib):
     # bench.py's step exactly: all 252 Qwen3-8B matrices through the row-shard
     # driver (world 1: one batched per-tensor-G call, run as the trailing-amax
-    # chain of 8 quantize launches), then sampled rows of
+    # chain of quantize launches), then sampled rows of
     # several tensors (first, middle and last batches) against the oracle.
     from paper_2605_12464_b200.dist import CudaOps, RowShardQuantizer, ShardPlan
     specs = ssgen.workload("c2_qwen3_8b_weights")
@@ -356,8 +356,8 @@ def test_bench_launch_configuration_c2_sampled(ss, oracle_lib):
     outs = [ops.alloc_out(x) for x in xs]
     q = RowShardQuantizer(ShardPlan([(s.rows, s.cols) for s in specs], 0, 1), ops, device="cuda")
     pl = ss.plan([(s.rows, s.cols) for s in specs], fmin=-8, fmax=8, gmode="tensor")
-    assert pl.amax_fused == 1 and pl.trail_batches == 8
-    assert q.step(xs, outs) == pl.launches == 8 * 2  # quantize + sums per batch
+    assert pl.amax_fused == 1 and pl.trail_batches > 1
+    assert q.step(xs, outs) == pl.launches == 2 * pl.trail_batches  # quantize + sums per batch
     # the pipelined variant (8 groups on two streams) gives the same outputs
     codes0 = [outs[k].codes.clone() for k in (0, 127, 251)]
     qp = RowShardQuantizer(ShardPlan([(s.rows, s.cols) for s in specs], 0, 1), ops, device="cuda",

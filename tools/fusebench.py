@@ -25,6 +25,24 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def trail_ends(ns, max_tensors=64):
+    """The library's trailing-amax batches (ss_api.cu trail_batches)."""
+    n_all = sum(ns)
+    lim = max(n_all // 64, 1)
+    ends, i = [], 0
+    while i < len(ns):
+        el = nt = 0
+        while i < len(ns) and nt < max_tensors:
+            if nt > 0 and (el + ns[i] > lim or el + ns[i] > (1 << 36)):
+                break
+            el += ns[i]
+            nt += ns[i] > 0
+            i += 1
+        ends.append(i)
+        lim = 2 * max(el, 1)
+    return ends
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1_gauss4096,c2_qwen3_8b_weights,c4_llama70b_kv")
@@ -77,6 +95,19 @@ def main():
             t_sep = timed(sep)
             t_fused = timed(fused)
             t_search = timed(search) if copies == 1 else None
+            # the search alone in the launch structure of the trailing-amax chain
+            pl = ss.plan([tuple(x.shape) for x in xs], fmin=fmin, fmax=fmax, gmode="tensor")
+            t_search_chain = None
+            if copies == 1 and pl.trail_batches > 1:
+                ends = trail_ends([x.numel() for x in xs])
+
+                def search_chain(s):
+                    i0 = 0
+                    for e in ends:
+                        ss.quantize_batched(s[i0:e], outs_a[i0:e], fmin=fmin, fmax=fmax, gmode="device_amax",
+                                            amax=amax[i0:e])
+                        i0 = e
+                t_search_chain = timed(search_chain)
             sep(xs)
             fused(xs)
             torch.cuda.synchronize()
@@ -86,7 +117,7 @@ def main():
                        if getattr(oa, f) is not None)
             print(json.dumps({"config": cfg, "window": [fmin, fmax], "tensors": len(xs), "elements": n,
                               "variant": a.variant,
-                              "sep_ms": t_sep, "fused_ms": t_fused, "search_only_ms": t_search, "speedup": t_sep / t_fused,
+                              "sep_ms": t_sep, "fused_ms": t_fused, "search_only_ms": t_search, "search_chain_ms": t_search_chain, "speedup": t_sep / t_fused,
                               "sep_gbs": 2 * n / t_sep / 1e6, "fused_gbs": 2 * n / t_fused / 1e6,
                               "bit_identical": bool(same),
                               "status": ss.device_status()}), flush=True)
