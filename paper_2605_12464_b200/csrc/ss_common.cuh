@@ -55,9 +55,7 @@ constexpr int kAmaxWarps = SS_AMAX_WARPS;
 constexpr int kAmaxUnitVecs = SS_AMAX_UNIT;    // 16-B vectors per amax unit (32 KiB)
 constexpr int kAmaxWarpVecs = SS_AMAXW_VECS;  // 16-B loads in flight per lane of an amax warp
 constexpr int kTrailVecs = 256;               // 16-B vectors per trailing-amax unit (4 KiB, 8 per lane)
-#ifndef SS_TRAIL_LOADS
-#define SS_TRAIL_LOADS 4  // trailing-amax loads in flight per lane (a divisor of 8)
-#endif
+
 
 constexpr uint32_t kOneSixthBits = 0x3E2AAAABu;  // RN(1/6) (Alg. 1 line 2; R8)
 constexpr float kGlobalNumer = 2688.0f;          // 6 * 448: largest NVFP4 magnitude (R9)

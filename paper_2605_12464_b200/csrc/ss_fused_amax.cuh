@@ -92,43 +92,52 @@ __device__ __forceinline__ void amax_unit(const QuantBatch& p, uint32_t u, int& 
   v1 = min(A.nvec, v0 + kAmaxUnitVecs);
 }
 
-// Trailing amax (QuantBatch::ntrail).  Trail unit u ->
-// its task (forward walk over am[tr0..nam) from `t`) and vector range [v0, v1).
-__device__ __forceinline__ void trail_unit(const QuantBatch& p, int u, int& t, int64_t& v0, int64_t& v1) {
-  if (t < p.tr0) t = p.tr0;
-  while (t + 1 < p.nam && p.am[t + 1].a0 <= u) t++;
-  const AmaxTask& A = p.am[t];
-  v0 = (int64_t)(u - A.a0) * kTrailVecs;
-  v1 = min(A.nvec, v0 + kTrailVecs);
+// Trailing amax (QuantBatch::ntrail).
+// Publish a warp's per-lane running max m (bf16 |x| pairs) into task t's slot:
+// atomicMax of the FP32 bits, fire-and-forget; NaN sorts above every finite
+// value as in amax_publish (R14).
+__device__ __forceinline__ void trail_publish(const QuantBatch& p, int t, uint32_t m, int lane) {
+  m &= 0x7FFF7FFFu;
+  const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, max(m & 0xFFFFu, m >> 16));
+  if (lane == 0 && r) atomicMax(p.am[t].slot, r << 16);
 }
 // Fold the trail units of scheduling unit su into their tensors' amax slots
-// (the whole warp: 8 coalesced 16-B loads per lane per unit, HMNMX2, one
-// atomicMax of the FP32 bits per unit when larger; NaN sorts above every
-// finite value as in amax_publish, R14).  The loads are not prefetched: an
-// L2 prefetch one work item ahead (per-lane prefetch.global.L2 or a bulk
-// prefetch) measured slower (C2 r = 8: 14.53 vs 14.32 ms per step).
+// (the whole warp: 8 coalesced 16-B loads per lane per 4-KiB unit, HMNMX2; one
+// publish per tensor the units touch).  A full unit loads from one base
+// address with constant offsets; only a tensor's last unit is predicated.
+// The loads are not prefetched: an L2 prefetch one work item ahead (per-lane
+// prefetch.global.L2 or a bulk prefetch) measured slower (C2 r = 8: 14.53 vs
+// 14.32 ms per step).
 __device__ __forceinline__ void trail_fold(const QuantBatch& p, int64_t su, int& t, int lane) {
-  const int64_t u0 = su * p.tpu;
-  for (int k = 0; k < p.tpu && u0 + k < p.ntrail; k++) {
-    int64_t v0, v1;
-    trail_unit(p, (int)(u0 + k), t, v0, v1);
-    const uint4* src = p.am[t].in;
-    uint32_t m = 0;
-#pragma unroll
-    for (int h = 0; h < kTrailVecs / 32; h += SS_TRAIL_LOADS) {  // loads in flight per lane
-      uint4 a[SS_TRAIL_LOADS];
-#pragma unroll
-      for (int j = 0; j < SS_TRAIL_LOADS; j++) {
-        const int64_t v = v0 + lane + 32 * (h + j);
-        a[j] = v < v1 ? __ldcs(src + v) : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll
-      for (int j = 0; j < SS_TRAIL_LOADS; j++) m = hmax_abs_vec(m, a[j]);
+  const int u0 = (int)(su * p.tpu);
+  const int ue = min(u0 + p.tpu, p.ntrail);
+  uint32_t m = 0;
+  for (int u = u0; u < ue; u++) {
+    int tn = t < p.tr0 ? p.tr0 : t;
+    while (tn + 1 < p.nam && p.am[tn + 1].a0 <= u) tn++;
+    if (tn != t) {  // warp-uniform
+      if (t >= p.tr0) trail_publish(p, t, m, lane);
+      m = 0;
+      t = tn;
     }
-    m &= 0x7FFF7FFFu;
-    const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, max(m & 0xFFFFu, m >> 16));
-    if (lane == 0 && r && (r << 16) > ld_relaxed_gpu(p.am[t].slot)) atomicMax(p.am[t].slot, r << 16);
+    const AmaxTask& A = p.am[t];
+    const int64_t v0 = (int64_t)(u - A.a0) * kTrailVecs;
+    const uint4* src = A.in + v0 + lane;
+    const int64_t left = A.nvec - v0;
+    if (left >= kTrailVecs) {  // warp-uniform
+      uint4 a[kTrailVecs / 32];
+#pragma unroll
+      for (int jj = 0; jj < kTrailVecs / 32; jj++) a[jj] = __ldcs(src + 32 * jj);
+#pragma unroll
+      for (int jj = 0; jj < kTrailVecs / 32; jj++) m = hmax_abs_vec(m, a[jj]);
+    } else {
+      const int n = (int)left;
+#pragma unroll
+      for (int jj = 0; jj < kTrailVecs / 32; jj++)
+        if (lane + 32 * jj < n) m = hmax_abs_vec(m, __ldcs(src + 32 * jj));
+    }
   }
+  if (t >= p.tr0 && ue > u0) trail_publish(p, t, m, lane);
 }
 
 // One amax warp: kAmaxWarpVecs coalesced 16-B loads in flight per lane; the next unit is
