@@ -466,7 +466,8 @@ def run_ours(a, rank, world, local_rank):
         try:
             with open(tf) as f:
                 tj = json.load(f)
-            tk = tj["fused" if fused else "plain"]
+            trail = fused and qplan.trail_batches > 1
+            tk = tj["trail" if trail and "trail" in tj else ("fused" if fused else "plain")]
             traffic = tk["dram_bytes_per_elem"] * n_local / qlaunches
             traffic_src = "not measured in this run: DRAM bytes/element of %s scaled to this launch" % (
                 tk.get("source", "profiles/quant_traffic.json"))

@@ -2,7 +2,7 @@
 """One C2 step as the trailing-amax chain (gmode tensor) and the same batches
 searched with precomputed amaxes (gmode device_amax), for an ncu launch list:
 
-    ncu --metrics gpu__time_duration.sum -k regex:quant_kernel --csv python tools/chainprof.py
+    ncu --metrics gpu__time_duration.sum -k regex:quant_kernel --csv python tools/chainprof.py [--chain-only]
 """
 import os
 import sys
@@ -25,6 +25,11 @@ def main():
     amax = ss.tensor_amax_batched(xs)
     ss.quantize_batched(xs, outs, fmin=-8, fmax=8, gmode="tensor")      # the chain
     ends = trail_ends([x.numel() for x in xs])
+    print("elements", sum(x.numel() for x in xs))
+    if "--chain-only" in sys.argv:
+        torch.cuda.synchronize()
+        print("ends", ends)
+        return
     i0 = 0
     for e in ends:                                                        # the same batches, amax given
         ss.quantize_batched(xs[i0:e], outs[i0:e], fmin=-8, fmax=8, gmode="device_amax", amax=amax[i0:e])
