@@ -33,7 +33,8 @@
  *  - candidates that provably cannot win are skipped (exact branch and
  *    bound);
  *  - with SS_GLOBAL_TENSOR the amax pass of a multi-tensor batch runs inside
- *    the quantize launch (§4.2a);
+ *    the quantize launch (§4.2a); a call of >= 2^26 elements runs as a chain
+ *    of launches whose search warps fold the next launch's amax (§4.2c);
  *  - a single small tensor (<= 2^19 blocks) takes a one-thread-per-block
  *    kernel built on the device routine of ss_device.cuh (§4.8);
  *  - FP32 input: ss_quantize_nvfp4_f32; sharded steps:
@@ -245,9 +246,13 @@ typedef struct {
  * tensor's amax inside the quantize launch when the format is NVFP4,
  * the scales are linear, the window has >= 4 offsets and the first tensor
  * holds at most half of the elements (amax warps run ahead of the search;
- * DESIGN.md §4.2a), else in one batched amax launch first.  Results are
- * bit-identical either way and to per-tensor calls; ss_quantize_plan reports
- * which was chosen.
+ * DESIGN.md §4.2a), else in one batched amax launch first.  A call of
+ * >= 2^26 elements then runs as a chain of launches (first batch ~1/64 of the
+ * elements, each later one at most twice its predecessor, <= 64 tensors),
+ * each folding the next batch's amax after its scheduling units (§4.2c);
+ * the launches of one call must not be interleaved with other work on the
+ * inputs.  Results are bit-identical every way and to per-tensor calls;
+ * ss_quantize_plan reports which was chosen.
  */
 SS_API ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min,
                                     int f_max, int global_scale_mode, void* stream);
