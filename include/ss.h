@@ -249,9 +249,8 @@ typedef struct {
  * DESIGN.md §4.2a), else in one batched amax launch first.  A call of
  * >= 2^26 elements then runs as a chain of launches (first batch ~1/64 of the
  * elements, each later one at most twice its predecessor, <= 64 tensors),
- * each folding the next batch's amax after its scheduling units (§4.2c);
- * the launches of one call must not be interleaved with other work on the
- * inputs.  Results are bit-identical every way and to per-tensor calls;
+ * each folding the next batch's amax after its scheduling units (§4.2c).
+ * Results are bit-identical every way and to per-tensor calls;
  * ss_quantize_plan reports which was chosen.
  */
 SS_API ss_status ss_quantize_nvfp4_batched(const ss_tensor_io* tensors, int count, int f_min,
