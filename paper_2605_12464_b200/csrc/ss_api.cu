@@ -629,6 +629,10 @@ std::vector<int> trail_batches(const ss_tensor_io* io, int count) {
     while (i < count && nt < ss::kMaxTensors / 2) {
       const int64_t n = io[i].rows * io[i].cols;
       if (nt > 0 && (el + n > lim || el + n > (int64_t(1) << 36))) break;  // 32-bit unit indices
+      // a later batch's first tensor alone over twice its predecessor: its amax
+      // would be folded by too few search warps (e.g. small tensors, then a huge
+      // one); no trailing amax for this call
+      if (nt == 0 && !bend.empty() && n > lim) return std::vector<int>();
       el += n;
       nt += n > 0;
       i++;
