@@ -109,6 +109,7 @@ __device__ __forceinline__ void trail_publish(const QuantBatch& p, int t, uint32
 // prefetch.global.L2 or a bulk prefetch) measured slower (C2 r = 8: 14.53 vs
 // 14.32 ms per step).
 __device__ __forceinline__ void trail_fold(const QuantBatch& p, int64_t su, int& t, int lane) {
+  if (su * p.tpu >= p.ntrail) return;  // (also keeps u0 within 32 bits)
   const int u0 = (int)(su * p.tpu);
   const int ue = min(u0 + p.tpu, p.ntrail);
   uint32_t m = 0;
