@@ -610,38 +610,45 @@ Plan make_plan(const ss_tensor_io* io, int count, int fmin, int fmax, int gmode,
 }
 
 // Launch batches of a trailing-amax call (§4.2c): exclusive tensor end index
-// per launch.  Batch 0 holds about 1/64 of the elements (its amax is the only
-// one a search waits for); each later batch at most doubles its predecessor's
-// elements (its amax is folded by the predecessor's search warps at up to
-// 4 KiB per 2 KiB work item); at most kMaxTensors / 2 tensors per batch, so a
-// launch's own and next-batch amax tasks fit QuantBatch::am.  A single batch
-// (empty result) means no trailing amax.
-std::vector<int> trail_batches(const ss_tensor_io* io, int count) {
+// per launch, and whether the batch computes its own amax (the amax warps of
+// §4.2a, with per-tensor waits) instead of having it folded by the previous
+// launch.  Batch 0 holds about 1/64 of the elements and computes its own;
+// each later batch at most doubles its predecessor's elements (its amax is
+// folded by the predecessor's search warps at up to 4 KiB per 2 KiB work
+// item), except that a batch whose first tensor alone is larger (small
+// tensors, then a huge one) computes its own too: too few warps would fold
+// it.  At most kMaxTensors / 2 tensors per batch, so a launch's own and
+// next-batch amax tasks fit QuantBatch::am.  Fewer than two batches (empty
+// result) means no trailing amax.
+struct TrailPlan {
+  std::vector<int> end;
+  std::vector<char> self;
+};
+TrailPlan trail_batches(const ss_tensor_io* io, int count) {
   int64_t n_all = 0;
   for (int i = 0; i < count; i++) n_all += io[i].rows * io[i].cols;
-  std::vector<int> bend;
-  if (count < 2 || kTrailMinElems <= 0 || n_all < kTrailMinElems) return bend;
+  TrailPlan tp;
+  if (count < 2 || kTrailMinElems <= 0 || n_all < kTrailMinElems) return tp;
   int64_t lim = std::max<int64_t>(n_all / 64, 1);
   int i = 0;
   while (i < count) {
     int64_t el = 0;
     int nt = 0;
+    bool self = tp.end.empty();
     while (i < count && nt < ss::kMaxTensors / 2) {
       const int64_t n = io[i].rows * io[i].cols;
       if (nt > 0 && (el + n > lim || el + n > (int64_t(1) << 36))) break;  // 32-bit unit indices
-      // a later batch's first tensor alone over twice its predecessor: its amax
-      // would be folded by too few search warps (e.g. small tensors, then a huge
-      // one); no trailing amax for this call
-      if (nt == 0 && !bend.empty() && n > lim) return std::vector<int>();
+      if (nt == 0 && n > lim) self = true;
       el += n;
       nt += n > 0;
       i++;
     }
-    bend.push_back(i);
+    tp.end.push_back(i);
+    tp.self.push_back(self);
     lim = 2 * std::max<int64_t>(el, 1);
   }
-  if (bend.size() < 2) bend.clear();
-  return bend;
+  if (tp.end.size() < 2) tp = TrailPlan();
+  return tp;
 }
 
 ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max, int gmode,
@@ -808,7 +815,8 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
   // own (small) batch's amax with the amax warps, and every launch's search
   // warps also fold the NEXT batch's amax after each scheduling unit, so no
   // later launch waits for an amax and the amax reads spread over the search.
-  const std::vector<int> bend = af_self && !xi ? trail_batches(io, count) : std::vector<int>();
+  const TrailPlan tplan = af_self && !xi ? trail_batches(io, count) : TrailPlan();
+  const std::vector<int>& bend = tplan.end;
   const bool trail = bend.size() > 1;
   size_t launch_idx = 0;
   bool next_done = false;
@@ -842,7 +850,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
     b.done = ws->done;
     bool sums = false;
     int64_t tk = 0, gr = 0, pk = 0;
-    const bool self_amax = af_self && (!trail || launch_idx == 0);
+    const bool self_amax = af_self && (!trail || tplan.self[launch_idx]);
     for (; i < count && b.n < ss::kMaxTensors && (!trail || i < bend[launch_idx]); i++) {
       const ss_tensor_io& t = io[i];
       const int64_t nb = t.rows * t.cols / 16;
@@ -951,7 +959,7 @@ ss_status quantize_core(const ss_tensor_io* io, int count, int f_min, int f_max,
       }
       next_done = true;
     }
-    if (trail && launch_idx + 1 < bend.size()) {  // the next batch's amax, folded by the search warps
+    if (trail && launch_idx + 1 < bend.size() && !tplan.self[launch_idx + 1]) {  // the next batch's amax, folded here
       b.tr0 = b.nam;
       for (int j = bend[launch_idx]; j < bend[launch_idx + 1]; j++) {
         const int64_t nv = 2 * (io[j].rows * io[j].cols / 16);
@@ -1324,7 +1332,7 @@ ss_status ss_quantize_plan(const ss_tensor_io* tensors, int count, int f_min, in
   if (global_scale_mode == SS_GLOBAL_ROW) launches += (plain_rows + per - 1) / per;              // rowscale_kernel
   bool split = false;  // tensors over the piece limit run as row pieces, never with the fused amax
   for (int i = 0; i < count; i++) split |= tensors[i].rows * tensors[i].cols / 16 > kPieceMax;
-  const std::vector<int> bend = pl.af_self && !split ? trail_batches(tensors, count) : std::vector<int>();
+  const std::vector<int> bend = pl.af_self && !split ? trail_batches(tensors, count).end : std::vector<int>();
   if (pl.small >= 0) {
     launches += 1 + (tensors[pl.small].d_err_sums ? 1 : 0);  // quant_small_kernel (+ sums_kernel)
   } else if (bend.size() > 1) {  // trailing amax: one quantize launch (+ sums_kernel) per batch

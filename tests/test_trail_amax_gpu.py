@@ -113,17 +113,32 @@ def test_trail_repeated_calls(ss):
         _same(a, ref)
 
 
-def test_trail_skewed_sizes_fall_back(ss):
+def test_trail_skewed_sizes_self_amax(ss):
     """Small tensors followed by one that alone exceeds twice the batch before
-    it: no trailing-amax chain (its amax would be folded by too few warps);
-    the call still equals the separate path and the oracle's G."""
+    it: that batch computes its own amax (too few warps would fold it) in a
+    2-launch chain; the call equals the separate path and the oracle's G."""
     xs = [ssgen.generate("gaussian", 1, 64, seed=14, tid=i, device="cuda") for i in range(30)]
     xs.append(ssgen.generate("student_t", 16384, 4096, seed=14, tid=99, device="cuda"))
     pl = ss.plan([tuple(x.shape) for x in xs], fmin=-8, fmax=8, gmode="tensor")
-    assert pl.trail_batches == 0
+    assert pl.amax_fused == 1 and pl.trail_batches == 2
     a, fa = _run(ss, xs, -8, 8, fused=True)
     b, fb = _run(ss, xs, -8, 8, fused=False)
     torch.cuda.synchronize()
     assert fa == fb == 0
     _same(a, b)
     assert np.float32(a[30].G.item()) == np.float32(oracle.global_scale(1, oracle.tensor_amax(xs[30].cpu())))
+
+
+def test_trail_self_batch_mid_chain(ss):
+    """A chain whose middle batch starts with a tensor over twice its
+    predecessor: batches before and after it fold, it computes its own amax."""
+    xs = [ssgen.generate("gaussian", 2048, 4096, seed=15, tid=i, device="cuda") for i in range(4)]
+    xs.append(ssgen.generate("student_t", 16384, 4096, seed=15, tid=50, device="cuda"))
+    xs += [ssgen.generate("kv_k", 4096, 4096, seed=15, tid=60 + i, device="cuda") for i in range(6)]
+    pl = ss.plan([tuple(x.shape) for x in xs], fmin=-8, fmax=8, gmode="tensor")
+    assert pl.amax_fused == 1 and pl.trail_batches > 2
+    a, fa = _run(ss, xs, -8, 8, fused=True)
+    b, fb = _run(ss, xs, -8, 8, fused=False)
+    torch.cuda.synchronize()
+    assert fa == fb == 0
+    _same(a, b)

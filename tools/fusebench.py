@@ -35,8 +35,6 @@ def trail_ends(ns, max_tensors=64):
         while i < len(ns) and nt < max_tensors:
             if nt > 0 and (el + ns[i] > lim or el + ns[i] > (1 << 36)):
                 break
-            if nt == 0 and ends and ns[i] > lim:
-                return []
             el += ns[i]
             nt += ns[i] > 0
             i += 1
