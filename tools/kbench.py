@@ -43,6 +43,7 @@ VARIANTS = {
     "seg512": ["SS_SEG_TASKS=512"],
     "corex2": ["SS_CORE_REPEAT=1"],
     "notrail": ["SS_TRAIL_MIN_ELEMS=0"],
+    "bpl1": ["SS_BPL=1"],
     "seg256": ["SS_SEG_TASKS=256"],
     "seg128": ["SS_SEG_TASKS=128"],
     "seg64": ["SS_SEG_TASKS=64"],
