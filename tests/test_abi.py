@@ -135,6 +135,28 @@ def test_device_header_compiles_standalone(tmp_path):
     assert res.returncode == 0, res.stderr
 
 
+def test_quantize_plan_trail(L):
+    """The trailing-amax chain of DESIGN.md §4.2c as ss_quantize_plan reports
+    it: per-tensor-G calls of >= 2^26 elements and >= 2 tensors; batch 0
+    ~1/64 of the elements, each later batch at most twice its predecessor and
+    at most 64 tensors; one quantize (+ error-sum) launch per batch."""
+    import ssgen
+    from paper_2605_12464_b200 import _binding as B
+    specs = ssgen.workload("c2_qwen3_8b_weights")
+    shapes = [(s.rows, s.cols) for s in specs]
+    p = B.plan(shapes, radius=8)
+    assert p.amax_fused == 1 and p.trail_batches == 8 and p.launches == 16
+    assert B.plan(shapes, radius=8, want_sums=False).launches == 8
+    assert B.plan(shapes, radius=8, gmode="device_amax").trail_batches == 0     # amax given
+    assert B.plan(shapes, radius=1).trail_batches == 0                           # HBM-bound window
+    assert B.plan([(4096, 4096)] * 3, radius=8).trail_batches == 0               # < 2^26 elements
+    assert B.plan([(16384, 8192)], radius=8).trail_batches == 0                  # one tensor
+    p = B.plan([(64, 64)] * 300 + [(4096, 4096)] * 4, radius=8)                  # <= 64 tensors per batch
+    assert p.trail_batches >= 300 // 64
+    p = B.plan([(1, 16)] * 30 + [(16384, 4096)], radius=8)                      # huge after tiny: own amax
+    assert p.amax_fused == 1 and p.trail_batches == 2 and p.launches == 4
+
+
 def test_quantize_plan(L):
     """ss_quantize_plan (no device needed): the fused-amax rule (>= 4 offsets,
     first tensor <= half of the batch), the small-tensor path,
