@@ -6,7 +6,9 @@ on the box's host cores (OpenMP over blocks).
     python tools/fullparity.py [--configs c2,c4,c3,c5] [--out FILE]
 
 C2 goes layer by layer (the 7 projections of a layer in one batched
-SS_GLOBAL_TENSOR call: the fused-amax persistent kernel), C4 layer by layer
+SS_GLOBAL_TENSOR call: the fused-amax persistent kernel) or, as `c2all`, in
+the bench's single call over all 252 matrices (the trailing-amax chain of
+DESIGN §4.2c; `c4all` likewise for C4), C4 layer by layer
 (K and V in one call), C3 at several radii (one tensor: the two-launch
 path), C5 1 GiB at r = 8.  Inputs are generated once on the device (ssgen,
 seeded) and copied to the host for the oracle, so both sides see the same
@@ -104,6 +106,12 @@ def main():
     if "c2" in cfgs:
         specs = ssgen.workload("c2_qwen3_8b_weights")
         check("c2_qwen3_8b_weights", specs, [list(range(7 * l, 7 * l + 7)) for l in range(36)], -8, 8)
+    if "c2all" in cfgs:     # the bench's call: all 252 matrices at once (the trailing-amax chain)
+        specs = ssgen.workload("c2_qwen3_8b_weights")
+        check("c2_qwen3_8b_weights_one_call", specs, [list(range(len(specs)))], -8, 8)
+    if "c4all" in cfgs:     # all 160 K/V tensors in one call (the trailing-amax chain)
+        specs = ssgen.workload("c4_llama70b_kv")
+        check("c4_llama70b_kv_one_call", specs, [list(range(len(specs)))], -8, 8)
     if "c4" in cfgs:
         specs = ssgen.workload("c4_llama70b_kv")
         check("c4_llama70b_kv", specs, [[2 * l, 2 * l + 1] for l in range(80)], -8, 8)
