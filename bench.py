@@ -5,8 +5,12 @@ One step = the whole hot path over one batch: for every tensor of the
 workload, the amax pass (a2), the global scale (a3) and the candidate search
 + emit (a4-a7) with radius 8, writing codes, scales and the per-block
 {err_best, err_base}.  Default workload = BASELINE.json configs[1]: the 252
-linear weights of Qwen3-8B (6.95 G bf16 elements, 13.9 GB), rows sharded over
-the ranks when N > 1 with ONE max all-reduce of the 252 shard amaxes (NCCL).
+linear weights of Qwen3-8B (6.95 G bf16 elements, 13.9 GB).  N = 1: one
+per-tensor-G call whose amax runs inside its quantize launches (the
+trailing-amax chain, DESIGN.md §4.2c).  N > 1: rows sharded over the ranks;
+the shard amaxes are exchanged inside the quantize launches over peer memory
+(`--exchange auto`, the default when every rank owns a GPU),
+else by NCCL max all-reduces.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
