@@ -42,7 +42,7 @@ if has fullparity; then
 fi
 if has mrank; then
   # the sharded bench path with 2 ranks sharing the one GPU (gloo carries the amax all-reduce)
-  SS_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 1 --workload c1_gauss4096 --no-cpu-baseline --out gpurun_out/bench_mrank_$TAG.json > gpurun_out/bench_mrank_$TAG.log 2>&1; echo "mrank exit $?" >> gpurun_out/bench_mrank_$TAG.log
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 1 --workload c1_gauss4096 --no-cpu-baseline --dist-backend gloo --out gpurun_out/bench_mrank_$TAG.json > gpurun_out/bench_mrank_$TAG.log 2>&1; echo "mrank exit $?" >> gpurun_out/bench_mrank_$TAG.log
 fi
 if has nccl1; then
   # the NCCL code path at world size 1 (test-only --force-dist)
