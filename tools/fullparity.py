@@ -109,6 +109,9 @@ def main():
     if "c2all" in cfgs:     # the bench's call: all 252 matrices at once (the trailing-amax chain)
         specs = ssgen.workload("c2_qwen3_8b_weights")
         check("c2_qwen3_8b_weights_one_call", specs, [list(range(len(specs)))], -8, 8)
+    if "c2all26" in cfgs:   # the same at the paper's production window [-2, 6]
+        specs = ssgen.workload("c2_qwen3_8b_weights")
+        check("c2_qwen3_8b_weights_one_call", specs, [list(range(len(specs)))], -2, 6)
     if "c4all" in cfgs:     # all 160 K/V tensors in one call (the trailing-amax chain)
         specs = ssgen.workload("c4_llama70b_kv")
         check("c4_llama70b_kv_one_call", specs, [list(range(len(specs)))], -8, 8)
